@@ -1,0 +1,184 @@
+/*
+ * dfm_b200.h — C ABI of the B200-native distributed-FastMNMF EM path.
+ *
+ * Drop-in boundary for the reference's estimator engine
+ * (/root/reference/proj; paths below are relative to it).  The reference has
+ * no FFI of its own; these entry points are the seams its C++ front ends
+ * (fastmnmf.cpp, dist.cpp, wiener.cpp) and pybind module (python/module.cpp)
+ * would bind instead of the Eigen engine:
+ *
+ *   dfm_create / dfm_destroy        engine state of detail::run_engine
+ *                                   (src/engine.cpp:167-190)
+ *   dfm_set_obs                     ObsTensor (include/fastmnmf/types.hpp:44-60)
+ *   dfm_set_model / dfm_get_model   InitBundle {nmf, w0, lambda0}
+ *                                   (include/fastmnmf/init.hpp:69-77) in,
+ *                                   EngineResult (src/engine.hpp:46-51) out
+ *   dfm_fit                         detail::run_engine loop (src/engine.cpp:197-272)
+ *                                   = fit_full (src/fastmnmf.cpp:118-128) and
+ *                                   fit_distributed shared mode (src/dist.cpp:60-67)
+ *   dfm_wiener                      wiener_block / wiener_full (src/wiener.cpp:38-69)
+ *   dfm_comm_init                   (new) frequency sharding, SURVEY.md §8e
+ *   dfm_step_*                      per-update API (src/fastmnmf.cpp:43-116,
+ *                                   src/dist.cpp:20-49)
+ *
+ * Buffer conventions: every buffer is HOST memory owned by the caller, laid
+ * out exactly as the reference's Eigen column-major containers, concatenated:
+ *   x      [F][T][M] complex128 (interleaved re, im) = ObsTensor::bins[i] (M x J)
+ *   Tm     [N][K][F]     NmfModel::T[n]    (I x K col-major)
+ *   V      [N][T][K]     NmfModel::V[n]    (K x J col-major)
+ *   lam    [F][M][N]     Lambda[i]         (N x M col-major)
+ *   w      [B][F][mb*mb] complex128: W_b[i](r, c) at c*mb + r (block-major)
+ *   eta, P [F][M][T]     per-bin J x M col-major
+ *   h      [F][N][T]     per-bin J x N col-major (detail::spectrogram)
+ *   a, b   [N][T][F]     per-source I x J col-major (build_tv_weights)
+ *   images [N][F][T][M]  complex128 (SourceImages::images[n])
+ * A context owns all device memory; layouts are converted once per
+ * set/get, never per iteration.  Contexts are not thread-safe (one per
+ * mixture).  All values are FP64, as in the reference.
+ *
+ * Errors: functions return DFM_OK (0) or a negative code; dfm_last_error()
+ * gives the message.  Codes map onto the reference's exceptions:
+ *   DFM_ERR_SHAPE     -> ShapeMismatch / std::invalid_argument
+ *   DFM_ERR_SINGULAR  -> SingularDemixer (cost functions only; inside a fit a
+ *                        singular demixer records a +inf cost, engine.hpp:41-43)
+ *   DFM_ERR_CUDA, DFM_ERR_NCCL -> std::runtime_error
+ */
+#ifndef DFM_B200_H
+#define DFM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DFM_OK 0
+#define DFM_ERR_SHAPE -1
+#define DFM_ERR_ARG -2
+#define DFM_ERR_SINGULAR -3
+#define DFM_ERR_CUDA -4
+#define DFM_ERR_NCCL -5
+#define DFM_ERR_UNSUPPORTED -6
+
+typedef struct dfm_ctx dfm_ctx;
+
+/* Thread-local message of the last failing call (context-free calls too). */
+const char* dfm_last_error(void);
+/* Compile-time limits: largest block size, number of blocks, sources, bases. */
+int dfm_limits(int* max_mb, int* max_blocks, int* max_n, int* max_k);
+
+/* ----------------------------------------------------------- engine context
+ * Problem dims are GLOBAL (F bins); the context owns bins [f_begin, f_end)
+ * (whole range for a single GPU).  block_sizes: BlockLayout::sizes
+ * (types.hpp:63-88).  floor: FitOptions::floor (model.hpp:95-99). */
+dfm_ctx* dfm_create(int F, int T, int nblocks, const int* block_sizes, int N, int K,
+                    double floor_, int device, int f_begin, int f_end);
+void dfm_destroy(dfm_ctx* ctx);
+int dfm_local_bins(const dfm_ctx* ctx, int* f_begin, int* f_end);
+
+/* x: the context's LOCAL bins [f_end - f_begin][T][M] complex128. */
+int dfm_set_obs(dfm_ctx* ctx, const double* x);
+/* Model arrays are GLOBAL-shaped (all F bins); only the local bins of Tm,
+ * lam and w are read/written, V is shared by every shard. */
+int dfm_set_model(dfm_ctx* ctx, const double* Tm, const double* V, const double* lam,
+                  const double* w);
+int dfm_get_model(dfm_ctx* ctx, double* Tm, double* V, double* lam, double* w);
+
+/* Multi-GPU frequency sharding: one NCCL communicator per context
+ * (nccl_unique_id = the 128-byte ncclUniqueId broadcast by the caller).
+ * The only per-iteration exchange is one allreduce of the V ("H") update
+ * numerator/denominator, 2*N*K*T doubles (engine.cpp:125-133). */
+int dfm_comm_init(dfm_ctx* ctx, const void* nccl_unique_id, int nranks, int rank);
+int dfm_nccl_get_unique_id(void* out128);
+
+/* Runs `iters` EM sweeps on the device-resident state (engine.cpp:197-272).
+ * cost_trace: iters+1 entries (initial cost first, FitReport::cost_trace);
+ * wall_seconds: iters per-iteration device times (may be NULL);
+ * stage_seconds[4] = {w_update, mm_update, eta, decorrelate} (may be NULL;
+ * the fused kernels report the bin kernel under w_update and the
+ * cross-bin V update under mm_update).  Returns the number of IP
+ * pinv fallbacks (>= 0) or an error code.
+ * With a communicator the cost entries are the GLOBAL cost (allreduced). */
+int dfm_fit(dfm_ctx* ctx, int iters, double* cost_trace, double* wall_seconds,
+            double* stage_seconds);
+
+/* Benchmark hooks: one steady-state EM iteration (fused bin kernel in
+ * "finish previous + start next" mode, then the V update), enqueued on the
+ * context stream; dfm_prime runs the first (cost-only) launch.  Device time
+ * of the last dfm_bench_step is returned by dfm_bench_last_ms. */
+int dfm_prime(dfm_ctx* ctx);
+int dfm_bench_step(dfm_ctx* ctx);
+int dfm_sync(dfm_ctx* ctx);
+double dfm_bench_last_ms(dfm_ctx* ctx);
+/* Kernel launches issued by the context so far (for the bench's gpu_launches). */
+long long dfm_launch_count(const dfm_ctx* ctx);
+/* Tuning override for the fused bin kernel: bins per CTA group (G) and
+ * cluster size (CTAs splitting T).  0 = heuristic. */
+int dfm_set_tiling(dfm_ctx* ctx, int bins_per_cta, int cluster_size);
+int dfm_get_tiling(const dfm_ctx* ctx, int* bins_per_cta, int* cluster_size, int* frames_per_cta,
+                   int* threads, int* smem_bytes);
+
+/* Multichannel Wiener separation of the context's local bins with the
+ * current model (wiener_block, wiener.cpp:50-69, shared spectrograms).
+ * images: [N][F_local][T][M] complex128. */
+int dfm_wiener(dfm_ctx* ctx, double* images);
+
+/* ------------------------------------------------- stateless per-update API
+ * Each call uploads its inputs, runs the step kernels once and downloads the
+ * result.  off/mb select a block (ip_update_block / decorrelate_block_into). */
+int dfm_step_spectrogram(int F, int T, int N, int K, const double* Tm, const double* V,
+                         double* h);
+int dfm_step_eta(int F, int T, int N, int M, const double* h, const double* lam, double floor_,
+                 double* eta);
+int dfm_step_decorrelate(int F, int T, int M, const double* x, int off, int mb,
+                         const double* wblk, double* y, double* P);
+/* ip_sweep_column (engine.cpp:30-58): wblk [F][mb*mb] updated in place;
+ * returns the number of pinv fallbacks or an error. */
+int dfm_step_ip_column(int F, int T, int M, const double* x, const double* eta, int off, int mb,
+                       double* wblk, int mu, double floor_);
+int dfm_step_tv_weights(int F, int T, int N, int M, const double* lam, const double* P,
+                        const double* eta, double* a, double* b);
+int dfm_step_update_t(int F, int T, int N, int K, double* Tm, const double* V, const double* a,
+                      const double* b, double floor_);
+int dfm_step_update_v(int F, int T, int N, int K, const double* Tm, double* V, const double* a,
+                      const double* b, double floor_);
+int dfm_step_update_lambda(int F, int T, int N, int M, double* lam, const double* h,
+                           const double* P, const double* eta, double floor_);
+/* power_term (engine.cpp:150-159) and logdet_term (engine.cpp:161-165). */
+int dfm_step_power_term(int F, int T, int N, int M, const double* P, const double* h,
+                        const double* lam, double floor_, double* out);
+int dfm_step_logdet(int F, int mb, const double* wblk, double* out);
+/* Full cost (cost_dist, dist.cpp:20-31 == cost_full for one block);
+ * DFM_ERR_SINGULAR on a singular demixer. */
+int dfm_step_cost(int F, int T, int nblocks, const int* block_sizes, int N, int K,
+                  const double* x, const double* Tm, const double* V, const double* lam,
+                  const double* w, double floor_, double* out);
+/* wiener_block with explicit model (shared spectrograms). */
+int dfm_step_wiener(int F, int T, int nblocks, const int* block_sizes, int N, int K,
+                    const double* x, const double* Tm, const double* V, const double* lam,
+                    const double* w, double floor_, double* images);
+
+/* ------------------------------------------------------- host runtime
+ * The reference's seeded initialisation and synthetic inputs, bit-exact with
+ * its splitmix64 streams (include/fastmnmf/rng.hpp:13-68):
+ *   dfm_random_init         init.cpp:496-521 (NmfModel::random, fastmnmf.cpp:8-24)
+ *   dfm_random_observations bench.cpp:10-20
+ *   dfm_generate_mixture    BASELINE.json configs (kind 0: point sources,
+ *                           kind 1: rank-1 + 0.01 I spatial covariances) */
+uint64_t dfm_derive_seed(uint64_t seed, const char* tag, uint64_t index);
+int dfm_random_init(int F, int T, int nblocks, const int* block_sizes, int N, int K, uint64_t seed,
+                    double* Tm, double* V, double* lam, double* w);
+int dfm_random_observations(int F, int T, int M, uint64_t seed, double* x);
+int dfm_generate_mixture(int kind, int F, int T, int M, int N, int K, uint64_t seed, double* x);
+
+/* ------------------------------------------------------------- probes
+ * FP64 FMA throughput microbenchmark (TFLOP/s, 2 flop per DFMA) and an L2
+ * flush helper (writes a buffer larger than L2 on the current device). */
+double dfm_probe_fp64_tflops(int device);
+int dfm_l2_flush(int device);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

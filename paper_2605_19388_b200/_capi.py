@@ -1,0 +1,128 @@
+"""ctypes binding of the C ABI in include/dfm_b200.h (libdfm_b200.so).
+
+There is no fallback: if the CUDA library is missing or cannot be loaded the
+import fails loudly, and every compute entry point raises when no CUDA
+device is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdfm_b200.so")
+
+_dp = C.POINTER(C.c_double)
+_ip = C.POINTER(C.c_int)
+_vp = C.c_void_p
+_i = C.c_int
+_d = C.c_double
+_u64 = C.c_uint64
+
+# name: (restype, argtypes)
+_SIGS = {
+    "dfm_last_error": (C.c_char_p, []),
+    "dfm_limits": (_i, [_ip, _ip, _ip, _ip]),
+    "dfm_create": (_vp, [_i, _i, _i, _ip, _i, _i, _d, _i, _i, _i]),
+    "dfm_destroy": (None, [_vp]),
+    "dfm_local_bins": (_i, [_vp, _ip, _ip]),
+    "dfm_set_obs": (_i, [_vp, _vp]),
+    "dfm_set_model": (_i, [_vp, _vp, _vp, _vp, _vp]),
+    "dfm_get_model": (_i, [_vp, _vp, _vp, _vp, _vp]),
+    "dfm_comm_init": (_i, [_vp, _vp, _i, _i]),
+    "dfm_nccl_get_unique_id": (_i, [_vp]),
+    "dfm_fit": (_i, [_vp, _i, _vp, _vp, _vp]),
+    "dfm_prime": (_i, [_vp]),
+    "dfm_bench_step": (_i, [_vp]),
+    "dfm_sync": (_i, [_vp]),
+    "dfm_bench_last_ms": (_d, [_vp]),
+    "dfm_launch_count": (C.c_longlong, [_vp]),
+    "dfm_set_tiling": (_i, [_vp, _i, _i]),
+    "dfm_get_tiling": (_i, [_vp, _ip, _ip, _ip, _ip, _ip]),
+    "dfm_wiener": (_i, [_vp, _vp]),
+    "dfm_step_spectrogram": (_i, [_i, _i, _i, _i, _vp, _vp, _vp]),
+    "dfm_step_eta": (_i, [_i, _i, _i, _i, _vp, _vp, _d, _vp]),
+    "dfm_step_decorrelate": (_i, [_i, _i, _i, _vp, _i, _i, _vp, _vp, _vp]),
+    "dfm_step_ip_column": (_i, [_i, _i, _i, _vp, _vp, _i, _i, _vp, _i, _d]),
+    "dfm_step_tv_weights": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp]),
+    "dfm_step_update_t": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _d]),
+    "dfm_step_update_v": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _d]),
+    "dfm_step_update_lambda": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _vp, _d]),
+    "dfm_step_power_term": (_i, [_i, _i, _i, _i, _vp, _vp, _vp, _d, _dp]),
+    "dfm_step_logdet": (_i, [_i, _i, _vp, _dp]),
+    "dfm_step_cost": (_i, [_i, _i, _i, _ip, _i, _i, _vp, _vp, _vp, _vp, _vp, _d, _dp]),
+    "dfm_step_wiener": (_i, [_i, _i, _i, _ip, _i, _i, _vp, _vp, _vp, _vp, _vp, _d, _vp]),
+    "dfm_derive_seed": (_u64, [_u64, C.c_char_p, _u64]),
+    "dfm_random_init": (_i, [_i, _i, _i, _ip, _i, _i, _u64, _vp, _vp, _vp, _vp]),
+    "dfm_random_observations": (_i, [_i, _i, _i, _u64, _vp]),
+    "dfm_generate_mixture": (_i, [_i, _i, _i, _i, _i, _i, _u64, _vp]),
+    "dfm_probe_fp64_tflops": (_d, [_i]),
+    "dfm_l2_flush": (_i, [_i]),
+}
+
+DFM_OK = 0
+DFM_ERR_SHAPE = -1
+DFM_ERR_ARG = -2
+DFM_ERR_SINGULAR = -3
+DFM_ERR_CUDA = -4
+DFM_ERR_NCCL = -5
+DFM_ERR_UNSUPPORTED = -6
+
+
+class ShapeMismatchError(ValueError):
+    """fastmnmf::ShapeMismatch (include/fastmnmf/types.hpp:18-20)."""
+
+
+class SingularDemixerError(RuntimeError):
+    """fastmnmf::SingularDemixer (include/fastmnmf/types.hpp:24-26)."""
+
+
+class NotPositiveDefiniteError(RuntimeError):
+    """fastmnmf::NotPositiveDefinite (include/fastmnmf/types.hpp:21-23)."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA / NCCL failure (std::runtime_error in the reference's terms)."""
+
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(the CUDA engine has no CPU fallback)")
+        lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def last_error() -> str:
+    msg = load().dfm_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(rc: int, what: str = "") -> int:
+    if rc >= 0:
+        return rc
+    msg = f"{what}: {last_error()}" if what else last_error()
+    if rc == DFM_ERR_SHAPE:
+        raise ShapeMismatchError(msg)
+    if rc == DFM_ERR_ARG:
+        raise ValueError(msg)
+    if rc == DFM_ERR_SINGULAR:
+        raise SingularDemixerError(msg)
+    if rc == DFM_ERR_UNSUPPORTED:
+        raise NotImplementedError(msg)
+    raise DeviceError(msg)
+
+
+def exported_symbols():
+    return list(_SIGS)

@@ -1,0 +1,754 @@
+// Step kernels of the FastMNMF EM iteration on sm_100a, one per reference
+// stage (src/engine.cpp:30-165), plus the Wiener separation
+// (src/wiener.cpp:11-69), the stateless per-update C API and the probes.
+//
+// The step kernels work directly on the reference's Eigen column-major
+// layouts (include/dfm_b200.h).  They back the per-update API
+// (ip_update_w / mm_update_* / cost_*; src/fastmnmf.cpp:43-116) and the
+// unfused device engine; the fused hot path lives in dfm_engine.cu.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "dfm_internal.cuh"
+
+namespace dfm {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+bool make_layout(int nb, const int* sizes, Layout& L) {
+  if (nb <= 0 || nb > DFM_MAX_BLOCKS) {
+    set_error("block layout: number of blocks must be in [1, " + std::to_string(DFM_MAX_BLOCKS) + "]");
+    return false;
+  }
+  L.nb = nb;
+  L.M = 0;
+  L.wsz = 0;
+  for (int b = 0; b < nb; ++b) {
+    if (sizes[b] <= 0) {
+      set_error("BlockLayout: block sizes must be positive");
+      return false;
+    }
+    if (sizes[b] > DFM_MAX_MB) {
+      set_error("block size " + std::to_string(sizes[b]) + " exceeds DFM_MAX_MB=" +
+                std::to_string(DFM_MAX_MB));
+      return false;
+    }
+    L.mb[b] = sizes[b];
+    L.off[b] = L.M;
+    L.woff[b] = L.wsz;
+    L.M += sizes[b];
+    L.wsz += sizes[b] * sizes[b];
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------- kernels
+// engine.cpp:71-81  h[i](j, n) = sum_k T[n](i, k) V[n](k, j)
+__global__ void k_spectrogram(int F, int T, int N, int K, const double* __restrict__ Tm,
+                              const double* __restrict__ V, double* __restrict__ h) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)F * N * T) return;
+  const int j = idx % T;
+  const int n = (idx / T) % N;
+  const int i = idx / ((long long)T * N);
+  double s = 0.0;
+  for (int k = 0; k < K; ++k) s += Tm[((size_t)n * K + k) * F + i] * V[((size_t)n * T + j) * K + k];
+  h[idx] = s;
+}
+
+// engine.cpp:83-87  eta = max(h Lambda, floor)
+__global__ void k_eta(int F, int T, int N, int M, const double* __restrict__ h,
+                      const double* __restrict__ lam, double floor_, double* __restrict__ eta) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)F * M * T) return;
+  const int j = idx % T;
+  const int m = (idx / T) % M;
+  const int i = idx / ((long long)T * M);
+  double s = 0.0;
+  for (int n = 0; n < N; ++n) s += h[((size_t)i * N + n) * T + j] * lam[((size_t)i * M + m) * N + n];
+  eta[idx] = fmax(s, floor_);
+}
+
+// engine.cpp:60-69  y = W_b^H x^b, P = |y|^2
+__global__ void k_decorrelate(int F, int T, int M, const cd* __restrict__ x, int off, int mb,
+                              const cd* __restrict__ w, cd* __restrict__ y, double* __restrict__ P) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)F * T) return;
+  const int j = idx % T;
+  const int i = idx / T;
+  const cd* wi = w + (size_t)i * mb * mb;
+  const cd* xj = x + ((size_t)i * T + j) * M + off;
+  for (int mu = 0; mu < mb; ++mu) {
+    cd s{0.0, 0.0};
+    for (int a = 0; a < mb; ++a) s = s + cmulc(wi[mu * mb + a], xj[a]);
+    if (y) y[((size_t)i * T + j) * M + off + mu] = s;
+    if (P) P[((size_t)i * M + off + mu) * T + j] = norm2(s);
+  }
+}
+
+// engine.cpp:30-58  one IP column for every bin: one warp per bin; lanes own
+// entries of Q and accumulate over frames in order, then the warp-level
+// solve of dfm_common.cuh.
+__global__ void __launch_bounds__(32) k_ip_column(int F, int T, int M, const cd* __restrict__ x,
+                                                  const double* __restrict__ eta, int off, int mb,
+                                                  cd* __restrict__ w, int mu, double floor_,
+                                                  int* __restrict__ fallbacks) {
+  __shared__ cd Q[DFM_MAX_MB * DFM_MAX_MB];
+  __shared__ IpScratch<DFM_MAX_MB> scr;
+  const int i = blockIdx.x;
+  const int lane = threadIdx.x;
+  const int n2 = mb * mb;
+  constexpr int PER = (DFM_MAX_MB * DFM_MAX_MB + 31) / 32;
+  cd acc[PER];
+#pragma unroll
+  for (int s = 0; s < PER; ++s) acc[s] = cd{0.0, 0.0};
+  const cd* xi = x + (size_t)i * T * M + off;
+  const double* et = eta + ((size_t)i * M + off + mu) * T;
+  for (int j = 0; j < T; ++j) {
+    const double wj = 1.0 / fmax(et[j], floor_);
+    const cd* xj = xi + (size_t)j * M;
+#pragma unroll
+    for (int s = 0; s < PER; ++s) {
+      const int idx = lane + 32 * s;
+      if (idx < n2) {
+        const int a = idx % mb, c = idx / mb;
+        const cd xa = xj[a] * wj;
+        acc[s] = acc[s] + xa * conjg(xj[c]);
+      }
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < PER; ++s) {
+    const int idx = lane + 32 * s;
+    if (idx < n2) Q[idx] = cdivr(acc[s], (double)T);
+  }
+  __syncwarp();
+  cd* wi = w + (size_t)i * n2;
+  auto qget = [&](int r, int c) { return Q[c * mb + r]; };
+  const int fb = ip_column_warp(mb, wi, mu, qget, floor_, scr);
+  if (lane == 0 && fb) atomicAdd(fallbacks, 1);
+}
+
+// engine.cpp:89-113  a_n = sum_m Lambda(n,m) P eta^-2, b_n = sum_m Lambda(n,m) eta^-1
+__global__ void k_tv_weights(int F, int T, int N, int M, const double* __restrict__ lam,
+                             const double* __restrict__ P, const double* __restrict__ eta,
+                             double* __restrict__ a, double* __restrict__ b) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)F * T) return;
+  const int i = idx % F;  // a/b are [N][T][F]
+  const int j = idx / F;
+  for (int n = 0; n < N; ++n) {
+    double sa = 0.0, sb = 0.0;
+    for (int m = 0; m < M; ++m) {
+      const double ie = 1.0 / eta[((size_t)i * M + m) * T + j];
+      const double z = P[((size_t)i * M + m) * T + j] * ie * ie;
+      const double l = lam[((size_t)i * M + m) * N + n];
+      sa += z * l;
+      sb += ie * l;
+    }
+    a[((size_t)n * T + j) * F + i] = sa;
+    b[((size_t)n * T + j) * F + i] = sb;
+  }
+}
+
+// engine.cpp:115-123
+__global__ void k_update_t(int F, int T, int N, int K, double* __restrict__ Tm,
+                           const double* __restrict__ V, const double* __restrict__ a,
+                           const double* __restrict__ b, double floor_) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)N * K * F) return;
+  const int i = idx % F;
+  const int k = (idx / F) % K;
+  const int n = idx / ((long long)F * K);
+  double num = 0.0, den = 0.0;
+  for (int j = 0; j < T; ++j) {
+    const double v = V[((size_t)n * T + j) * K + k];
+    num += a[((size_t)n * T + j) * F + i] * v;
+    den += b[((size_t)n * T + j) * F + i] * v;
+  }
+  const double t = Tm[idx];
+  Tm[idx] = fmax(t * sqrt(num / fmax(den, floor_)), floor_);
+}
+
+// engine.cpp:125-133 (the cross-bin reduction)
+__global__ void k_update_v(int F, int T, int N, int K, const double* __restrict__ Tm,
+                           double* __restrict__ V, const double* __restrict__ a,
+                           const double* __restrict__ b, double floor_) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)N * T * K) return;
+  const int k = idx % K;
+  const int j = (idx / K) % T;
+  const int n = idx / ((long long)K * T);
+  double num = 0.0, den = 0.0;
+  const double* an = a + ((size_t)n * T + j) * F;
+  const double* bn = b + ((size_t)n * T + j) * F;
+  const double* tn = Tm + ((size_t)n * K + k) * F;
+  for (int i = 0; i < F; ++i) {
+    num += tn[i] * an[i];
+    den += tn[i] * bn[i];
+  }
+  V[idx] = fmax(V[idx] * sqrt(num / fmax(den, floor_)), floor_);
+}
+
+// engine.cpp:135-148
+__global__ void k_update_lambda(int F, int T, int N, int M, double* __restrict__ lam,
+                                const double* __restrict__ h, const double* __restrict__ P,
+                                const double* __restrict__ eta, double floor_) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)F * M * N) return;
+  const int n = idx % N;
+  const int m = (idx / N) % M;
+  const int i = idx / ((long long)N * M);
+  double num = 0.0, den = 0.0;
+  for (int j = 0; j < T; ++j) {
+    const double ie = 1.0 / eta[((size_t)i * M + m) * T + j];
+    const double z = P[((size_t)i * M + m) * T + j] * ie * ie;
+    const double hv = h[((size_t)i * N + n) * T + j];
+    num += hv * z;
+    den += hv * ie;
+  }
+  lam[idx] = fmax(lam[idx] * sqrt(num / fmax(den, floor_)), floor_);
+}
+
+// engine.cpp:150-159 per-bin partial (block tree reduction, fixed order)
+__global__ void __launch_bounds__(256) k_power_term(int F, int T, int N, int M,
+                                                    const double* __restrict__ P,
+                                                    const double* __restrict__ h,
+                                                    const double* __restrict__ lam, double floor_,
+                                                    double* __restrict__ part) {
+  __shared__ double red[256];
+  const int i = blockIdx.x;
+  double acc = 0.0;
+  for (int e = threadIdx.x; e < M * T; e += blockDim.x) {
+    const int m = e / T, j = e % T;
+    double raw = 0.0;
+    for (int n = 0; n < N; ++n) raw += h[((size_t)i * N + n) * T + j] * lam[((size_t)i * M + m) * N + n];
+    acc += P[((size_t)i * M + m) * T + j] / fmax(raw, floor_);
+    acc += log(fmax(raw, 1e-300));
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[i] = red[0];
+}
+
+// engine.cpp:161-165 per bin: 2 ln|det W_i|
+__global__ void k_logdet(int F, int mb, const cd* __restrict__ w, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= F) return;
+  cd lu[DFM_MAX_MB * DFM_MAX_MB];
+  out[i] = 2.0 * log_abs_det_serial(mb, w + (size_t)i * mb * mb, lu);
+}
+
+// (W_b^H)^-1 per (bin, block) for the Wiener filter (wiener.cpp:25): LU of
+// W^H, solved against the identity.  G stored col-major per (f, b).
+__global__ void k_wh_inverse(int F, Layout L, const cd* __restrict__ W, long long wstride,
+                             cd* __restrict__ G) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= F * L.nb) return;
+  const int b = idx % L.nb, f = idx / L.nb;
+  const int mb = L.mb[b];
+  const cd* w = W + (size_t)f * wstride + L.woff[b];
+  cd lu[DFM_MAX_MB * DFM_MAX_MB];
+  int perm[DFM_MAX_MB];
+  for (int c = 0; c < mb; ++c)
+    for (int r = 0; r < mb; ++r) lu[c * mb + r] = conjg(w[r * mb + c]);
+  for (int k = 0; k < mb; ++k) {
+    int piv = k;
+    double best = hypot(lu[k * mb + k].re, lu[k * mb + k].im);
+    for (int r = k + 1; r < mb; ++r) {
+      const double v = hypot(lu[k * mb + r].re, lu[k * mb + r].im);
+      if (v > best) {
+        best = v;
+        piv = r;
+      }
+    }
+    perm[k] = piv;
+    if (best != 0.0) {
+      if (piv != k)
+        for (int c = 0; c < mb; ++c) {
+          const cd t = lu[c * mb + k];
+          lu[c * mb + k] = lu[c * mb + piv];
+          lu[c * mb + piv] = t;
+        }
+      const cd d = lu[k * mb + k];
+      for (int r = k + 1; r < mb; ++r) lu[k * mb + r] = cdiv(lu[k * mb + r], d);
+    }
+    for (int c = k + 1; c < mb; ++c)
+      for (int r = k + 1; r < mb; ++r) lu[c * mb + r] = lu[c * mb + r] - lu[k * mb + r] * lu[c * mb + k];
+  }
+  cd* g = G + (size_t)f * L.wsz + L.woff[b];
+  for (int col = 0; col < mb; ++col) {
+    cd v[DFM_MAX_MB];
+    for (int r = 0; r < mb; ++r) v[r] = cd{r == col ? 1.0 : 0.0, 0.0};
+    for (int k = 0; k < mb; ++k)
+      if (perm[k] != k) {
+        const cd t = v[k];
+        v[k] = v[perm[k]];
+        v[perm[k]] = t;
+      }
+    for (int r = 1; r < mb; ++r)
+      for (int c = 0; c < r; ++c) v[r] = v[r] - lu[c * mb + r] * v[c];
+    for (int r = mb - 1; r >= 0; --r) {
+      for (int c = r + 1; c < mb; ++c) v[r] = v[r] - lu[c * mb + r] * v[c];
+      v[r] = cdiv(v[r], lu[r * mb + r]);
+    }
+    for (int r = 0; r < mb; ++r) g[col * mb + r] = v[r];
+  }
+}
+
+// wiener.cpp:11-34 for every block: c_n = (W^H)^-1 (g_n .* (W^H x)),
+// g_n = h_n Lambda(n, m) / max(h Lambda, floor).  One thread per (bin, frame);
+// HBM-bound (reads x once, writes N images).
+template <int MAXN>
+__global__ void __launch_bounds__(128) k_wiener(int F, int T, int N, int K, Layout L,
+                                                const cd* __restrict__ x, ModelView mv,
+                                                const cd* __restrict__ W, long long wstride,
+                                                const cd* __restrict__ G, double floor_,
+                                                cd* __restrict__ images) {
+  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (idx >= (long long)F * T) return;
+  const int j = idx % T;
+  const int f = idx / T;
+  double h[MAXN];
+#pragma unroll
+  for (int n = 0; n < MAXN; ++n) {
+    double s = 0.0;
+    if (n < N)
+      for (int k = 0; k < K; ++k)
+        s += mv.Tm[n * mv.sTn + f * mv.sTf + k * mv.sTk] * mv.V[n * mv.sVn + k * mv.sVk + j * mv.sVt];
+    h[n] = s;
+  }
+  const cd* xj = x + ((size_t)f * T + j) * L.M;
+  for (int b = 0; b < L.nb; ++b) {
+    const int mb = L.mb[b], off = L.off[b];
+    const cd* wb = W + (size_t)f * wstride + L.woff[b];
+    const cd* gb = G + (size_t)f * L.wsz + L.woff[b];
+    cd y[DFM_MAX_MB];
+    double eta[DFM_MAX_MB];
+    for (int mu = 0; mu < mb; ++mu) {
+      cd s{0.0, 0.0};
+      for (int a = 0; a < mb; ++a) s = s + cmulc(wb[mu * mb + a], xj[off + a]);
+      y[mu] = s;
+      double e = 0.0;
+#pragma unroll
+      for (int n = 0; n < MAXN; ++n)
+        if (n < N) e += h[n] * mv.lam[f * mv.sLf + n * mv.sLn + (off + mu) * mv.sLm];
+      eta[mu] = fmax(e, floor_);
+    }
+#pragma unroll
+    for (int n = 0; n < MAXN; ++n) {
+      if (n >= N) break;
+      cd sc[DFM_MAX_MB];
+      for (int mu = 0; mu < mb; ++mu) {
+        const double gain = (h[n] * mv.lam[f * mv.sLf + n * mv.sLn + (off + mu) * mv.sLm]) / eta[mu];
+        sc[mu] = y[mu] * gain;
+      }
+      cd* out = images + (((size_t)n * F + f) * T + j) * L.M + off;
+      for (int r = 0; r < mb; ++r) {
+        cd s{0.0, 0.0};
+        for (int c = 0; c < mb; ++c) s = s + gb[c * mb + r] * sc[c];
+        out[r] = s;
+      }
+    }
+  }
+}
+
+static inline unsigned nblk(long long n, int b) { return (unsigned)((n + b - 1) / b); }
+
+void launch_wiener(const Layout& L, int F, int T, int N, int K, const cd* x, const ModelView& mv,
+                   const cd* W, long long wstride, double floor_, cd* images, cudaStream_t s,
+                   long long* launches) {
+  DBuf<cd> G((size_t)F * L.wsz);
+  k_wh_inverse<<<nblk((long long)F * L.nb, 128), 128, 0, s>>>(F, L, W, wstride, G.p);
+  DFM_CK_LAUNCH();
+  const unsigned grid = nblk((long long)F * T, 128);
+  if (N <= 8)
+    k_wiener<8><<<grid, 128, 0, s>>>(F, T, N, K, L, x, mv, W, wstride, G.p, floor_, images);
+  else if (N <= 32)
+    k_wiener<32><<<grid, 128, 0, s>>>(F, T, N, K, L, x, mv, W, wstride, G.p, floor_, images);
+  else {
+    set_error("wiener: more than 32 sources is unsupported");
+    throw CudaError{DFM_ERR_UNSUPPORTED};
+  }
+  DFM_CK_LAUNCH();
+  if (launches) *launches += 2;
+  DFM_CK(cudaStreamSynchronize(s));
+}
+
+// ------------------------------------------------------------ probes
+__global__ void k_fp64_probe(double* out, int iters) {
+  double a0 = threadIdx.x * 1e-9, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,
+         a6 = a0 + 6, a7 = a0 + 7;
+  const double m = 0.999999, c = 1e-7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+      a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+    }
+  }
+  const double r = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (r == 12345.678) out[0] = r;
+}
+
+__global__ void k_fill(double* p, size_t n, double v) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+}  // namespace dfm
+
+using namespace dfm;
+
+// ------------------------------------------------------------ C ABI
+#define DFM_API_BEGIN try {
+#define DFM_API_END                                          \
+  }                                                          \
+  catch (const ::dfm::CudaError& e) { return e.code; }       \
+  catch (const std::exception& e) {                          \
+    ::dfm::set_error(e.what());                              \
+    return DFM_ERR_ARG;                                      \
+  }
+
+extern "C" {
+
+const char* dfm_last_error(void) { return g_err.c_str(); }
+
+int dfm_limits(int* max_mb, int* max_blocks, int* max_n, int* max_k) {
+  if (max_mb) *max_mb = DFM_MAX_MB;
+  if (max_blocks) *max_blocks = DFM_MAX_BLOCKS;
+  if (max_n) *max_n = 8;
+  if (max_k) *max_k = 64;
+  return DFM_OK;
+}
+
+static int check_dims(std::initializer_list<int> dims) {
+  for (int d : dims)
+    if (d <= 0) {
+      set_error("dimensions must be positive");
+      return DFM_ERR_SHAPE;
+    }
+  return DFM_OK;
+}
+
+int dfm_step_spectrogram(int F, int T, int N, int K, const double* Tm, const double* V, double* h) {
+  if (int rc = check_dims({F, T, N, K})) return rc;
+  DFM_API_BEGIN
+  DBuf<double> dT((size_t)N * K * F), dV((size_t)N * T * K), dh((size_t)F * N * T);
+  dT.upload(Tm, dT.n);
+  dV.upload(V, dV.n);
+  k_spectrogram<<<nblk(dh.n, 256), 256>>>(F, T, N, K, dT.p, dV.p, dh.p);
+  DFM_CK_LAUNCH();
+  dh.download(h, dh.n);
+  DFM_CK(cudaDeviceSynchronize());
+  return DFM_OK;
+  DFM_API_END
+}
+
+int dfm_step_eta(int F, int T, int N, int M, const double* h, const double* lam, double floor_,
+                 double* eta) {
+  if (int rc = check_dims({F, T, N, M})) return rc;
+  DFM_API_BEGIN
+  DBuf<double> dh((size_t)F * N * T), dl((size_t)F * M * N), de((size_t)F * M * T);
+  dh.upload(h, dh.n);
+  dl.upload(lam, dl.n);
+  k_eta<<<nblk(de.n, 256), 256>>>(F, T, N, M, dh.p, dl.p, floor_, de.p);
+  DFM_CK_LAUNCH();
+  de.download(eta, de.n);
+  DFM_CK(cudaDeviceSynchronize());
+  return DFM_OK;
+  DFM_API_END
+}
+
+int dfm_step_decorrelate(int F, int T, int M, const double* x, int off, int mb, const double* wblk,
+                         double* y, double* P) {
+  if (int rc = check_dims({F, T, M, mb})) return rc;
+  if (off < 0 || off + mb > M || mb > DFM_MAX_MB) {
+    set_error("decorrelate: block out of range");
+    return DFM_ERR_SHAPE;
+  }
+  DFM_API_BEGIN
+  DBuf<cd> dx((size_t)F * T * M), dw((size_t)F * mb * mb), dy(y ? (size_t)F * T * M : 0);
+  DBuf<double> dP(P ? (size_t)F * M * T : 0);
+  dx.upload((const cd*)x, dx.n);
+  dw.upload((const cd*)wblk, dw.n);
+  if (y) dy.upload((const cd*)y, dy.n);
+  if (P) dP.upload(P, dP.n);
+  k_decorrelate<<<nblk((long long)F * T, 256), 256>>>(F, T, M, dx.p, off, mb, dw.p, dy.p, dP.p);
+  DFM_CK_LAUNCH();
+  if (y) dy.download((cd*)y, dy.n);
+  if (P) dP.download(P, dP.n);
+  DFM_CK(cudaDeviceSynchronize());
+  return DFM_OK;
+  DFM_API_END
+}
+
+int dfm_step_ip_column(int F, int T, int M, const double* x, const double* eta, int off, int mb,
+                       double* wblk, int mu, double floor_) {
+  if (int rc = check_dims({F, T, M, mb})) return rc;
+  if (off < 0 || off + mb > M || mb > DFM_MAX_MB || mu < 0 || mu >= mb) {
+    set_error("ip_update_block: (block, mu) out of range");
+    return DFM_ERR_SHAPE;
+  }
+  DFM_API_BEGIN
+  DBuf<cd> dx((size_t)F * T * M), dw((size_t)F * mb * mb);
+  DBuf<double> de((size_t)F * M * T);
+  DBuf<int> dfb(1);
+  dx.upload((const cd*)x, dx.n);
+  de.upload(eta, de.n);
+  dw.upload((const cd*)wblk, dw.n);
+  DFM_CK(cudaMemset(dfb.p, 0, sizeof(int)));
+  k_ip_column<<<F, 32>>>(F, T, M, dx.p, de.p, off, mb, dw.p, mu, floor_, dfb.p);
+  DFM_CK_LAUNCH();
+  int fb = 0;
+  dw.download((cd*)wblk, dw.n);
+  dfb.download(&fb, 1);
+  DFM_CK(cudaDeviceSynchronize());
+  return fb;
+  DFM_API_END
+}
+
+int dfm_step_tv_weights(int F, int T, int N, int M, const double* lam, const double* P,
+                        const double* eta, double* a, double* b) {
+  if (int rc = check_dims({F, T, N, M})) return rc;
+  DFM_API_BEGIN
+  DBuf<double> dl((size_t)F * M * N), dP((size_t)F * M * T), de((size_t)F * M * T);
+  DBuf<double> da((size_t)N * T * F), db((size_t)N * T * F);
+  dl.upload(lam, dl.n);
+  dP.upload(P, dP.n);
+  de.upload(eta, de.n);
+  k_tv_weights<<<nblk((long long)F * T, 256), 256>>>(F, T, N, M, dl.p, dP.p, de.p, da.p, db.p);
+  DFM_CK_LAUNCH();
+  da.download(a, da.n);
+  db.download(b, db.n);
+  DFM_CK(cudaDeviceSynchronize());
+  return DFM_OK;
+  DFM_API_END
+}
+
+int dfm_step_update_t(int F, int T, int N, int K, double* Tm, const double* V, const double* a,
+                      const double* b, double floor_) {
+  if (int rc = check_dims({F, T, N, K})) return rc;
+  DFM_API_BEGIN
+  DBuf<double> dT((size_t)N * K * F), dV((size_t)N * T * K), da((size_t)N * T * F), db((size_t)N * T * F);
+  dT.upload(Tm, dT.n);
+  dV.upload(V, dV.n);
+  da.upload(a, da.n);
+  db.upload(b, db.n);
+  k_update_t<<<nblk(dT.n, 256), 256>>>(F, T, N, K, dT.p, dV.p, da.p, db.p, floor_);
+  DFM_CK_LAUNCH();
+  dT.download(Tm, dT.n);
+  DFM_CK(cudaDeviceSynchronize());
+  return DFM_OK;
+  DFM_API_END
+}
+
+int dfm_step_update_v(int F, int T, int N, int K, const double* Tm, double* V, const double* a,
+                      const double* b, double floor_) {
+  if (int rc = check_dims({F, T, N, K})) return rc;
+  DFM_API_BEGIN
+  DBuf<double> dT((size_t)N * K * F), dV((size_t)N * T * K), da((size_t)N * T * F), db((size_t)N * T * F);
+  dT.upload(Tm, dT.n);
+  dV.upload(V, dV.n);
+  da.upload(a, da.n);
+  db.upload(b, db.n);
+  k_update_v<<<nblk(dV.n, 256), 256>>>(F, T, N, K, dT.p, dV.p, da.p, db.p, floor_);
+  DFM_CK_LAUNCH();
+  dV.download(V, dV.n);
+  DFM_CK(cudaDeviceSynchronize());
+  return DFM_OK;
+  DFM_API_END
+}
+
+int dfm_step_update_lambda(int F, int T, int N, int M, double* lam, const double* h,
+                           const double* P, const double* eta, double floor_) {
+  if (int rc = check_dims({F, T, N, M})) return rc;
+  DFM_API_BEGIN
+  DBuf<double> dl((size_t)F * M * N), dh((size_t)F * N * T), dP((size_t)F * M * T), de((size_t)F * M * T);
+  dl.upload(lam, dl.n);
+  dh.upload(h, dh.n);
+  dP.upload(P, dP.n);
+  de.upload(eta, de.n);
+  k_update_lambda<<<nblk(dl.n, 256), 256>>>(F, T, N, M, dl.p, dh.p, dP.p, de.p, floor_);
+  DFM_CK_LAUNCH();
+  dl.download(lam, dl.n);
+  DFM_CK(cudaDeviceSynchronize());
+  return DFM_OK;
+  DFM_API_END
+}
+
+int dfm_step_power_term(int F, int T, int N, int M, const double* P, const double* h,
+                        const double* lam, double floor_, double* out) {
+  if (int rc = check_dims({F, T, N, M})) return rc;
+  DFM_API_BEGIN
+  DBuf<double> dP((size_t)F * M * T), dh((size_t)F * N * T), dl((size_t)F * M * N), dpart(F);
+  dP.upload(P, dP.n);
+  dh.upload(h, dh.n);
+  dl.upload(lam, dl.n);
+  k_power_term<<<F, 256>>>(F, T, N, M, dP.p, dh.p, dl.p, floor_, dpart.p);
+  DFM_CK_LAUNCH();
+  std::vector<double> part(F);
+  dpart.download(part.data(), F);
+  DFM_CK(cudaDeviceSynchronize());
+  double s = 0.0;
+  for (int i = 0; i < F; ++i) s += part[i];
+  *out = s;
+  return DFM_OK;
+  DFM_API_END
+}
+
+int dfm_step_logdet(int F, int mb, const double* wblk, double* out) {
+  if (int rc = check_dims({F, mb})) return rc;
+  if (mb > DFM_MAX_MB) {
+    set_error("logdet: block too large");
+    return DFM_ERR_SHAPE;
+  }
+  DFM_API_BEGIN
+  DBuf<cd> dw((size_t)F * mb * mb);
+  DBuf<double> dout(F);
+  dw.upload((const cd*)wblk, dw.n);
+  k_logdet<<<nblk(F, 64), 64>>>(F, mb, dw.p, dout.p);
+  DFM_CK_LAUNCH();
+  std::vector<double> v(F);
+  dout.download(v.data(), F);
+  DFM_CK(cudaDeviceSynchronize());
+  double s = 0.0;
+  for (int i = 0; i < F; ++i) s += v[i];
+  *out = s;
+  return DFM_OK;
+  DFM_API_END
+}
+
+int dfm_step_cost(int F, int T, int nblocks, const int* block_sizes, int N, int K, const double* x,
+                  const double* Tm, const double* V, const double* lam, const double* w,
+                  double floor_, double* out) {
+  Layout L;
+  if (!make_layout(nblocks, block_sizes, L)) return DFM_ERR_SHAPE;
+  if (int rc = check_dims({F, T, N, K})) return rc;
+  const int M = L.M;
+  DFM_API_BEGIN
+  DBuf<cd> dx((size_t)F * T * M), dw((size_t)F * L.wsz);
+  DBuf<double> dT((size_t)N * K * F), dV((size_t)N * T * K), dl((size_t)F * M * N);
+  DBuf<double> dh((size_t)F * N * T), dP((size_t)F * M * T), dpart(F), dld(F);
+  dx.upload((const cd*)x, dx.n);
+  dw.upload((const cd*)w, dw.n);
+  dT.upload(Tm, dT.n);
+  dV.upload(V, dV.n);
+  dl.upload(lam, dl.n);
+  double det = 0.0;
+  size_t wo = 0;
+  std::vector<double> v(F);
+  for (int b = 0; b < L.nb; ++b) {
+    const int mb = L.mb[b];
+    k_decorrelate<<<nblk((long long)F * T, 256), 256>>>(F, T, M, dx.p, L.off[b], mb, dw.p + wo, nullptr, dP.p);
+    DFM_CK_LAUNCH();
+    k_logdet<<<nblk(F, 64), 64>>>(F, mb, dw.p + wo, dld.p);
+    DFM_CK_LAUNCH();
+    dld.download(v.data(), F);
+    DFM_CK(cudaDeviceSynchronize());
+    for (int i = 0; i < F; ++i) det += v[i];
+    wo += (size_t)F * mb * mb;
+  }
+  k_spectrogram<<<nblk(dh.n, 256), 256>>>(F, T, N, K, dT.p, dV.p, dh.p);
+  DFM_CK_LAUNCH();
+  k_power_term<<<F, 256>>>(F, T, N, M, dP.p, dh.p, dl.p, floor_, dpart.p);
+  DFM_CK_LAUNCH();
+  dpart.download(v.data(), F);
+  DFM_CK(cudaDeviceSynchronize());
+  double pw = 0.0;
+  for (int i = 0; i < F; ++i) pw += v[i];
+  if (!std::isfinite(det)) {
+    set_error("cost_dist: singular demixing matrix");
+    return DFM_ERR_SINGULAR;
+  }
+  *out = pw - (double)T * det;
+  return DFM_OK;
+  DFM_API_END
+}
+
+int dfm_step_wiener(int F, int T, int nblocks, const int* block_sizes, int N, int K,
+                    const double* x, const double* Tm, const double* V, const double* lam,
+                    const double* w, double floor_, double* images) {
+  Layout L;
+  if (!make_layout(nblocks, block_sizes, L)) return DFM_ERR_SHAPE;
+  if (int rc = check_dims({F, T, N, K})) return rc;
+  const int M = L.M;
+  DFM_API_BEGIN
+  DBuf<cd> dx((size_t)F * T * M), dw((size_t)F * L.wsz), dimg((size_t)N * F * T * M);
+  DBuf<double> dT((size_t)N * K * F), dV((size_t)N * T * K), dl((size_t)F * M * N);
+  dx.upload((const cd*)x, dx.n);
+  dT.upload(Tm, dT.n);
+  dV.upload(V, dV.n);
+  dl.upload(lam, dl.n);
+  // block-major [B][F][mb^2] -> bin-major [F][wsz]
+  {
+    std::vector<cd> wbin((size_t)F * L.wsz);
+    const cd* src = (const cd*)w;
+    for (int b = 0; b < L.nb; ++b) {
+      const int n2 = L.mb[b] * L.mb[b];
+      for (int f = 0; f < F; ++f)
+        std::memcpy(&wbin[(size_t)f * L.wsz + L.woff[b]], src + (size_t)F * L.woff[b] + (size_t)f * n2,
+                    sizeof(cd) * n2);
+    }
+    dw.upload(wbin.data(), wbin.size());
+    DFM_CK(cudaDeviceSynchronize());
+  }
+  ModelView mv{dT.p, (long long)K * F, 1, F, dV.p, (long long)T * K, 1, K, dl.p, (long long)M * N, 1, N};
+  launch_wiener(L, F, T, N, K, dx.p, mv, dw.p, L.wsz, floor_, dimg.p, 0, nullptr);
+  dimg.download((cd*)images, dimg.n);
+  DFM_CK(cudaDeviceSynchronize());
+  return DFM_OK;
+  DFM_API_END
+}
+
+double dfm_probe_fp64_tflops(int device) {
+  try {
+    DFM_CK(cudaSetDevice(device));
+    int sms = 0;
+    DFM_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    DBuf<double> out(1);
+    const int iters = 4096, threads = 512, blocks = sms * 4;
+    k_fp64_probe<<<blocks, threads>>>(out.p, 16);
+    DFM_CK_LAUNCH();
+    cudaEvent_t e0, e1;
+    DFM_CK(cudaEventCreate(&e0));
+    DFM_CK(cudaEventCreate(&e1));
+    DFM_CK(cudaEventRecord(e0));
+    k_fp64_probe<<<blocks, threads>>>(out.p, iters);
+    DFM_CK(cudaEventRecord(e1));
+    DFM_CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    DFM_CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const double flops = 2.0 * 8 * 16 * (double)iters * threads * blocks;
+    return flops / (ms * 1e-3) / 1e12;
+  } catch (...) {
+    return -1.0;
+  }
+}
+
+int dfm_l2_flush(int device) {
+  DFM_API_BEGIN
+  static thread_local DBuf<double>* buf = nullptr;
+  DFM_CK(cudaSetDevice(device));
+  if (!buf) {
+    buf = new DBuf<double>();
+    buf->alloc((size_t)48 << 20);  // 384 MB > 126 MB L2
+  }
+  k_fill<<<1184, 256>>>(buf->p, buf->n, 1.0);
+  DFM_CK_LAUNCH();
+  return DFM_OK;
+  DFM_API_END
+}
+
+}  // extern "C"
