@@ -1,0 +1,405 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native distributed-FastMNMF EM iteration.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                  [--workload config1|config0|config2|config3] [--e2e-iters I]
+
+A *step* is one steady-state EM iteration of BASELINE.json's config 1
+(B=3 subarrays x M_b=4 mics, N=5 sources, F=513 bins, T=626 frames, K=16):
+the fused bin kernel (finishes iteration i-1: Lambda update + cost; starts
+iteration i: IP sweep, decorrelation, T update, V-update weights) followed by
+the cross-bin V update.  Inputs are resident in HBM; X (61.7 MB) fits in the
+126 MB L2, so L2 is FLUSHED (384 MB write, untimed) before every timed step.
+Timing: CUDA events on the engine stream, summed over exactly K steps,
+barrier + synchronize on both sides, max over ranks.
+
+N > 1 (torchrun): frequency bins sharded over the ranks, one NCCL allreduce of
+the V-update numerator/denominator per iteration (strong scaling).
+
+--impl reference: the reference's CPU algorithm (oracle/ restatement; the
+reference itself needs Eigen, absent here) on all host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "config0": dict(kind=0, F=257, T=200, sizes=[2, 2], N=3, K=4, iters=50),
+    "config1": dict(kind=1, F=513, T=626, sizes=[4, 4, 4], N=5, K=16, iters=200),
+    "config2": dict(kind=1, F=513, T=626, sizes=[12], N=5, K=16, iters=200),
+    "config3": dict(kind=1, F=1025, T=2000, sizes=[4] * 8, N=8, K=32, iters=100),
+}
+SEED_X, SEED_INIT = 2605, 19388
+PAPER_CPU_TFBIN = 266.5e3  # BASELINE.md derived paper figure (other config/hardware), context only
+
+
+def alg_bytes(c) -> float:
+    """SURVEY.md §8(d) compulsory bytes per EM iteration."""
+    F, T, N, K, M = c["F"], c["T"], c["N"], c["K"], sum(c["sizes"])
+    S2 = sum(s * s for s in c["sizes"])
+    return 16.0 * F * T * M + 2 * 8.0 * (F * K * N + K * T * N + F * N * M) + 2 * 16.0 * F * S2 + 32.0 * N * K * T
+
+
+def alg_bytes_bin_kernel(c) -> float:
+    """Compulsory bytes of the fused bin kernel alone: X once, T/Lambda/W read
+    and written, V read (the V update's own traffic excluded)."""
+    F, T, N, K, M = c["F"], c["T"], c["N"], c["K"], sum(c["sizes"])
+    S2 = sum(s * s for s in c["sizes"])
+    return 16.0 * F * T * M + 8.0 * (2 * F * K * N + K * T * N + 2 * F * N * M) + 32.0 * F * S2
+
+
+def alg_flops(c) -> float:
+    """SURVEY.md §8(d) algorithmic flops per EM iteration (FMA = 2)."""
+    F, T, N, K, M = c["F"], c["T"], c["N"], c["K"], sum(c["sizes"])
+    S2 = sum(s * s for s in c["sizes"])
+    FTM = F * T * M
+    f = F * T * sum(2 * m ** 3 + 5 * m ** 2 + 3 * m for m in c["sizes"])
+    f += F * sum(m * (32.0 / 3 * m ** 3 + 24 * m ** 2) for m in c["sizes"])
+    f += 8.0 * F * T * S2 + 3 * FTM
+    f += 2.0 * F * T * (4 * N * M + 3 * M)
+    f += 8.0 * N * F * K * T
+    f += 4.0 * N * F * T * K
+    f += 3 * (2.0 * F * T * N * M + FTM)
+    f += 4.0 * F * T * N * M + 3 * FTM
+    f += 4.0 * FTM
+    return f
+
+
+def peaks():
+    p = dict(hbm_gbs=6540.5, source="fallback (MEASURED_PEAKS.json absent)")
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            j = json.load(fh)
+        p = dict(hbm_gbs=float(j["hbm_gbs"]), source="measured (MEASURED_PEAKS.json)")
+    return p
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons via NVML during the timed region."""
+
+    def __init__(self, device: int, period_s: float = 0.02):
+        self.device, self.period, self.samples, self.reasons = device, period_s, [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            names = {
+                getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8): "hw_slowdown",
+                getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40): "hw_thermal_slowdown",
+                getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20): "sw_thermal_slowdown",
+                getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4): "sw_power_cap",
+                getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80): "hw_power_brake",
+            }
+
+            def run():
+                while not self._stop.is_set():
+                    try:
+                        self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        for bit, name in names.items():
+                            if r & bit:
+                                self.reasons.add(name)
+                    except Exception:
+                        pass
+                    time.sleep(self.period)
+
+            self._t = threading.Thread(target=run, daemon=True)
+            self._t.start()
+        except Exception as e:  # NVML unavailable: record why
+            self.reasons.add(f"nvml_unavailable:{type(e).__name__}")
+        return self
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=1)
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def shard(F: int, world: int, rank: int):
+    base, rem = divmod(F, world)
+    f0 = rank * base + min(rank, rem)
+    return f0, f0 + base + (1 if rank < rem else 0)
+
+
+def cpu_baseline(c, x, init_d, threads: int, target_s: float = 15.0):
+    """The oracle (C restatement of engine.cpp) timed on host cores over a
+    bounded sample of the workload: the first Fs bins, a few EM iterations."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+
+    oracle.build()
+    oracle.set_threads(threads)
+    F, T = c["F"], c["T"]
+    # probe the per-bin cost on a small slice, then size the sample
+    Fp = min(F, 16)
+    sub = lambda Fs: dict(T=np.ascontiguousarray(init_d["T"][:, :Fs]), V=init_d["V"],
+                          lam=np.ascontiguousarray(init_d["lam"][:Fs]),
+                          w=[np.ascontiguousarray(w[:Fs]) for w in init_d["w"]])
+    r = oracle.run_engine(np.ascontiguousarray(x[:Fp]), c["sizes"], sub(Fp), 2)
+    per_bin_iter = max(float(np.mean(r["wall_seconds"])) / Fp, 1e-9)
+    iters = 3
+    Fs = int(max(Fp, min(F, target_s / (iters * per_bin_iter))))
+    r = oracle.run_engine(np.ascontiguousarray(x[:Fs]), c["sizes"], sub(Fs), iters)
+    t_iter = float(np.mean(r["wall_seconds"][1:]))  # first timed iteration treated as warm-up
+    return dict(value=Fs * T / t_iter, unit="TF-bin*iter/s", cores=threads, kind="port",
+                sample=f"oracle/ run_engine on the first {Fs} of {F} bins x {T} frames, {iters} EM iters "
+                       f"(mean of iters 2..{iters}; {t_iter:.3f} s/iter)",
+                seconds_per_iter_full=t_iter * F / Fs)
+
+
+def run_reference(args, c, world, rank):
+    """--impl reference: the reference's CPU algorithm on all host threads."""
+    if rank != 0:
+        return None
+    import paper_2605_19388_b200 as dfm
+
+    layout = dfm.BlockLayout(c["sizes"])
+    x = dfm.generate_mixture(c["kind"], c["F"], c["T"], layout.total, c["N"], c["K"], SEED_X)
+    init = dfm.random_init(c["F"], c["T"], layout, c["N"], c["K"], SEED_INIT)
+    init_d = dict(T=init.nmf.T, V=init.nmf.V, lam=init.lambda0, w=init.w0)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle
+
+    oracle.build()
+    threads = os.cpu_count() or 1
+    oracle.set_threads(threads)
+    F, T = c["F"], c["T"]
+    Fp = min(F, 32)
+    sub = lambda Fs: dict(T=np.ascontiguousarray(init_d["T"][:, :Fs]), V=init_d["V"],
+                          lam=np.ascontiguousarray(init_d["lam"][:Fs]),
+                          w=[np.ascontiguousarray(w[:Fs]) for w in init_d["w"]])
+    r = oracle.run_engine(np.ascontiguousarray(x[:Fp]), c["sizes"], sub(Fp), 2)
+    per_bin_iter = max(float(np.mean(r["wall_seconds"])) / Fp, 1e-9)
+    total_iters = args.warmup + args.steps
+    Fs = int(max(8, min(F, 150.0 / (total_iters * per_bin_iter))))
+    r = oracle.run_engine(np.ascontiguousarray(x[:Fs]), c["sizes"], sub(Fs), total_iters)
+    timed = r["wall_seconds"][args.warmup:]
+    total = float(np.sum(timed))
+    value = Fs * T * args.steps / total
+    sample = (f"oracle/ C restatement of engine.cpp (reference needs Eigen3, unbuildable here) on the first "
+              f"{Fs} of {F} bins x {T} frames per step, OpenMP over bins")
+    return {
+        "metric": "dFastMNMF EM TF-bin*iter/s (BASELINE config 1)", "value": value, "unit": "TF-bin*iter/s",
+        "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, **{k: c[k] for k in ("F", "T", "sizes", "N", "K")}},
+        "cpu_baseline": {"value": value, "unit": "TF-bin*iter/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "TF-bin*iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "iter_per_s_full_config": value / (F * T),
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="config1", choices=sorted(CONFIGS))
+    ap.add_argument("--e2e-iters", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tiling", default="", help="G,CS override of the bin-kernel tiling")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    c = CONFIGS[args.workload]
+    world, rank, local = dist_setup()
+
+    if args.impl == "reference":
+        line = run_reference(args, c, world, rank)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+    import paper_2605_19388_b200 as dfm
+
+    lib = dfm._capi.load()
+    layout = dfm.BlockLayout(c["sizes"])
+    F, T, N, K, M = c["F"], c["T"], c["N"], c["K"], layout.total
+    x = dfm.generate_mixture(c["kind"], F, T, M, N, K, SEED_X)
+    init = dfm.random_init(F, T, layout, N, K, SEED_INIT)
+    f0, f1 = shard(F, world, rank)
+
+    eng = dfm.Engine(F, T, layout, N, K, device=local, f_begin=f0, f_end=f1)
+    if args.tiling:
+        g, cs = (int(v) for v in args.tiling.split(","))
+        eng.set_tiling(g, cs)
+    if world > 1:
+        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            import ctypes
+
+            buf = ctypes.create_string_buffer(128)
+            dfm._capi.check(lib.dfm_nccl_get_unique_id(buf))
+            uid.copy_(torch.frombuffer(bytearray(buf.raw), dtype=torch.uint8))
+        pg.broadcast(uid, 0)
+        eng.comm_init(bytes(uid.cpu().numpy().tobytes()), world, rank)
+    eng.set_obs(np.ascontiguousarray(x[f0:f1]))
+    eng.set_model(init.nmf, init.w0, init.lambda0)
+    ctx = eng.ctx
+
+    def step():
+        dfm._capi.check(lib.dfm_l2_flush(local))  # untimed: outside the step's events
+        dfm._capi.check(lib.dfm_bench_step(ctx))
+        ms = lib.dfm_bench_last_ms(ctx)
+        import ctypes
+
+        a, b = ctypes.c_double(), ctypes.c_double()
+        lib.dfm_bench_last_split(ctx, ctypes.byref(a), ctypes.byref(b))
+        return ms, a.value, b.value
+
+    dfm._capi.check(lib.dfm_prime(ctx))
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize()
+    launches0 = eng.launches()
+    sampler = ClockSampler(local).start()
+    t_ms, bin_ms, v_ms = [], [], []
+    for _ in range(args.steps):
+        ms, a, b = step()
+        t_ms.append(ms)
+        bin_ms.append(a)
+        v_ms.append(b)
+    dfm._capi.check(lib.dfm_sync(ctx))
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    launches = eng.launches() - launches0
+    total_ms = float(np.sum(t_ms))
+    if pg:
+        tt = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        pg.all_reduce(tt, op=pg.ReduceOp.MAX)
+        total_ms = float(tt.item())
+        pg.barrier()
+    torch.cuda.synchronize()
+    ms_step = total_ms / args.steps
+    value = F * T * args.steps / (total_ms * 1e-3)
+
+    # ---------------------------------------------------------------- e2e
+    # one user call through the public API per e2e step: pinned host X +
+    # init in (H2D), e2e_iters EM sweeps, cost trace + fitted model out (D2H)
+    xs = torch.from_numpy(np.ascontiguousarray(x[f0:f1])).pin_memory().numpy()
+    h2d = xs.nbytes + (init.nmf.T.nbytes + init.nmf.V.nbytes + init.lambda0.nbytes
+                       + sum(w.nbytes for w in init.w0)) * (f1 - f0) // F
+    e2e_times = []
+    for rep in range(3):
+        if pg:
+            pg.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        eng.set_obs(xs)
+        eng.set_model(init.nmf, init.w0, init.lambda0)
+        eng.fit(args.e2e_iters)  # cost trace D2H (allreduced across ranks when sharded)
+        eng.get_model()
+        dt = time.perf_counter() - t0
+        if pg:
+            tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            pg.all_reduce(tt, op=pg.ReduceOp.MAX)
+            dt = float(tt.item())
+        e2e_times.append(dt)
+    e2e_dt = min(e2e_times)
+    d2h = (init.nmf.T.nbytes + init.nmf.V.nbytes + init.lambda0.nbytes
+           + sum(w.nbytes for w in init.w0)) * (f1 - f0) // F + 8 * (args.e2e_iters + 1)
+    e2e_value = F * T * args.e2e_iters / e2e_dt
+
+    if rank != 0:
+        if pg:
+            pg.destroy_process_group()
+        return
+
+    pk = peaks()
+    bin_avg = float(np.mean(bin_ms))
+    ab_bin = alg_bytes_bin_kernel(c) * (f1 - f0) / F
+    achieved = ab_bin / (bin_avg * 1e-3) / 1e9
+    fp64_peak = float(lib.dfm_probe_fp64_tflops(local))
+    fl = alg_flops(c) / (ms_step * 1e-3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as fh:
+                traffic = json.load(fh).get(args.workload, {}).get("k_bin_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": "dFastMNMF EM TF-bin*iter/s (BASELINE config 1)",
+        "value": value, "unit": "TF-bin*iter/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded STFT-domain mixture, BASELINE config generator)",
+        "config": {"workload": args.workload, "F": F, "T": T, "sizes": c["sizes"], "N": N, "K": K,
+                   "l2": "flushed before every timed step (384 MB write, untimed)",
+                   "parallelism": f"freq-shard x{world}" if world > 1 else "1 GPU",
+                   "tiling": eng.tiling()},
+        "iter_per_s": 1e3 / ms_step,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "kernel": "k_bin",
+                     "alg_bytes_per_launch": ab_bin, "kernel_ms": bin_avg, "peak_source": pk["source"]},
+        "roofline_fp64": {"bound": "fp64", "achieved": fl, "peak": fp64_peak, "unit": "TFLOP/s",
+                          "frac": fl / fp64_peak if fp64_peak > 0 else None,
+                          "alg_flops_per_iter": alg_flops(c),
+                          "peak_source": "measured in this run (DFMA microbenchmark, dfm_probe_fp64_tflops)"},
+        "iteration_roofline": {"alg_bytes_per_iter": alg_bytes(c), "hbm_frac": alg_bytes(c) / (ms_step * 1e-3) / 1e9 / pk["hbm_gbs"]},
+        "kernel_split_ms": {"k_bin": bin_avg, "v_update": float(np.mean(v_ms))},
+        "e2e": {"value": e2e_value, "unit": "TF-bin*iter/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h),
+                "step": f"Engine.set_obs/set_model (pinned host X + init H2D), Engine.fit({args.e2e_iters}) "
+                        "(cost trace D2H), Engine.get_model (model D2H); best of 3",
+                "seconds_per_step": e2e_dt},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "paper_cpu_tfbin_iter_per_s_other_config": PAPER_CPU_TFBIN,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        init_d = dict(T=init.nmf.T, V=init.nmf.V, lam=init.lambda0, w=init.w0)
+        line["cpu_baseline"] = cpu_baseline(c, x, init_d, threads=1)
+        mt = os.cpu_count() or 1
+        line["cpu_baseline_all_cores"] = cpu_baseline(c, x, init_d, threads=mt)
+    print(json.dumps(line), flush=True)
+    eng.close()
+    if pg:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

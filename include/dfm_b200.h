@@ -111,6 +111,8 @@ int dfm_prime(dfm_ctx* ctx);
 int dfm_bench_step(dfm_ctx* ctx);
 int dfm_sync(dfm_ctx* ctx);
 double dfm_bench_last_ms(dfm_ctx* ctx);
+/* Split of the last dfm_bench_step: fused bin kernel vs V update (+ allreduce). */
+int dfm_bench_last_split(dfm_ctx* ctx, double* bin_ms, double* vupd_ms);
 /* Kernel launches issued by the context so far (for the bench's gpu_launches). */
 long long dfm_launch_count(const dfm_ctx* ctx);
 /* Tuning override for the fused bin kernel: bins per CTA group (G) and

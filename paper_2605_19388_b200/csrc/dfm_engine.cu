@@ -594,7 +594,7 @@ struct dfm_ctx {
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
   long long launches = 0;
-  cudaEvent_t eb0 = nullptr, eb1 = nullptr;
+  cudaEvent_t eb0 = nullptr, eb1 = nullptr, ebm = nullptr;
   bool has_obs = false, has_model = false;
   std::vector<cudaEvent_t> iter_ev;
 };
@@ -664,7 +664,7 @@ size_t smem_for(dfm_ctx* c, int G, int CS, int& Ts, int& Tsp, int& threads) {
 // Tiling heuristic: keep each CTA's frame slice resident (<= ~113 KB so two
 // clusters' CTAs share an SM), prefer more bins per group (V reuse) and
 // enough CTAs to fill 148 SMs twice.
-void choose_tiling(dfm_ctx* c) {
+bool choose_tiling(dfm_ctx* c) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   struct Cand {
@@ -681,7 +681,6 @@ void choose_tiling(dfm_ctx* c) {
       int Ts, Tsp, thr;
       const size_t sm = smem_for(c, G, CS, Ts, Tsp, thr);
       if (sm > 227 * 1024) continue;
-      if ((c->T + Ts - 1) / Ts < CS) continue;  // empty ranks
       const int ngroups = (c->F + G - 1) / G;
       const double ctas = (double)ngroups * CS;
       const int per_sm = std::max(1, (int)((228 * 1024) / (sm + 1024)));
@@ -694,10 +693,15 @@ void choose_tiling(dfm_ctx* c) {
       score += std::min(1.0, (double)(G * Ts) / 256.0);   // busy threads
       if (score > best.score) best = Cand{G, CS, sm, score};
     }
+  if (best.score == -1e30) {
+    set_error("no feasible tiling (shared memory exceeds 227 KB per CTA)");
+    return false;
+  }
   c->G = best.G;
   c->CS = best.CS;
   c->smem = (int)smem_for(c, c->G, c->CS, c->Ts, c->Tsp, c->threads);
   c->ngroups = (c->F + c->G - 1) / c->G;
+  return true;
 }
 
 void launch_bin(dfm_ctx* c, int finish, int start, int slot) {
@@ -806,6 +810,7 @@ dfm_ctx* dfm_create(int F, int T, int nblocks, const int* block_sizes, int N, in
     DFM_CK(cudaStreamCreate(&c->stream));
     DFM_CK(cudaEventCreate(&c->eb0));
     DFM_CK(cudaEventCreate(&c->eb1));
+    DFM_CK(cudaEventCreate(&c->ebm));
     c->x.alloc((size_t)c->F * T * c->M);
     c->W.alloc((size_t)c->F * L.wsz);
     c->Tf.alloc((size_t)c->F * N * K);
@@ -816,7 +821,7 @@ dfm_ctx* dfm_create(int F, int T, int nblocks, const int* block_sizes, int N, in
     c->numden.alloc(2 * (size_t)N * K * T);
     c->fallbacks.alloc(1);
     DFM_CK(cudaMemset(c->fallbacks.p, 0, sizeof(int)));
-    choose_tiling(c);
+    if (!choose_tiling(c)) throw CudaError{DFM_ERR_UNSUPPORTED};
     set_kernel_attrs(c);
     ensure_cost(c, 2);
   } catch (const CudaError&) {
@@ -833,6 +838,7 @@ void dfm_destroy(dfm_ctx* c) {
   for (auto e : c->iter_ev) cudaEventDestroy(e);
   if (c->eb0) cudaEventDestroy(c->eb0);
   if (c->eb1) cudaEventDestroy(c->eb1);
+  if (c->ebm) cudaEventDestroy(c->ebm);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -1022,6 +1028,7 @@ int dfm_bench_step(dfm_ctx* c) {
   DFM_API_BEGIN
   DFM_CK(cudaEventRecord(c->eb0, c->stream));
   launch_bin(c, 2, 1, 1);
+  DFM_CK(cudaEventRecord(c->ebm, c->stream));
   launch_vupd(c);
   DFM_CK(cudaEventRecord(c->eb1, c->stream));
   return DFM_OK;
@@ -1044,6 +1051,19 @@ double dfm_bench_last_ms(dfm_ctx* c) {
   return ms;
 }
 
+int dfm_bench_last_split(dfm_ctx* c, double* bin_ms, double* vupd_ms) {
+  if (!c) return DFM_ERR_ARG;
+  DFM_API_BEGIN
+  DFM_CK(cudaEventSynchronize(c->eb1));
+  float a = 0.f, b = 0.f;
+  DFM_CK(cudaEventElapsedTime(&a, c->eb0, c->ebm));
+  DFM_CK(cudaEventElapsedTime(&b, c->ebm, c->eb1));
+  if (bin_ms) *bin_ms = a;
+  if (vupd_ms) *vupd_ms = b;
+  return DFM_OK;
+  DFM_API_END
+}
+
 long long dfm_launch_count(const dfm_ctx* c) { return c ? c->launches : -1; }
 
 int dfm_set_tiling(dfm_ctx* c, int bins_per_cta, int cluster_size) {
@@ -1051,9 +1071,15 @@ int dfm_set_tiling(dfm_ctx* c, int bins_per_cta, int cluster_size) {
     return DFM_ERR_ARG;
   DFM_API_BEGIN
   DFM_CK(cudaSetDevice(c->device));
+  const int oG = c->req_G, oCS = c->req_CS;
   c->req_G = bins_per_cta;
   c->req_CS = cluster_size;
-  choose_tiling(c);
+  if (!choose_tiling(c)) {
+    c->req_G = oG;
+    c->req_CS = oCS;
+    choose_tiling(c);
+    return DFM_ERR_UNSUPPORTED;
+  }
   set_kernel_attrs(c);
   return DFM_OK;
   DFM_API_END
