@@ -118,6 +118,9 @@ long long dfm_launch_count(const dfm_ctx* ctx);
 /* Tuning override for the fused bin kernel: bins per CTA group (G) and
  * cluster size (CTAs splitting T).  0 = heuristic. */
 int dfm_set_tiling(dfm_ctx* ctx, int bins_per_cta, int cluster_size);
+/* Use the generic (runtime-shape) bin kernel even when a compile-time-shape
+ * instantiation matches the layout (A/B testing of the two code paths). */
+int dfm_force_generic(dfm_ctx* ctx, int on);
 int dfm_get_tiling(const dfm_ctx* ctx, int* bins_per_cta, int* cluster_size, int* frames_per_cta,
                    int* threads, int* smem_bytes);
 

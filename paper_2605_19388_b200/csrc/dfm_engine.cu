@@ -64,510 +64,9 @@ struct BinArgs {
   int start;   // 1 = IP + T update + V weights
 };
 
-// Shared-memory carve-up, identical on host and device.
-struct SmemPlan {
-  size_t xs, ps, es, tsm, lsm, wsm, qsum, red, uni, hs, ab, bb, qpart, ipscr, ldet, total;
-  int nwarps, nitems, ssplit, nred;
-};
-
-template <int MAXMB>
-__host__ __device__ inline size_t ipscr_bytes() {
-  return (sizeof(IpScratch<MAXMB>) + 15) / 16 * 16;
-}
-
-template <int MAXMB>
-__host__ __device__ inline SmemPlan plan_smem(const BinArgs& a, int nthreads) {
-  SmemPlan p;
-  auto al = [](size_t v) { return (v + 15) / 16 * 16; };
-  const size_t G = a.G, Tsp = a.Tsp, M = a.M, N = a.N, K = a.K;
-  p.nwarps = nthreads / 32;
-  p.nitems = a.G * a.etot;
-  p.ssplit = nthreads / p.nitems;
-  if (p.ssplit < 1) p.ssplit = 1;
-  size_t o = 0;
-  p.xs = o; o += al(G * M * Tsp * sizeof(cd));
-  p.ps = o; o += al(G * M * Tsp * sizeof(double));
-  p.es = o; o += al(G * M * Tsp * sizeof(double));
-  p.tsm = o; o += al(G * N * K * sizeof(double));
-  p.lsm = o; o += al(G * N * M * sizeof(double));
-  p.wsm = o; o += al(G * a.wsz * sizeof(cd));
-  p.qsum = o; o += al((size_t)G * a.qper * sizeof(cd));
-  size_t nred = 2 * G * N * M;
-  nred = nred > 2 * (size_t)G * a.qper ? nred : 2 * (size_t)G * a.qper;
-  nred = nred > 2 * G * N * K ? nred : 2 * G * N * K;
-  p.nred = (int)nred;
-  p.red = o; o += al((nred + 2) * sizeof(double));
-  p.ldet = o; o += al(G * a.nb * sizeof(double));
-  // union: {hs, ab, bb} | qpart | ipscr
-  const size_t u1 = 3 * al(G * N * Tsp * sizeof(double));
-  const size_t slots = (size_t)(nthreads > p.nitems ? nthreads : p.nitems);
-  const size_t u2 = al(slots * MAXMB * sizeof(cd));
-  const size_t u3 = (size_t)p.nwarps * ipscr_bytes<MAXMB>();
-  size_t u = u1 > u2 ? u1 : u2;
-  u = u > u3 ? u : u3;
-  p.uni = o;
-  p.hs = o;
-  p.ab = o + al(G * N * Tsp * sizeof(double));
-  p.bb = o + 2 * al(G * N * Tsp * sizeof(double));
-  p.qpart = o;
-  p.ipscr = o;
-  o += u;
-  p.total = o;
-  return p;
-}
-
-__device__ __forceinline__ void decode_entry(int e, int& r, int& c) {
-  c = 0;
-  while ((c + 1) * (c + 2) / 2 <= e) ++c;
-  r = e - c * (c + 1) / 2;
-}
-
-template <int MAXMB>
-__global__ void __launch_bounds__(kThreads) k_bin(const BinArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  cg::cluster_group cluster = cg::this_cluster();
-  const int rank = (int)cluster.block_rank();
-  const int grp = blockIdx.x / a.CS;
-  const int t0 = rank * a.Ts;
-  const int tn = max(0, min(a.Ts, a.T - t0));
-  const int f0 = grp * a.G;
-  const int gn = min(a.G, a.F - f0);
-  const int tid = threadIdx.x, nth = blockDim.x;
-  const int M = a.M, N = a.N, K = a.K, Tsp = a.Tsp;
-  const SmemPlan sp = plan_smem<MAXMB>(a, nth);
-  cd* xs = (cd*)(smem + sp.xs);        // [g][m][Tsp]
-  double* ps = (double*)(smem + sp.ps);  // [g][m][Tsp]
-  double* es = (double*)(smem + sp.es);  // [g][m][Tsp]  1/eta
-  double* Tsm = (double*)(smem + sp.tsm);  // [g][n][k]
-  double* Lsm = (double*)(smem + sp.lsm);  // [g][n][m]
-  cd* Wsm = (cd*)(smem + sp.wsm);          // [g][wsz]
-  cd* Qsum = (cd*)(smem + sp.qsum);        // [g][qper]
-  double* red = (double*)(smem + sp.red);  // [2 + nred]
-  double* ldet = (double*)(smem + sp.ldet);
-  double* hs = (double*)(smem + sp.hs);  // [g][n][Tsp]
-  double* ab = (double*)(smem + sp.ab);  // [g][n][Tsp]
-  double* bb = (double*)(smem + sp.bb);  // [g][n][Tsp]
-  cd* qpart = (cd*)(smem + sp.qpart);
-  const double floor_ = a.floor_;
-
-  // ---- stage the X slice (transposed to [m][t] for conflict-free frame-parallel
-  // access) and the per-bin parameters
-  for (int g = 0; g < gn; ++g) {
-    const cd* src = a.x + ((size_t)(f0 + g) * a.T + t0) * M;
-    for (int e = tid; e < tn * M; e += nth) {
-      const int t = e / M, m = e % M;
-      xs[((size_t)g * M + m) * Tsp + t] = src[e];
-    }
-  }
-  for (int e = tid; e < gn * N * K; e += nth) Tsm[e] = a.Tf[(size_t)f0 * N * K + e];
-  for (int e = tid; e < gn * N * M; e += nth) Lsm[e] = a.lam[(size_t)f0 * N * M + e];
-  for (int e = tid; e < gn * a.wsz; e += nth) Wsm[e] = a.W[(size_t)f0 * a.wsz + e];
-  __syncthreads();
-
-  const int npair = gn * tn;
-  double cost = 0.0;
-
-  // per-frame spectrogram h = T V and projected power P = |W^H x|^2 (old W)
-  auto frame_h_p = [&](int g, int t) {
-    double h[kMaxN];
-#pragma unroll
-    for (int n = 0; n < kMaxN; ++n) {
-      double s = 0.0;
-      if (n < N) {
-        const double* tr = Tsm + ((size_t)g * N + n) * K;
-        const double* vr = a.V + (size_t)n * K * a.T + t0 + t;
-        for (int k = 0; k < K; ++k) s += tr[k] * vr[(size_t)k * a.T];
-        hs[((size_t)g * N + n) * Tsp + t] = s;
-      }
-      h[n] = s;
-    }
-    for (int b = 0; b < a.nb; ++b) {
-      const int mb = a.mb[b], off = a.off[b];
-      const cd* wb = Wsm + (size_t)g * a.wsz + a.woff[b];
-      for (int mu = 0; mu < mb; ++mu) {
-        cd s{0.0, 0.0};
-        for (int q = 0; q < mb; ++q) s = s + cmulc(wb[mu * mb + q], xs[((size_t)g * M + off + q) * Tsp + t]);
-        ps[((size_t)g * M + off + mu) * Tsp + t] = norm2(s);
-      }
-    }
-    return 0;
-  };
-
-  // ================================================================ pass A
-  if (a.finish == 2) {
-    for (int p = tid; p < npair; p += nth) {
-      const int g = p / tn, t = p % tn;
-      frame_h_p(g, t);
-      for (int m = 0; m < M; ++m) {
-        double raw = 0.0;
-#pragma unroll
-        for (int n = 0; n < kMaxN; ++n)
-          if (n < N) raw += hs[((size_t)g * N + n) * Tsp + t] * Lsm[((size_t)g * N + n) * M + m];
-        es[((size_t)g * M + m) * Tsp + t] = 1.0 / fmax(raw, floor_);
-      }
-    }
-    __syncthreads();
-    // Lambda numerator / denominator over this CTA's frames (engine.cpp:139-145)
-    for (int q = tid; q < gn * N * M; q += nth) {
-      const int g = q / (N * M), n = (q / M) % N, m = q % M;
-      const double* hr = hs + ((size_t)g * N + n) * Tsp;
-      const double* pr = ps + ((size_t)g * M + m) * Tsp;
-      const double* er = es + ((size_t)g * M + m) * Tsp;
-      double num = 0.0, den = 0.0;
-      for (int t = 0; t < tn; ++t) {
-        const double ie = er[t];
-        const double z = pr[t] * ie * ie;
-        num += hr[t] * z;
-        den += hr[t] * ie;
-      }
-      red[2 + 2 * q] = num;
-      red[2 + 2 * q + 1] = den;
-    }
-    cluster.sync();
-    for (int q = tid; q < gn * N * M; q += nth) {
-      double num = 0.0, den = 0.0;
-      for (int r = 0; r < a.CS; ++r) {
-        const double* rr = cluster.map_shared_rank(red, r);
-        num += rr[2 + 2 * q];
-        den += rr[2 + 2 * q + 1];
-      }
-      const int g = q / (N * M), n = (q / M) % N, m = q % M;
-      double& l = Lsm[((size_t)g * N + n) * M + m];
-      l = fmax(l * sqrt(num / fmax(den, floor_)), floor_);
-    }
-    cluster.sync();
-    if (rank == 0)
-      for (int e = tid; e < gn * N * M; e += nth) a.lam[(size_t)f0 * N * M + e] = Lsm[e];
-  }
-
-  // ================================================================ pass B
-  // eta with the current Lambda, the cost terms (engine.cpp:150-159) and the
-  // IP weights 1/max(eta, floor) (engine.cpp:43)
-  for (int p = tid; p < npair; p += nth) {
-    const int g = p / tn, t = p % tn;
-    if (a.finish != 2) frame_h_p(g, t);
-    for (int m = 0; m < M; ++m) {
-      double raw = 0.0;
-#pragma unroll
-      for (int n = 0; n < kMaxN; ++n)
-        if (n < N) raw += hs[((size_t)g * N + n) * Tsp + t] * Lsm[((size_t)g * N + n) * M + m];
-      const double e = fmax(raw, floor_);
-      cost += ps[((size_t)g * M + m) * Tsp + t] / e;
-      cost += log(fmax(raw, 1e-300));
-      es[((size_t)g * M + m) * Tsp + t] = 1.0 / e;
-    }
-  }
-  // block reduction of the cost partial (fixed order)
-  cost = warp_sum(cost);
-  __syncthreads();  // hs no longer needed: the union region is free
-  double* wsum = (double*)(smem + sp.qpart);
-  if ((tid & 31) == 0) wsum[tid >> 5] = cost;
-  // log|det W| of the pre-IP demixers (engine.cpp:161-165), rank 0 only
-  __syncthreads();
-  if (tid == 0) {
-    double c = 0.0;
-    for (int w = 0; w < sp.nwarps; ++w) c += wsum[w];
-    red[0] = c;
-  }
-  __syncthreads();
-  if (rank == 0) {
-    const int warp = tid >> 5, lane = tid & 31;
-    for (int sys = warp; sys < gn * a.nb; sys += sp.nwarps) {
-      const int g = sys / a.nb, b = sys % a.nb, mb = a.mb[b];
-      IpScratch<MAXMB>& s = *(IpScratch<MAXMB>*)(smem + sp.ipscr + warp * ipscr_bytes<MAXMB>());
-      const cd* wb = Wsm + (size_t)g * a.wsz + a.woff[b];
-      for (int e = lane; e < mb * mb; e += 32) s.S[e] = wb[e];
-      __syncwarp();
-      warp_lu(mb, s.S, s.perm);
-      double acc = 0.0;
-      bool sing = false;
-      for (int k = lane; k < mb; k += 32) {
-        const double p = hypot(s.S[k * mb + k].re, s.S[k * mb + k].im);
-        if (!(p > 0.0)) sing = true;
-        acc += log(p);
-      }
-      sing = __any_sync(0xffffffffu, sing);
-      acc = warp_sum(acc);
-      if (lane == 0) ldet[sys] = sing ? -INFINITY : 2.0 * acc;
-      __syncwarp();
-    }
-  }
-  __syncthreads();
-  if (rank == 0 && tid == 0) {
-    double det = 0.0;
-    for (int sys = 0; sys < gn * a.nb; ++sys) det += ldet[sys];
-    red[1] = -(double)a.T * det;
-  } else if (tid == 0) {
-    red[1] = 0.0;
-  }
-
-  // Q accumulation: every (bin, block, Hermitian entry r<=c) item sums, for
-  // all columns mu of its block at once, w_t,mu * x_r conj(x_c) over frames
-  // (engine.cpp:42-45 with the weighted covariances of all mu built from one
-  // pass over the resident X slice).
-  if (a.start) {
-    const int nitems = gn * a.etot;
-    const int S = max(1, nth / max(1, nitems));
-    for (int u = tid; u < nitems * S; u += nth) {
-      const int item = u % nitems, s = u / nitems;
-      const int g = item / a.etot;
-      int rem = item % a.etot, b = 0;
-      while (b + 1 < a.nb && rem >= a.eofs[b + 1]) ++b;
-      rem -= a.eofs[b];
-      int r, c;
-      decode_entry(rem, r, c);
-      const int mb = a.mb[b], off = a.off[b];
-      cd acc[MAXMB];
-#pragma unroll
-      for (int mu = 0; mu < MAXMB; ++mu) acc[mu] = cd{0.0, 0.0};
-      const cd* xr = xs + ((size_t)g * M + off + r) * Tsp;
-      const cd* xc = xs + ((size_t)g * M + off + c) * Tsp;
-      const double* ew = es + ((size_t)g * M + off) * Tsp;
-      for (int t = s; t < tn; t += S) {
-        const cd pr = xr[t] * conjg(xc[t]);
-#pragma unroll
-        for (int mu = 0; mu < MAXMB; ++mu)
-          if (mu < mb) acc[mu] = acc[mu] + pr * ew[(size_t)mu * Tsp + t];
-      }
-      // qpart aliases the (now dead) hs region; wsum above lives there too but
-      // was consumed before the last __syncthreads
-#pragma unroll
-      for (int mu = 0; mu < MAXMB; ++mu) qpart[((size_t)s * nitems + item) * MAXMB + mu] = acc[mu];
-    }
-    __syncthreads();
-    for (int idx = tid; idx < nitems * MAXMB; idx += nth) {
-      const int it = idx / MAXMB, mu = idx % MAXMB;
-      const int g = it / a.etot;
-      int rem = it % a.etot, b = 0;
-      while (b + 1 < a.nb && rem >= a.eofs[b + 1]) ++b;
-      rem -= a.eofs[b];
-      if (mu >= a.mb[b]) continue;
-      cd sum{0.0, 0.0};
-      for (int ss = 0; ss < S; ++ss) sum = sum + qpart[((size_t)ss * nitems + it) * MAXMB + mu];
-      const int E = a.mb[b] * (a.mb[b] + 1) / 2;
-      const size_t dst = (size_t)g * a.qper + a.qofs[b] + (size_t)mu * E + rem;
-      red[2 + 2 * dst] = sum.re;
-      red[2 + 2 * dst + 1] = sum.im;
-    }
-  }
-  cluster.sync();
-  if (rank == 0 && tid == 0) {
-    double c = 0.0;
-    for (int r = 0; r < a.CS; ++r) {
-      const double* rr = cluster.map_shared_rank(red, r);
-      c += rr[0];
-    }
-    c += red[1];
-    a.cost_out[grp] = c;
-  }
-  if (a.start) {
-    for (int q = tid; q < gn * a.qper; q += nth) {
-      double re = 0.0, im = 0.0;
-      for (int r = 0; r < a.CS; ++r) {
-        const double* rr = cluster.map_shared_rank(red, r);
-        re += rr[2 + 2 * q];
-        im += rr[2 + 2 * q + 1];
-      }
-      Qsum[q] = cd{re / (double)a.T, im / (double)a.T};
-    }
-  }
-  cluster.sync();
-  if (!a.start) return;
-
-  // ============================================================ IP solves
-  {
-    const int warp = tid >> 5;
-    int fbs = 0;
-    for (int sys = warp; sys < gn * a.nb; sys += sp.nwarps) {
-      const int g = sys / a.nb, b = sys % a.nb, mb = a.mb[b];
-      const int E = mb * (mb + 1) / 2;
-      IpScratch<MAXMB>& s = *(IpScratch<MAXMB>*)(smem + sp.ipscr + warp * ipscr_bytes<MAXMB>());
-      cd* wb = Wsm + (size_t)g * a.wsz + a.woff[b];
-      for (int mu = 0; mu < mb; ++mu) {
-        const cd* qp = Qsum + (size_t)g * a.qper + a.qofs[b] + (size_t)mu * E;
-        auto qget = [&](int r, int c) {
-          return r <= c ? qp[c * (c + 1) / 2 + r] : conjg(qp[r * (r + 1) / 2 + c]);
-        };
-        fbs += ip_column_warp<MAXMB>(mb, wb, mu, qget, floor_, s);
-      }
-    }
-    if (rank == 0 && (tid & 31) == 0 && fbs) atomicAdd(a.fallbacks, fbs);
-  }
-  __syncthreads();
-  if (rank == 0)
-    for (int e = tid; e < gn * a.wsz; e += nth) a.W[(size_t)f0 * a.wsz + e] = Wsm[e];
-
-  // ================================================================ pass C
-  // new P = |W^H x|^2 (engine.cpp:219-222), T-update weights with the
-  // pre-update eta (engine.cpp:100-109)
-  for (int p = tid; p < npair; p += nth) {
-    const int g = p / tn, t = p % tn;
-    for (int b = 0; b < a.nb; ++b) {
-      const int mb = a.mb[b], off = a.off[b];
-      const cd* wb = Wsm + (size_t)g * a.wsz + a.woff[b];
-      for (int mu = 0; mu < mb; ++mu) {
-        cd s{0.0, 0.0};
-        for (int q = 0; q < mb; ++q) s = s + cmulc(wb[mu * mb + q], xs[((size_t)g * M + off + q) * Tsp + t]);
-        ps[((size_t)g * M + off + mu) * Tsp + t] = norm2(s);
-      }
-    }
-    double A[kMaxN], B[kMaxN];
-#pragma unroll
-    for (int n = 0; n < kMaxN; ++n) A[n] = B[n] = 0.0;
-    for (int m = 0; m < M; ++m) {
-      const double ie = es[((size_t)g * M + m) * Tsp + t];
-      const double z = ps[((size_t)g * M + m) * Tsp + t] * ie * ie;
-#pragma unroll
-      for (int n = 0; n < kMaxN; ++n)
-        if (n < N) {
-          const double l = Lsm[((size_t)g * N + n) * M + m];
-          A[n] += z * l;
-          B[n] += ie * l;
-        }
-    }
-#pragma unroll
-    for (int n = 0; n < kMaxN; ++n)
-      if (n < N) {
-        ab[((size_t)g * N + n) * Tsp + t] = A[n];
-        bb[((size_t)g * N + n) * Tsp + t] = B[n];
-      }
-  }
-  __syncthreads();
-  // T numerator / denominator (engine.cpp:117-118): one thread per (n, k),
-  // each V row read once and reused for all G bins of the group
-  for (int q = tid; q < N * K; q += nth) {
-    const int n = q / K, k = q % K;
-    double num[kGMax], den[kGMax];
-#pragma unroll
-    for (int g = 0; g < kGMax; ++g) num[g] = den[g] = 0.0;
-    const double* vr = a.V + ((size_t)n * K + k) * a.T + t0;
-    for (int t = 0; t < tn; ++t) {
-      const double v = vr[t];
-#pragma unroll
-      for (int g = 0; g < kGMax; ++g)
-        if (g < gn) {
-          num[g] += ab[((size_t)g * N + n) * Tsp + t] * v;
-          den[g] += bb[((size_t)g * N + n) * Tsp + t] * v;
-        }
-    }
-#pragma unroll
-    for (int g = 0; g < kGMax; ++g)
-      if (g < gn) {
-        const size_t o = ((size_t)g * N + n) * K + k;
-        red[2 + 2 * o] = num[g];
-        red[2 + 2 * o + 1] = den[g];
-      }
-  }
-  cluster.sync();
-  for (int q = tid; q < gn * N * K; q += nth) {
-    double num = 0.0, den = 0.0;
-    for (int r = 0; r < a.CS; ++r) {
-      const double* rr = cluster.map_shared_rank(red, r);
-      num += rr[2 + 2 * q];
-      den += rr[2 + 2 * q + 1];
-    }
-    Tsm[q] = fmax(Tsm[q] * sqrt(num / fmax(den, floor_)), floor_);
-  }
-  cluster.sync();
-  if (rank == 0)
-    for (int e = tid; e < gn * N * K; e += nth) a.Tf[(size_t)f0 * N * K + e] = Tsm[e];
-
-  // ================================================================ pass D
-  // h' = T_new V, eta' (engine.cpp:231-232), V-update weights (engine.cpp:236)
-  for (int p = tid; p < npair; p += nth) {
-    const int g = p / tn, t = p % tn;
-    double h[kMaxN];
-#pragma unroll
-    for (int n = 0; n < kMaxN; ++n) {
-      double s = 0.0;
-      if (n < N) {
-        const double* tr = Tsm + ((size_t)g * N + n) * K;
-        const double* vr = a.V + (size_t)n * K * a.T + t0 + t;
-        for (int k = 0; k < K; ++k) s += tr[k] * vr[(size_t)k * a.T];
-      }
-      h[n] = s;
-    }
-    double A[kMaxN], B[kMaxN];
-#pragma unroll
-    for (int n = 0; n < kMaxN; ++n) A[n] = B[n] = 0.0;
-    for (int m = 0; m < M; ++m) {
-      double raw = 0.0;
-#pragma unroll
-      for (int n = 0; n < kMaxN; ++n)
-        if (n < N) raw += h[n] * Lsm[((size_t)g * N + n) * M + m];
-      const double ie = 1.0 / fmax(raw, floor_);
-      const double z = ps[((size_t)g * M + m) * Tsp + t] * ie * ie;
-#pragma unroll
-      for (int n = 0; n < kMaxN; ++n)
-        if (n < N) {
-          const double l = Lsm[((size_t)g * N + n) * M + m];
-          A[n] += z * l;
-          B[n] += ie * l;
-        }
-    }
-#pragma unroll
-    for (int n = 0; n < kMaxN; ++n)
-      if (n < N) {
-        const size_t o = ((size_t)n * a.F + f0 + g) * a.T + t0 + t;
-        a.Ap[o] = A[n];
-        a.Bp[o] = B[n];
-      }
-  }
-}
-
-// V update (engine.cpp:125-133): one thread per (n, k-subset, frame), bins
-// summed in ascending order (deterministic; no atomics).  numden == nullptr:
-// apply in place; else write {num, den} for the cross-GPU allreduce.
-__global__ void __launch_bounds__(256) k_vupd(int F, int T, int N, int K, const double* __restrict__ Tf,
-                                             const double* __restrict__ Ap, const double* __restrict__ Bp,
-                                             double* __restrict__ V, double* __restrict__ numden,
-                                             double floor_) {
-  constexpr int KPW = kMaxK / 8;  // k per warp (8 warps)
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int t = blockIdx.x * 32 + lane;
-  const int n = blockIdx.y;
-  if (t >= T) return;
-  double num[KPW], den[KPW];
-#pragma unroll
-  for (int j = 0; j < KPW; ++j) num[j] = den[j] = 0.0;
-  const double* ar = Ap + (size_t)n * F * T + t;
-  const double* br = Bp + (size_t)n * F * T + t;
-  for (int f = 0; f < F; ++f) {
-    const double av = ar[(size_t)f * T], bv = br[(size_t)f * T];
-    const double* tr = Tf + ((size_t)f * N + n) * K;
-#pragma unroll
-    for (int j = 0; j < KPW; ++j) {
-      const int k = warp + 8 * j;
-      if (k < K) {
-        const double tv = tr[k];
-        num[j] += tv * av;
-        den[j] += tv * bv;
-      }
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < KPW; ++j) {
-    const int k = warp + 8 * j;
-    if (k < K) {
-      const size_t o = ((size_t)n * K + k) * T + t;
-      if (numden) {
-        numden[o] = num[j];
-        numden[(size_t)N * K * T + o] = den[j];
-      } else {
-        V[o] = fmax(V[o] * sqrt(num[j] / fmax(den[j], floor_)), floor_);
-      }
-    }
-  }
-}
-
-__global__ void k_vapply(size_t nkt, const double* __restrict__ numden, double* __restrict__ V,
-                         double floor_) {
-  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (i >= nkt) return;
-  V[i] = fmax(V[i] * sqrt(numden[i] / fmax(numden[nkt + i], floor_)), floor_);
-}
-
 }  // namespace dfm
+
+#include "dfm_bin_kernel.cuh"
 
 using namespace dfm;
 
@@ -590,6 +89,9 @@ struct dfm_ctx {
   DBuf<double> Tf, V, lam, Ap, Bp, numden, cost_part, cost_sum;
   DBuf<int> fallbacks;
   int G = 1, CS = 1, Ts = 1, Tsp = 1, threads = 256, smem = 0, maxmb = 4, ngroups = 1;
+  int kmaxmb = 4;           // MAXMB of the selected k_bin instantiation
+  void (*kbin)(BinArgs) = nullptr;
+  bool force_generic = false;
   int req_G = 0, req_CS = 0;
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
@@ -640,6 +142,34 @@ BinArgs make_args(dfm_ctx* c) {
   return a;
 }
 
+size_t plan_total(const BinArgs& a, int threads, int kmaxmb) {
+  switch (kmaxmb) {
+    case 2: return plan_smem<2>(a, threads).total;
+    case 4: return plan_smem<4>(a, threads).total;
+    case 12: return plan_smem<12>(a, threads).total;
+    default: return plan_smem<DFM_MAX_MB>(a, threads).total;
+  }
+}
+
+// Kernel selection: a compile-time-shape instantiation when the layout is
+// uniform and matches one (BASELINE configs 0-3), else the generic kernel.
+void select_kernel(dfm_ctx* c) {
+  bool uniform = true;
+  for (int b = 1; b < c->L.nb; ++b) uniform = uniform && c->L.mb[b] == c->L.mb[0];
+  const int mb = c->L.mb[0], nb = c->L.nb, N = c->N;
+  c->kbin = nullptr;
+  if (uniform && !c->force_generic) {
+    if (mb == 4 && nb == 3 && N == 5) { c->kbin = k_bin<4, 3, 5, 4>; c->kmaxmb = 4; }
+    else if (mb == 2 && nb == 2 && N == 3) { c->kbin = k_bin<2, 2, 3, 2>; c->kmaxmb = 2; }
+    else if (mb == 4 && nb == 8 && N == 8) { c->kbin = k_bin<4, 8, 8, 4>; c->kmaxmb = 4; }
+    else if (mb == 12 && nb == 1 && N == 5) { c->kbin = k_bin<12, 1, 5, 12>; c->kmaxmb = 12; }
+  }
+  if (!c->kbin) {
+    if (c->maxmb <= 4) { c->kbin = k_bin<0, 0, 0, 4>; c->kmaxmb = 4; }
+    else { c->kbin = k_bin<0, 0, 0, DFM_MAX_MB>; c->kmaxmb = DFM_MAX_MB; }
+  }
+}
+
 size_t smem_for(dfm_ctx* c, int G, int CS, int& Ts, int& Tsp, int& threads) {
   Ts = (c->T + CS - 1) / CS;
   Tsp = Ts | 1;
@@ -657,8 +187,7 @@ size_t smem_for(dfm_ctx* c, int G, int CS, int& Ts, int& Tsp, int& threads) {
     c->Ts = sTs;
     c->Tsp = sTsp;
   }
-  const SmemPlan p = c->maxmb <= 4 ? plan_smem<4>(a, threads) : plan_smem<DFM_MAX_MB>(a, threads);
-  return p.total;
+  return plan_total(a, threads, c->kmaxmb);
 }
 
 // Tiling heuristic: keep each CTA's frame slice resident (<= ~113 KB so two
@@ -721,17 +250,14 @@ void launch_bin(dfm_ctx* c, int finish, int start, int slot) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (c->maxmb <= 4)
-    DFM_CK(cudaLaunchKernelEx(&cfg, k_bin<4>, a));
-  else
-    DFM_CK(cudaLaunchKernelEx(&cfg, k_bin<DFM_MAX_MB>, a));
+  DFM_CK(cudaLaunchKernelEx(&cfg, c->kbin, a));
   c->launches++;
 }
 
 void launch_vupd(dfm_ctx* c) {
-  const dim3 grid((c->T + 31) / 32, c->N);
+  const dim3 grid((c->T + 31) / 32, c->N, (c->K + kVupdKPT - 1) / kVupdKPT);
   const bool sharded = c->comm != nullptr && c->nranks > 1;
-  k_vupd<<<grid, 256, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->Ap.p, c->Bp.p, c->V.p,
+  k_vupd<<<grid, 32 * kVupdWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->Ap.p, c->Bp.p, c->V.p,
                                       sharded ? c->numden.p : nullptr, c->floor_);
   DFM_CK_LAUNCH();
   c->launches++;
@@ -749,13 +275,8 @@ void ensure_cost(dfm_ctx* c, int slots) {
 }
 
 void set_kernel_attrs(dfm_ctx* c) {
-  if (c->maxmb <= 4) {
-    DFM_CK(cudaFuncSetAttribute(k_bin<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem));
-    DFM_CK(cudaFuncSetAttribute(k_bin<4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  } else {
-    DFM_CK(cudaFuncSetAttribute(k_bin<DFM_MAX_MB>, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem));
-    DFM_CK(cudaFuncSetAttribute(k_bin<DFM_MAX_MB>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  }
+  DFM_CK(cudaFuncSetAttribute(c->kbin, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem));
+  DFM_CK(cudaFuncSetAttribute(c->kbin, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
 }
 
 }  // namespace
@@ -806,6 +327,7 @@ dfm_ctx* dfm_create(int F, int T, int nblocks, const int* block_sizes, int N, in
     c->L = L;
     c->maxmb = 1;
     for (int b = 0; b < L.nb; ++b) c->maxmb = std::max(c->maxmb, L.mb[b]);
+    select_kernel(c);
     DFM_CK(cudaSetDevice(device));
     DFM_CK(cudaStreamCreate(&c->stream));
     DFM_CK(cudaEventCreate(&c->eb0));
@@ -1080,6 +602,18 @@ int dfm_set_tiling(dfm_ctx* c, int bins_per_cta, int cluster_size) {
     choose_tiling(c);
     return DFM_ERR_UNSUPPORTED;
   }
+  set_kernel_attrs(c);
+  return DFM_OK;
+  DFM_API_END
+}
+
+int dfm_force_generic(dfm_ctx* c, int on) {
+  if (!c) return DFM_ERR_ARG;
+  DFM_API_BEGIN
+  DFM_CK(cudaSetDevice(c->device));
+  c->force_generic = on != 0;
+  select_kernel(c);
+  if (!choose_tiling(c)) return DFM_ERR_UNSUPPORTED;
   set_kernel_attrs(c);
   return DFM_OK;
   DFM_API_END

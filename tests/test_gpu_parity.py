@@ -296,3 +296,26 @@ def test_config1_trajectory_20_iterations(dfm, oracle):
     img = dfm.wiener_block(x, fit.models, fit.spatial).images
     ref_img = oracle.wiener_block(x, sizes, ref)
     assert _rel(img, ref_img) < 1e-6
+
+
+@pytest.mark.parametrize("sizes,N,K", [([2, 2], 3, 4), ([4, 4, 4], 5, 16), ([12], 5, 16), ([4] * 8, 8, 32)])
+def test_static_shape_kernels_match_generic_and_oracle(dfm, oracle, sizes, N, K):
+    """The compile-time-shape k_bin instantiations (BASELINE configs 0-3) and
+    the generic runtime-shape kernel both track the oracle."""
+    F, T, iters = 9, 57, 12
+    layout = dfm.BlockLayout(sizes)
+    x = dfm.generate_mixture(1, F, T, layout.total, N, K, 4)
+    init = dfm.random_init(F, T, layout, N, K, 8)
+    ref = oracle.run_engine(x, sizes, _init_dict(init), iters)
+    costs = []
+    for generic in (0, 1):
+        with dfm.Engine(F, T, layout, N, K) as eng:
+            dfm._capi.check(eng.lib.dfm_force_generic(eng.ctx, generic))
+            eng.set_obs(x)
+            eng.set_model(init.nmf, init.w0, init.lambda0)
+            cost, _, _, _ = eng.fit(iters)
+            costs.append(cost)
+            nmf, wb, lam = eng.get_model()
+        assert np.max(np.abs(cost - ref["cost_trace"]) / np.abs(ref["cost_trace"])) < TRAJ_RTOL
+        assert _rel(nmf.V, ref["V"]) < 1e-7 and _rel(lam, ref["lam"]) < 1e-7
+    assert np.max(np.abs(costs[0] - costs[1]) / np.abs(costs[1])) < TRAJ_RTOL
