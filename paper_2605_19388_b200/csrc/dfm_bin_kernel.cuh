@@ -16,10 +16,10 @@ struct SmemPlan {
   int nwarps, nitems, nred;
 };
 
+template <int MB>
+struct IpWork;
 template <int MAXMB>
-__host__ __device__ inline size_t ipscr_bytes() {
-  return (sizeof(IpScratch<MAXMB>) + 15) / 16 * 16;
-}
+__host__ __device__ inline size_t ipscr_bytes();
 
 template <int MAXMB>
 __host__ __device__ inline SmemPlan plan_smem(const BinArgs& a, int nthreads) {
@@ -216,9 +216,31 @@ __device__ int ip_solve_thread(cd* W, const cd* qb, double floor_, IpScratch<MB>
   return fb;
 }
 
-// 2 ln|det W| of one MB x MB block (engine.cpp:17-26, :161-165), one thread.
+template <int MAXMB>
+__host__ __device__ inline size_t ipscr_bytes() {
+  if constexpr (MAXMB <= 4)
+    return (sizeof(IpWork<MAXMB>) + 15) / 16 * 16;
+  else
+    return (sizeof(IpScratch<MAXMB>) + 15) / 16 * 16;
+}
+
+// Per owned (bin, block) system scratch of the fast IP path (MB <= 4).
 template <int MB>
-__device__ double logdet2_thread(const cd* W) {
+struct IpWork {
+  IpScratch<MB> slow;            // exact LU + pinv path (fallback)
+  cd Winv[MB * MB];              // W^-1, col-major
+  cd Wold[MB * MB];              // W before the sweep (restored on fallback)
+  cd L[MB][MB * (MB + 1) / 2];   // Cholesky factor of each Q_mu, packed lower
+  double dinv[MB][MB];           // 1 / L(c, c)
+  int ok[MB];
+};
+
+// 2 ln|det W| (engine.cpp:17-26, :161-165) and W^-1 from one partial-pivot
+// LU held in registers, one thread.  A singular W gives -inf (the fit then
+// records a +inf cost, engine.hpp:41-43) and a non-finite inverse, which
+// sends the IP sweep to the exact fallback.
+template <int MB>
+__device__ double logdet2_inverse_thread(const cd* W, cd* Winv) {
   cd L[MB][MB];
 #pragma unroll
   for (int r = 0; r < MB; ++r)
@@ -226,6 +248,8 @@ __device__ double logdet2_thread(const cd* W) {
     for (int c = 0; c < MB; ++c) L[r][c] = W[c * MB + r];
   double acc = 0.0;
   bool sing = false;
+  int perm[MB];
+  cd inv[MB];
 #pragma unroll
   for (int k = 0; k < MB; ++k) {
     int piv = k;
@@ -238,6 +262,7 @@ __device__ double logdet2_thread(const cd* W) {
         piv = r;
       }
     }
+    perm[k] = piv;
 #pragma unroll
     for (int r = k + 1; r < MB; ++r)
       if (piv == r)
@@ -249,19 +274,165 @@ __device__ double logdet2_thread(const cd* W) {
         }
     if (best != 0.0) {
       const double id = 1.0 / best;
-      const cd inv{L[k][k].re * id, -L[k][k].im * id};
+      inv[k] = cd{L[k][k].re * id, -L[k][k].im * id};
 #pragma unroll
-      for (int r = k + 1; r < MB; ++r) L[r][k] = L[r][k] * inv;
+      for (int r = k + 1; r < MB; ++r) L[r][k] = L[r][k] * inv[k];
       acc += 0.5 * log(best);
     } else {
       sing = true;
+      inv[k] = cd{INFINITY, 0.0};
     }
 #pragma unroll
     for (int r = k + 1; r < MB; ++r)
 #pragma unroll
       for (int c = k + 1; c < MB; ++c) L[r][c] = L[r][c] - L[r][k] * L[k][c];
   }
+#pragma unroll 1
+  for (int col = 0; col < MB; ++col) {
+    cd v[MB];
+#pragma unroll
+    for (int r = 0; r < MB; ++r) v[r] = cd{r == col ? 1.0 : 0.0, 0.0};
+#pragma unroll
+    for (int k = 0; k < MB; ++k)
+#pragma unroll
+      for (int r = k + 1; r < MB; ++r)
+        if (perm[k] == r) {
+          const cd t = v[k];
+          v[k] = v[r];
+          v[r] = t;
+        }
+#pragma unroll
+    for (int r = 1; r < MB; ++r)
+#pragma unroll
+      for (int c = 0; c < r; ++c) v[r] = v[r] - L[r][c] * v[c];
+#pragma unroll
+    for (int r = MB - 1; r >= 0; --r) {
+#pragma unroll
+      for (int c = r + 1; c < MB; ++c) v[r] = v[r] - L[r][c] * v[c];
+      v[r] = v[r] * inv[r];
+    }
+#pragma unroll
+    for (int r = 0; r < MB; ++r) Winv[col * MB + r] = v[r];
+  }
   return sing ? -INFINITY : 2.0 * acc;
+}
+
+// Cholesky Q_mu = L L^H of one weighted covariance (Hermitian, packed upper
+// triangle qp), one thread; false when Q_mu is not numerically positive
+// definite (the exact fallback then decides, as the reference's LU would).
+template <int MB>
+__device__ bool chol_thread(const cd* qp, cd* L, double* dinv) {
+  auto Q = [&](int r, int c) -> cd { return r <= c ? qp[c * (c + 1) / 2 + r] : conjg(qp[r * (r + 1) / 2 + c]); };
+  auto Li = [](int r, int c) { return r * (r + 1) / 2 + c; };
+#pragma unroll
+  for (int c = 0; c < MB; ++c) {
+    double d = Q(c, c).re;
+#pragma unroll
+    for (int k = 0; k < c; ++k) d -= norm2(L[Li(c, k)]);
+    if (!(d > 0.0) || !isfinite(d)) return false;
+    const double lc = sqrt(d);
+    dinv[c] = 1.0 / lc;
+    L[Li(c, c)] = cd{lc, 0.0};
+#pragma unroll
+    for (int r = c + 1; r < MB; ++r) {
+      cd s = Q(r, c);
+#pragma unroll
+      for (int k = 0; k < c; ++k) s = s - L[Li(r, k)] * conjg(L[Li(c, k)]);
+      L[Li(r, c)] = s * dinv[c];
+    }
+  }
+  return true;
+}
+
+// Fast IP sweep of one system (engine.cpp:40-51 for mu = 0..MB-1):
+//   u = (W^H Q_mu)^-1 e_mu = Q_mu^-1 W^-H e_mu  (two triangular solves),
+//   u /= sqrt(max(Re(u^H Q u), floor)),  W[:, mu] = u,
+//   W^-1 refreshed by Sherman-Morrison for the replaced column.
+// Every column still passes the reference's test ||W^H Q u - e_mu|| <= 1e-6
+// (with the current W, as engine.cpp:47-49); any failure returns false and
+// the caller reruns the exact LU + pinv sweep from W_old.
+template <int MB>
+__device__ bool ip_sweep_fast(cd* W, IpWork<MB>& f, const cd* qb, double floor_) {
+  constexpr int E = MB * (MB + 1) / 2;
+#pragma unroll
+  for (int mu = 0; mu < MB; ++mu)
+    if (!f.ok[mu]) return false;
+  auto Li = [](int r, int c) { return r * (r + 1) / 2 + c; };
+#pragma unroll 1
+  for (int mu = 0; mu < MB; ++mu) {
+    const cd* qp = qb + mu * E;
+    auto Q = [&](int r, int c) -> cd { return r <= c ? qp[c * (c + 1) / 2 + r] : conjg(qp[r * (r + 1) / 2 + c]); };
+    const cd* L = f.L[mu];
+    const double* di = f.dinv[mu];
+    cd u[MB];
+    // L y = W^-H e_mu  (b_k = conj(Winv(mu, k)))
+#pragma unroll
+    for (int r = 0; r < MB; ++r) {
+      cd s = conjg(f.Winv[r * MB + mu]);
+#pragma unroll
+      for (int c = 0; c < r; ++c) s = s - L[Li(r, c)] * u[c];
+      u[r] = s * di[r];
+    }
+    // L^H u = y
+#pragma unroll
+    for (int r = MB - 1; r >= 0; --r) {
+      cd s = u[r];
+#pragma unroll
+      for (int c = r + 1; c < MB; ++c) s = s - cmulc(L[Li(c, r)], u[c]);
+      u[r] = s * di[r];
+    }
+    cd qu[MB];
+    bool fin = true;
+#pragma unroll
+    for (int a = 0; a < MB; ++a) {
+      fin = fin && cfinite(u[a]);
+      cd s{0.0, 0.0};
+#pragma unroll
+      for (int c = 0; c < MB; ++c) s = s + Q(a, c) * u[c];
+      qu[a] = s;
+    }
+    double r2 = 0.0, nq = 0.0;
+#pragma unroll
+    for (int a = 0; a < MB; ++a) {
+      cd s{0.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < MB; ++k) s = s + cmulc(W[a * MB + k], qu[k]);
+      if (a == mu) s.re -= 1.0;
+      r2 += norm2(s);
+      nq += cmulc(u[a], qu[a]).re;
+    }
+    if (!fin || !(sqrt(r2) <= 1e-6)) return false;
+    const double sc = sqrt(fmax(nq, floor_));
+    cd d[MB];
+#pragma unroll
+    for (int a = 0; a < MB; ++a) {
+      u[a] = cdivr(u[a], sc);
+      d[a] = u[a] - W[mu * MB + a];
+    }
+    // Sherman-Morrison: (W + d e_mu^T)^-1 = W^-1 - z (e_mu^T W^-1) / (1 + z_mu), z = W^-1 d
+    cd z[MB];
+#pragma unroll
+    for (int r = 0; r < MB; ++r) {
+      cd s{0.0, 0.0};
+#pragma unroll
+      for (int c = 0; c < MB; ++c) s = s + f.Winv[c * MB + r] * d[c];
+      z[r] = s;
+    }
+    const cd den = cd{1.0 + z[mu].re, z[mu].im};
+    const double dn = norm2(den);
+    if (!(dn > 0.0)) return false;
+    const cd iden{den.re / dn, -den.im / dn};
+    cd row[MB];
+#pragma unroll
+    for (int c = 0; c < MB; ++c) row[c] = f.Winv[c * MB + mu] * iden;
+#pragma unroll
+    for (int c = 0; c < MB; ++c)
+#pragma unroll
+      for (int r = 0; r < MB; ++r) f.Winv[c * MB + r] = f.Winv[c * MB + r] - z[r] * row[c];
+#pragma unroll
+    for (int a = 0; a < MB; ++a) W[mu * MB + a] = u[a];
+  }
+  return true;
 }
 
 template <int MB_, int NB_, int NS_, int MAXMB>
@@ -464,7 +635,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
       const int s = rank + CS * i;
       if (s >= nsys) break;
       const int g = s / nb, b = s - g * nb;
-      det += logdet2_thread<MB_>(Wsm + g * wsz + b * MB_ * MB_);
+      IpWork<MB_>& w = *(IpWork<MB_>*)(smem + sp.ipscr + i * ipscr_bytes<MAXMB>());
+      const cd* wb = Wsm + g * wsz + b * MB_ * MB_;
+#pragma unroll
+      for (int e = 0; e < MB_ * MB_; ++e) w.Wold[e] = wb[e];
+      det += logdet2_inverse_thread<MB_>(wb, w.Winv);
     }
   } else {
     const int warp = tid >> 5, lane = tid & 31;
@@ -593,14 +768,31 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
   {
     int fbs = 0;
     if constexpr (SB && MB_ <= 4) {
+      constexpr int E = MB_ * (MB_ + 1) / 2;
+      // Cholesky of every Q_mu of every owned system, in parallel
+      for (int idx = tid; idx < per_rank * MB_; idx += nth) {
+        const int i = idx / MB_, mu = idx - i * MB_;
+        const int s = rank + CS * i;
+        if (s >= nsys) continue;
+        const int g = s / nb, b = s - g * nb;
+        IpWork<MB_>& w = *(IpWork<MB_>*)(smem + sp.ipscr + i * ipscr_bytes<MAXMB>());
+        w.ok[mu] = chol_thread<MB_>(Qsum + g * a.qper + a.qofs[b] + mu * E, w.L[mu], w.dinv[mu]) ? 1 : 0;
+      }
+      __syncthreads();
       for (int i = tid; i < per_rank; i += nth) {
         const int s = rank + CS * i;
         if (s >= nsys) break;
         const int g = s / nb, b = s - g * nb;
-        IpScratch<MAXMB>& sc = *(IpScratch<MAXMB>*)(smem + sp.ipscr + i * ipscr_bytes<MAXMB>());
-        fbs = ip_solve_thread<MB_>(Wsm + g * wsz + b * MB_ * MB_, Qsum + g * a.qper + a.qofs[b], floor_,
-                                   *reinterpret_cast<IpScratch<MB_>*>(&sc));
-        if (fbs) atomicAdd(a.fallbacks, fbs);
+        IpWork<MB_>& w = *(IpWork<MB_>*)(smem + sp.ipscr + i * ipscr_bytes<MAXMB>());
+        cd* wb = Wsm + g * wsz + b * MB_ * MB_;
+        const cd* qb = Qsum + g * a.qper + a.qofs[b];
+        if (!ip_sweep_fast<MB_>(wb, w, qb, floor_)) {
+          // exact path (engine.cpp:47-49: LU, residual test, pinv) from W_old
+#pragma unroll
+          for (int e = 0; e < MB_ * MB_; ++e) wb[e] = w.Wold[e];
+          fbs = ip_solve_thread<MB_>(wb, qb, floor_, w.slow);
+          if (fbs) atomicAdd(a.fallbacks, fbs);
+        }
       }
     } else {
       const int warp = tid >> 5, lane = tid & 31;
