@@ -118,6 +118,10 @@ long long dfm_launch_count(const dfm_ctx* ctx);
 /* Tuning override for the fused bin kernel: bins per CTA group (G) and
  * cluster size (CTAs splitting T).  0 = heuristic. */
 int dfm_set_tiling(dfm_ctx* ctx, int bins_per_cta, int cluster_size);
+/* Profiling aid: per-CTA %globaltimer stamps at the phase boundaries of the
+ * bin kernel (16 slots per CTA).  dfm_set_trace returns the buffer length. */
+int dfm_set_trace(dfm_ctx* ctx, int on);
+int dfm_get_trace(dfm_ctx* ctx, unsigned long long* out, int n);
 /* Use the generic (runtime-shape) bin kernel even when a compile-time-shape
  * instantiation matches the layout (A/B testing of the two code paths). */
 int dfm_force_generic(dfm_ctx* ctx, int on);

@@ -41,6 +41,8 @@ _SIGS = {
     "dfm_set_tiling": (_i, [_vp, _i, _i]),
     "dfm_get_tiling": (_i, [_vp, _ip, _ip, _ip, _ip, _ip]),
     "dfm_force_generic": (_i, [_vp, _i]),
+    "dfm_set_trace": (_i, [_vp, _i]),
+    "dfm_get_trace": (_i, [_vp, _vp, _i]),
     "dfm_wiener": (_i, [_vp, _vp]),
     "dfm_step_spectrogram": (_i, [_i, _i, _i, _i, _vp, _vp, _vp]),
     "dfm_step_eta": (_i, [_i, _i, _i, _i, _vp, _vp, _d, _vp]),

@@ -435,6 +435,14 @@ __device__ bool ip_sweep_fast(cd* W, IpWork<MB>& f, const cd* qb, double floor_)
   return true;
 }
 
+__device__ __forceinline__ void stamp(const BinArgs& a, int phase) {
+  if (a.trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[blockIdx.x * 16 + phase] = t;
+  }
+}
+
 template <int MB_, int NB_, int NS_, int MAXMB>
 __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
   constexpr bool SB = MB_ > 0 && NB_ > 0;  // uniform, compile-time layout
@@ -471,6 +479,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
   cd* qpart = (cd*)(smem + sp.qpart);
   const double floor_ = a.floor_;
   const int nsys = gn * nb;
+  stamp(a, 0);
 
   // ---- stage the X slice ([m][t], conflict-free frame-parallel access) and
   // the per-bin parameters
@@ -485,6 +494,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
   for (int e = tid; e < gn * N * M; e += nth) Lsm[e] = a.lam[(size_t)f0 * N * M + e];
   for (int e = tid; e < gn * wsz; e += nth) Wsm[e] = a.W[(size_t)f0 * wsz + e];
   __syncthreads();
+  stamp(a, 1);
 
   const int npair = gn * tn;
 
@@ -553,6 +563,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
       }
     }
     __syncthreads();
+    stamp(a, 2);
     for (int q = tid; q < gn * N * M; q += nth) {
       const int g = q / (N * M), n = (q / M) % N, m = q % M;
       const double* hr = hs + (g * N + n) * Tsp;
@@ -581,6 +592,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
       l = fmax(l * sqrt(num / fmax(den, floor_)), floor_);
     }
     cluster.sync();
+    stamp(a, 3);
     if (rank == 0)
       for (int e = tid; e < gn * N * M; e += nth) a.lam[(size_t)f0 * N * M + e] = Lsm[e];
   }
@@ -619,6 +631,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
   cost += lacc.value();
   cost = warp_sum(cost);
   __syncthreads();  // hs is dead from here on: its union slot is reused
+  stamp(a, 4);
   double* wsum = (double*)(smem + sp.qpart);
   if ((tid & 31) == 0) wsum[tid >> 5] = cost;
   __syncthreads();
@@ -676,6 +689,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
     red[1] = -(double)T * d;
   }
   __syncthreads();
+  stamp(a, 5);
 
   // Q accumulation: every (bin, block, Hermitian entry r<=c) item sums, for
   // all columns mu of its block at once, w_t,mu x_r conj(x_c) over frames
@@ -716,6 +730,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
       for (int mu = 0; mu < MAXMB; ++mu) qpart[(s * nitems + item) * MAXMB + mu] = acc[mu];
     }
     __syncthreads();
+    stamp(a, 6);
     for (int idx = tid; idx < nitems * MAXMB; idx += nth) {
       const int it = idx / MAXMB, mu = idx - it * MAXMB;
       const int g = it / a.etot;
@@ -760,6 +775,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
     }
   }
   cluster.sync();
+  stamp(a, 7);
   if (!a.start) return;
 
   // ============================================================ IP solves
@@ -816,6 +832,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
     }
   }
   cluster.sync();
+  stamp(a, 8);
   // gather the systems owned by other ranks; owners write them back to HBM
   for (int s = 0; s < nsys; ++s) {
     const int owner = s % CS;
@@ -829,6 +846,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
     }
   }
   cluster.sync();  // peers finished reading before anyone reuses shared memory
+  stamp(a, 9);
 
   // ================================================================ pass C
   // new P = |W^H x|^2 (engine.cpp:219-222); T-update weights with the
@@ -859,6 +877,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
       }
   }
   __syncthreads();
+  stamp(a, 10);
   // T numerator / denominator (engine.cpp:117-118): one thread per (n, k);
   // each V row is read once and reused for all G bins of the group
   for (int q = tid; q < N * K; q += nth) {
@@ -896,6 +915,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
     Tsm[q] = fmax(Tsm[q] * sqrt(num / fmax(den, floor_)), floor_);
   }
   cluster.sync();
+  stamp(a, 11);
   if (rank == 0)
     for (int e = tid; e < gn * N * K; e += nth) a.Tf[(size_t)f0 * N * K + e] = Tsm[e];
 
@@ -932,6 +952,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
         a.Bp[o] = B[n];
       }
   }
+  __syncthreads();
+  stamp(a, 12);
 }
 
 // V update (engine.cpp:125-133), the only cross-bin reduction.  Grid:

@@ -62,6 +62,7 @@ struct BinArgs {
   int* fallbacks;
   int finish;  // 1 = cost only (first launch), 2 = Lambda update + cost
   int start;   // 1 = IP + T update + V weights
+  unsigned long long* trace;  // optional per-CTA phase timestamps [cta][16]
 };
 
 }  // namespace dfm
@@ -93,6 +94,8 @@ struct dfm_ctx {
   void (*kbin)(BinArgs) = nullptr;
   bool force_generic = false;
   int req_G = 0, req_CS = 0;
+  DBuf<unsigned long long> trace;
+  bool tracing = false;
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
   long long launches = 0;
@@ -238,6 +241,7 @@ void launch_bin(dfm_ctx* c, int finish, int start, int slot) {
   a.finish = finish;
   a.start = start;
   a.cost_out = c->cost_part.p + (size_t)slot * c->ngroups;
+  a.trace = c->tracing ? c->trace.p : nullptr;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(c->ngroups * c->CS);
   cfg.blockDim = dim3(c->threads);
@@ -604,6 +608,30 @@ int dfm_set_tiling(dfm_ctx* c, int bins_per_cta, int cluster_size) {
   }
   set_kernel_attrs(c);
   return DFM_OK;
+  DFM_API_END
+}
+
+int dfm_set_trace(dfm_ctx* c, int on) {
+  if (!c) return DFM_ERR_ARG;
+  DFM_API_BEGIN
+  DFM_CK(cudaSetDevice(c->device));
+  c->tracing = on != 0;
+  if (c->tracing) {
+    c->trace.alloc((size_t)c->ngroups * c->CS * 16);
+    DFM_CK(cudaMemset(c->trace.p, 0, sizeof(unsigned long long) * c->trace.n));
+  }
+  return (int)std::min<size_t>(c->trace.n, 0x7fffffff);
+  DFM_API_END
+}
+
+int dfm_get_trace(dfm_ctx* c, unsigned long long* out, int n) {
+  if (!c || !out) return DFM_ERR_ARG;
+  DFM_API_BEGIN
+  DFM_CK(cudaStreamSynchronize(c->stream));
+  const size_t m = std::min<size_t>(n, c->trace.n);
+  c->trace.download(out, m, c->stream);
+  DFM_CK(cudaStreamSynchronize(c->stream));
+  return (int)m;
   DFM_API_END
 }
 

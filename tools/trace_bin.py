@@ -1,0 +1,71 @@
+"""Phase breakdown of the fused bin kernel from its %globaltimer stamps.
+
+  python tools/trace_bin.py [--workload config1] [--tiling G,CS]
+
+Runs one steady-state EM step of the chosen BASELINE config with per-CTA
+tracing on and prints, per phase, the mean/max duration over CTAs, the CTA
+lifetime and how the CTAs spread over the kernel's span (waves)."""
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+PHASES = ["stage", "A:frames", "A:lambda-reduce", "B:frames", "B:logdet", "B:Q-accum", "B:Q-reduce",
+          "IP", "W-gather", "C:frames", "C:T-reduce", "D:frames"]
+
+
+def main():
+    import bench
+    import paper_2605_19388_b200 as dfm
+
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="config1")
+    ap.add_argument("--tiling", default="")
+    ap.add_argument("--generic", action="store_true")
+    args = ap.parse_args()
+    c = bench.CONFIGS[args.workload]
+    layout = dfm.BlockLayout(c["sizes"])
+    F, T, N, K = c["F"], c["T"], c["N"], c["K"]
+    x = dfm.generate_mixture(c["kind"], F, T, layout.total, N, K, bench.SEED_X)
+    init = dfm.random_init(F, T, layout, N, K, bench.SEED_INIT)
+    eng = dfm.Engine(F, T, layout, N, K)
+    lib = eng.lib
+    if args.generic:
+        dfm._capi.check(lib.dfm_force_generic(eng.ctx, 1))
+    if args.tiling:
+        g, cs = (int(v) for v in args.tiling.split(","))
+        eng.set_tiling(g, cs)
+    eng.set_obs(x)
+    eng.set_model(init.nmf, init.w0, init.lambda0)
+    dfm._capi.check(lib.dfm_prime(eng.ctx))
+    for _ in range(3):
+        dfm._capi.check(lib.dfm_bench_step(eng.ctx))
+    n = dfm._capi.check(lib.dfm_set_trace(eng.ctx, 1))
+    dfm._capi.check(lib.dfm_l2_flush(0))
+    dfm._capi.check(lib.dfm_bench_step(eng.ctx))
+    ms = lib.dfm_bench_last_ms(eng.ctx)
+    buf = np.zeros(n, dtype=np.uint64)
+    dfm._capi.check(lib.dfm_get_trace(eng.ctx, buf.ctypes.data_as(ctypes.c_void_p), n))
+    tr = buf.reshape(-1, 16)[:, :13].astype(np.int64)
+    t0 = tr[:, 0].min()
+    tr = tr - t0
+    d = np.diff(tr, axis=1) / 1e3  # us
+    life = (tr[:, 12] - tr[:, 0]) / 1e3
+    out = {"workload": args.workload, "tiling": eng.tiling(), "step_ms": ms, "ctas": int(tr.shape[0]),
+           "span_us": float(tr[:, 12].max() / 1e3), "cta_life_us_mean": float(life.mean()),
+           "cta_life_us_max": float(life.max()),
+           "phases_us_mean": {p: round(float(d[:, i].mean()), 3) for i, p in enumerate(PHASES)},
+           "phases_us_max": {p: round(float(d[:, i].max()), 3) for i, p in enumerate(PHASES)}}
+    starts = np.sort(tr[:, 0]) / 1e3
+    out["start_percentiles_us"] = [round(float(np.percentile(starts, q)), 1) for q in (0, 10, 25, 50, 75, 90, 100)]
+    print(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
