@@ -145,9 +145,9 @@ def dist_setup():
 
 
 def shard(F: int, world: int, rank: int):
-    base, rem = divmod(F, world)
-    f0 = rank * base + min(rank, rem)
-    return f0, f0 + base + (1 if rank < rem else 0)
+    from paper_2605_19388_b200.sharding import shard_bins
+
+    return shard_bins(F, world, rank)
 
 
 def cpu_baseline(c, x, init_d, threads: int, target_s: float = 15.0):
