@@ -26,6 +26,8 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -71,13 +73,50 @@ struct BinArgs {
 
 using namespace dfm;
 
-#define NCCL_CK(call)                                                          \
-  do {                                                                         \
-    ncclResult_t r_ = (call);                                                  \
-    if (r_ != ncclSuccess) {                                                   \
-      ::dfm::set_error(std::string(#call) + ": " + ncclGetErrorString(r_));    \
-      throw ::dfm::CudaError{DFM_ERR_NCCL};                                    \
-    }                                                                          \
+// NCCL is resolved lazily with dlopen: a process that already loaded
+// torch reuses torch's libnccl (the library never pins a second copy), and
+// single-GPU use needs no NCCL at all.
+namespace {
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+      api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+      api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+      api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+      api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+      api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy && api.GetErrorString;
+    }
+  }
+  if (!api.ok) {
+    ::dfm::set_error("libnccl.so.2 could not be loaded (needed for multi-GPU frequency sharding)");
+    throw ::dfm::CudaError{DFM_ERR_NCCL};
+  }
+  return api;
+}
+}  // namespace
+
+#define NCCL_CK(call)                                                              \
+  do {                                                                             \
+    ncclResult_t r_ = (call);                                                      \
+    if (r_ != ncclSuccess) {                                                       \
+      ::dfm::set_error(std::string(#call) + ": " + nccl().GetErrorString(r_));     \
+      throw ::dfm::CudaError{DFM_ERR_NCCL};                                        \
+    }                                                                              \
   } while (0)
 
 struct dfm_ctx {
@@ -267,7 +306,7 @@ void launch_vupd(dfm_ctx* c) {
   c->launches++;
   if (sharded) {
     const size_t nkt = (size_t)c->N * c->K * c->T;
-    NCCL_CK(ncclAllReduce(c->numden.p, c->numden.p, 2 * nkt, ncclDouble, ncclSum, c->comm, c->stream));
+    NCCL_CK(nccl().AllReduce(c->numden.p, c->numden.p, 2 * nkt, ncclDouble, ncclSum, c->comm, c->stream));
     k_vapply<<<(unsigned)((nkt + 255) / 256), 256, 0, c->stream>>>(nkt, c->numden.p, c->V.p, c->floor_);
     DFM_CK_LAUNCH();
     c->launches++;
@@ -360,7 +399,7 @@ dfm_ctx* dfm_create(int F, int T, int nblocks, const int* block_sizes, int N, in
 void dfm_destroy(dfm_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->comm) nccl().CommDestroy(c->comm);
   for (auto e : c->iter_ev) cudaEventDestroy(e);
   if (c->eb0) cudaEventDestroy(c->eb0);
   if (c->eb1) cudaEventDestroy(c->eb1);
@@ -460,7 +499,7 @@ int dfm_get_model(dfm_ctx* c, double* Tm, double* V, double* lam, double* w) {
 int dfm_nccl_get_unique_id(void* out128) {
   DFM_API_BEGIN
   ncclUniqueId id;
-  NCCL_CK(ncclGetUniqueId(&id));
+  NCCL_CK(nccl().GetUniqueId(&id));
   std::memcpy(out128, &id, sizeof(id));
   return DFM_OK;
   DFM_API_END
@@ -472,7 +511,7 @@ int dfm_comm_init(dfm_ctx* c, const void* uid, int nranks, int rank) {
   DFM_CK(cudaSetDevice(c->device));
   ncclUniqueId id;
   std::memcpy(&id, uid, sizeof(id));
-  NCCL_CK(ncclCommInitRank(&c->comm, nranks, id, rank));
+  NCCL_CK(nccl().CommInitRank(&c->comm, nranks, id, rank));
   c->nranks = nranks;
   c->rank = rank;
   return DFM_OK;
@@ -516,7 +555,7 @@ int dfm_fit(dfm_ctx* c, int iters, double* cost_trace, double* wall_seconds, dou
   if (c->comm && c->nranks > 1) {
     if (c->cost_sum.n < (size_t)iters + 1) c->cost_sum.alloc(iters + 1);
     c->cost_sum.upload(cost.data(), iters + 1, c->stream);
-    NCCL_CK(ncclAllReduce(c->cost_sum.p, c->cost_sum.p, iters + 1, ncclDouble, ncclSum, c->comm, c->stream));
+    NCCL_CK(nccl().AllReduce(c->cost_sum.p, c->cost_sum.p, iters + 1, ncclDouble, ncclSum, c->comm, c->stream));
     c->cost_sum.download(cost.data(), iters + 1, c->stream);
     DFM_CK(cudaStreamSynchronize(c->stream));
   }
