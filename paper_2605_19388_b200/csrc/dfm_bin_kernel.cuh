@@ -435,6 +435,35 @@ __device__ bool ip_sweep_fast(cd* W, IpWork<MB>& f, const cd* qb, double floor_)
   return true;
 }
 
+// Sum over the cluster's ranks (in rank order, so every CTA gets the same
+// bits) of the {a, b} pair at red[2 + 2q]: all remote DSMEM loads are issued
+// before the adds.
+__device__ __forceinline__ double2 cluster_pair_sum(cg::cluster_group& cl, double* red, int q, int CS) {
+  constexpr int kMaxCS = 16;
+  double2 v[kMaxCS];
+#pragma unroll
+  for (int r = 0; r < kMaxCS; ++r)
+    if (r < CS) v[r] = *reinterpret_cast<const double2*>(cl.map_shared_rank(red, r) + 2 + 2 * q);
+  double x = 0.0, y = 0.0;
+#pragma unroll
+  for (int r = 0; r < kMaxCS; ++r)
+    if (r < CS) {
+      x += v[r].x;
+      y += v[r].y;
+    }
+  return make_double2(x, y);
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 __device__ __forceinline__ void stamp(const BinArgs& a, int phase) {
   if (a.trace && threadIdx.x == 0) {
     unsigned long long t;
@@ -443,7 +472,7 @@ __device__ __forceinline__ void stamp(const BinArgs& a, int phase) {
   }
 }
 
-template <int MB_, int NB_, int NS_, int MAXMB>
+template <int MB_, int NB_, int NS_, int NK_, int MAXMB>
 __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
   constexpr bool SB = MB_ > 0 && NB_ > 0;  // uniform, compile-time layout
   extern __shared__ __align__(16) unsigned char smem[];
@@ -459,7 +488,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
   const int M = SB ? MB_ * NB_ : a.M;
   const int nb = SB ? NB_ : a.nb;
   const int N = NS_ > 0 ? NS_ : a.N;
-  const int K = a.K, T = a.T, Tsp = a.Tsp;
+  const int K = NK_ > 0 ? NK_ : a.K;
+  const int T = a.T, Tsp = a.Tsp;
   const int wsz = SB ? MB_ * MB_ * NB_ : a.wsz;
   auto MBof = [&](int b) { return SB ? MB_ : a.mb[b]; };
   auto OFF = [&](int b) { return SB ? b * MB_ : a.off[b]; };
@@ -483,16 +513,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
 
   // ---- stage the X slice ([m][t], conflict-free frame-parallel access) and
   // the per-bin parameters
+  // asynchronous copies (cp.async): every load of the slice is in flight at once
   for (int g = 0; g < gn; ++g) {
     const cd* src = a.x + ((size_t)(f0 + g) * T + t0) * M;
     for (int e = tid; e < tn * M; e += nth) {
       const int t = e / M, m = e - t * M;
-      xs[(g * M + m) * Tsp + t] = src[e];
+      cp_async16(&xs[(g * M + m) * Tsp + t], src + e);
     }
   }
-  for (int e = tid; e < gn * N * K; e += nth) Tsm[e] = a.Tf[(size_t)f0 * N * K + e];
-  for (int e = tid; e < gn * N * M; e += nth) Lsm[e] = a.lam[(size_t)f0 * N * M + e];
-  for (int e = tid; e < gn * wsz; e += nth) Wsm[e] = a.W[(size_t)f0 * wsz + e];
+  for (int e = tid; e < gn * N * K; e += nth) cp_async8(&Tsm[e], a.Tf + (size_t)f0 * N * K + e);
+  for (int e = tid; e < gn * N * M; e += nth) cp_async8(&Lsm[e], a.lam + (size_t)f0 * N * M + e);
+  for (int e = tid; e < gn * wsz; e += nth) cp_async16(&Wsm[e], a.W + (size_t)f0 * wsz + e);
+  cp_async_wait_all();
   __syncthreads();
   stamp(a, 1);
 
@@ -505,8 +537,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
       if (n < N) {
         const double* tr = Tsm + (g * N + n) * K;
         const double* vr = a.V + n * K * T + t0 + t;
+        if constexpr (NK_ > 0) {
+          double v[NK_];
+#pragma unroll
+          for (int k = 0; k < NK_; ++k) v[k] = __ldg(vr + k * T);
+#pragma unroll
+          for (int k = 0; k < NK_; ++k) s += tr[k] * v[k];
+        } else {
 #pragma unroll 4
-        for (int k = 0; k < K; ++k) s += tr[k] * __ldg(vr + k * T);
+          for (int k = 0; k < K; ++k) s += tr[k] * __ldg(vr + k * T);
+        }
       }
       h[n] = s;
     }
@@ -582,14 +622,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
     }
     cluster.sync();
     for (int q = tid; q < gn * N * M; q += nth) {
-      double num = 0.0, den = 0.0;
-      for (int r = 0; r < CS; ++r) {
-        const double* rr = cluster.map_shared_rank(red, r);
-        num += rr[2 + 2 * q];
-        den += rr[2 + 2 * q + 1];
-      }
+      const double2 nd = cluster_pair_sum(cluster, red, q, CS);
       double& l = Lsm[q];
-      l = fmax(l * sqrt(num / fmax(den, floor_)), floor_);
+      l = fmax(l * sqrt(nd.x / fmax(nd.y, floor_)), floor_);
     }
     cluster.sync();
     stamp(a, 3);
@@ -756,22 +791,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
   }
   cluster.sync();
   if (rank == 0 && tid == 0) {
-    double c = 0.0;
-    for (int r = 0; r < CS; ++r) {
-      const double* rr = cluster.map_shared_rank(red, r);
-      c += rr[0] + rr[1];
-    }
-    a.cost_out[grp] = c;
+    const double2 c = cluster_pair_sum(cluster, red, -1, CS);  // red[0], red[1]
+    a.cost_out[grp] = c.x + c.y;
   }
   if (a.start) {
     for (int q = tid; q < gn * a.qper; q += nth) {
-      double re = 0.0, im = 0.0;
-      for (int r = 0; r < CS; ++r) {
-        const double* rr = cluster.map_shared_rank(red, r);
-        re += rr[2 + 2 * q];
-        im += rr[2 + 2 * q + 1];
-      }
-      Qsum[q] = cd{re / (double)T, im / (double)T};
+      const double2 v = cluster_pair_sum(cluster, red, q, CS);
+      Qsum[q] = cd{v.x / (double)T, v.y / (double)T};
     }
   }
   cluster.sync();
@@ -886,15 +912,22 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
 #pragma unroll
     for (int g = 0; g < kGMax; ++g) num[g] = den[g] = 0.0;
     const double* vr = a.V + (n * K + k) * T + t0;
-#pragma unroll 2
-    for (int t = 0; t < tn; ++t) {
-      const double v = __ldg(vr + t);
+    constexpr int kChunk = 8;  // V loads in flight per thread
+    for (int tb = 0; tb < tn; tb += kChunk) {
+      double v[kChunk];
 #pragma unroll
-      for (int g = 0; g < kGMax; ++g)
-        if (g < gn) {
-          num[g] += ab[(g * N + n) * Tsp + t] * v;
-          den[g] += bb[(g * N + n) * Tsp + t] * v;
-        }
+      for (int j = 0; j < kChunk; ++j) v[j] = tb + j < tn ? __ldg(vr + tb + j) : 0.0;
+#pragma unroll
+      for (int j = 0; j < kChunk; ++j) {
+        const int t = tb + j;
+        if (t < tn)
+#pragma unroll
+          for (int g = 0; g < kGMax; ++g)
+            if (g < gn) {
+              num[g] += ab[(g * N + n) * Tsp + t] * v[j];
+              den[g] += bb[(g * N + n) * Tsp + t] * v[j];
+            }
+      }
     }
 #pragma unroll
     for (int g = 0; g < kGMax; ++g)
@@ -906,13 +939,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
   }
   cluster.sync();
   for (int q = tid; q < gn * N * K; q += nth) {
-    double num = 0.0, den = 0.0;
-    for (int r = 0; r < CS; ++r) {
-      const double* rr = cluster.map_shared_rank(red, r);
-      num += rr[2 + 2 * q];
-      den += rr[2 + 2 * q + 1];
-    }
-    Tsm[q] = fmax(Tsm[q] * sqrt(num / fmax(den, floor_)), floor_);
+    const double2 nd = cluster_pair_sum(cluster, red, q, CS);
+    Tsm[q] = fmax(Tsm[q] * sqrt(nd.x / fmax(nd.y, floor_)), floor_);
   }
   cluster.sync();
   stamp(a, 11);

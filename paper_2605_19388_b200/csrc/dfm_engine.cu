@@ -201,14 +201,14 @@ void select_kernel(dfm_ctx* c) {
   const int mb = c->L.mb[0], nb = c->L.nb, N = c->N;
   c->kbin = nullptr;
   if (uniform && !c->force_generic) {
-    if (mb == 4 && nb == 3 && N == 5) { c->kbin = k_bin<4, 3, 5, 4>; c->kmaxmb = 4; }
-    else if (mb == 2 && nb == 2 && N == 3) { c->kbin = k_bin<2, 2, 3, 2>; c->kmaxmb = 2; }
-    else if (mb == 4 && nb == 8 && N == 8) { c->kbin = k_bin<4, 8, 8, 4>; c->kmaxmb = 4; }
-    else if (mb == 12 && nb == 1 && N == 5) { c->kbin = k_bin<12, 1, 5, 12>; c->kmaxmb = 12; }
+    if (mb == 4 && nb == 3 && N == 5 && c->K == 16) { c->kbin = k_bin<4, 3, 5, 16, 4>; c->kmaxmb = 4; }
+    else if (mb == 2 && nb == 2 && N == 3 && c->K == 4) { c->kbin = k_bin<2, 2, 3, 4, 2>; c->kmaxmb = 2; }
+    else if (mb == 4 && nb == 8 && N == 8 && c->K == 32) { c->kbin = k_bin<4, 8, 8, 32, 4>; c->kmaxmb = 4; }
+    else if (mb == 12 && nb == 1 && N == 5 && c->K == 16) { c->kbin = k_bin<12, 1, 5, 16, 12>; c->kmaxmb = 12; }
   }
   if (!c->kbin) {
-    if (c->maxmb <= 4) { c->kbin = k_bin<0, 0, 0, 4>; c->kmaxmb = 4; }
-    else { c->kbin = k_bin<0, 0, 0, DFM_MAX_MB>; c->kmaxmb = DFM_MAX_MB; }
+    if (c->maxmb <= 4) { c->kbin = k_bin<0, 0, 0, 0, 4>; c->kmaxmb = 4; }
+    else { c->kbin = k_bin<0, 0, 0, 0, DFM_MAX_MB>; c->kmaxmb = DFM_MAX_MB; }
   }
 }
 
