@@ -12,7 +12,7 @@ namespace dfm {
 
 // Shared-memory carve-up, identical on host and device.
 struct SmemPlan {
-  size_t xs, ps, es, tsm, lsm, wsm, qsum, red, hs, ab, bb, qpart, ipscr, total;
+  size_t xs, ps, es, tsm, lsm, wsm, qsum, red, hs, ab, bb, qpart, ipscr, wsum, ldet, total;
   int nwarps, nitems, nred;
 };
 
@@ -44,6 +44,8 @@ __host__ __device__ inline SmemPlan plan_smem(const BinArgs& a, int nthreads) {
   // one fallback / LU scratch per system owned by this CTA (ceil(G*nb / CS))
   const int nsys = (a.G * a.nb + a.CS - 1) / a.CS;
   p.ipscr = o; o += (size_t)(nsys > p.nwarps ? nsys : p.nwarps) * ipscr_bytes<MAXMB>();
+  p.wsum = o; o += al(32 * sizeof(double));
+  p.ldet = o; o += al((size_t)(nsys > 1 ? nsys : 1) * sizeof(double));
   // union: {hs, ab, bb} | qpart
   const size_t u1 = 3 * al(G * N * Tsp * sizeof(double));
   const size_t slots = (size_t)(nthreads > p.nitems ? nthreads : p.nitems);
@@ -472,6 +474,106 @@ __device__ __forceinline__ void stamp(const BinArgs& a, int phase) {
   }
 }
 
+// Quad-cooperative version of ip_sweep_fast: the MB (<= 4) lanes of one
+// 4-lane segment own rows l of the triangular solves, of Q u, of the
+// residual and of the Sherman-Morrison update, exchanging values with
+// width-4 shuffles.  Same algebra and the same reference residual test as
+// ip_sweep_fast; every early exit is uniform across the quad.
+__device__ __forceinline__ cd shfl4(unsigned mask, cd v, int src) {
+  return cd{__shfl_sync(mask, v.re, src, 4), __shfl_sync(mask, v.im, src, 4)};
+}
+
+template <int MB>
+__device__ bool ip_sweep_quad(cd* W, IpWork<MB>& f, const cd* qb, double floor_, int l, unsigned mask) {
+  constexpr int E = MB * (MB + 1) / 2;
+  bool okall = true;
+#pragma unroll
+  for (int mu = 0; mu < MB; ++mu) okall = okall && f.ok[mu];
+  if (!okall) return false;
+  auto Li = [](int r, int c) { return r * (r + 1) / 2 + c; };
+  const bool act = l < MB;
+  const int la = act ? l : 0;
+#pragma unroll 1
+  for (int mu = 0; mu < MB; ++mu) {
+    const cd* L = f.L[mu];
+    const double* di = f.dinv[mu];
+    const cd* qp = qb + mu * E;
+    auto Q = [&](int r, int c) -> cd { return r <= c ? qp[c * (c + 1) / 2 + r] : conjg(qp[r * (r + 1) / 2 + c]); };
+    // forward: L y = b, b_l = conj(Winv(mu, l))
+    cd acc = act ? conjg(f.Winv[la * MB + mu]) : cd{0.0, 0.0};
+    cd y{0.0, 0.0};
+#pragma unroll
+    for (int c = 0; c < MB; ++c) {
+      if (l == c) y = acc * di[c];
+      const cd yc = shfl4(mask, y, c);
+      if (act && l > c) acc = acc - L[Li(la, c)] * yc;
+    }
+    // backward: L^H u = y
+    acc = y;
+    cd u{0.0, 0.0};
+#pragma unroll
+    for (int c = MB - 1; c >= 0; --c) {
+      if (l == c) u = acc * di[c];
+      const cd uc = shfl4(mask, u, c);
+      if (act && l < c) acc = acc - cmulc(L[Li(c, la)], uc);
+    }
+    cd uv[MB];
+    bool fin = true;
+#pragma unroll
+    for (int c = 0; c < MB; ++c) {
+      uv[c] = shfl4(mask, u, c);
+      fin = fin && cfinite(uv[c]);
+    }
+    cd qu{0.0, 0.0};
+    if (act)
+#pragma unroll
+      for (int c = 0; c < MB; ++c) qu = qu + Q(la, c) * uv[c];
+    cd quv[MB];
+#pragma unroll
+    for (int c = 0; c < MB; ++c) quv[c] = shfl4(mask, qu, c);
+    double r2 = 0.0, nq = 0.0;
+    if (act) {
+      cd r{0.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < MB; ++k) r = r + cmulc(W[la * MB + k], quv[k]);
+      if (l == mu) r.re -= 1.0;
+      r2 = norm2(r);
+      nq = cmulc(u, qu).re;
+    }
+    r2 += __shfl_xor_sync(mask, r2, 1, 4);
+    r2 += __shfl_xor_sync(mask, r2, 2, 4);
+    nq += __shfl_xor_sync(mask, nq, 1, 4);
+    nq += __shfl_xor_sync(mask, nq, 2, 4);
+    if (!fin || !(sqrt(r2) <= 1e-6)) return false;
+    const double sc = sqrt(fmax(nq, floor_));
+    const cd un = cdivr(u, sc);
+    const cd d = act ? un - W[mu * MB + la] : cd{0.0, 0.0};
+    cd dv[MB];
+#pragma unroll
+    for (int c = 0; c < MB; ++c) dv[c] = shfl4(mask, d, c);
+    cd z{0.0, 0.0};
+    if (act)
+#pragma unroll
+      for (int c = 0; c < MB; ++c) z = z + f.Winv[c * MB + la] * dv[c];
+    const cd zmu = shfl4(mask, z, mu);
+    const cd den{1.0 + zmu.re, zmu.im};
+    const double dn = norm2(den);
+    if (!(dn > 0.0)) return false;
+    const cd iden{den.re / dn, -den.im / dn};
+    cd row[MB];
+#pragma unroll
+    for (int c = 0; c < MB; ++c) row[c] = f.Winv[c * MB + mu] * iden;
+    __syncwarp(mask);
+    if (act) {
+#pragma unroll
+      for (int c = 0; c < MB; ++c) f.Winv[c * MB + la] = f.Winv[c * MB + la] - z * row[c];
+      W[mu * MB + la] = un;
+    }
+    __syncwarp(mask);
+  }
+  return true;
+}
+
 template <int MB_, int NB_, int NS_, int NK_, int MAXMB>
 __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
   constexpr bool SB = MB_ > 0 && NB_ > 0;  // uniform, compile-time layout
@@ -665,31 +767,36 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
   }
   cost += lacc.value();
   cost = warp_sum(cost);
-  __syncthreads();  // hs is dead from here on: its union slot is reused
-  stamp(a, 4);
-  double* wsum = (double*)(smem + sp.qpart);
+  double* wsum = (double*)(smem + sp.wsum);
+  double* ldet = (double*)(smem + sp.ldet);
   if ((tid & 31) == 0) wsum[tid >> 5] = cost;
-  __syncthreads();
+  __syncthreads();  // hs is dead from here on: its union slot is reused by qpart
+  stamp(a, 4);
   if (tid == 0) {
     double c = 0.0;
     for (int w = 0; w < sp.nwarps; ++w) c += wsum[w];
     red[0] = c;
   }
-  // 2 ln|det W| of the pre-IP demixers, each (bin, block) by its owner rank
-  double det = 0.0;
+  // 2 ln|det W| (and W^-1 for the fast IP path) of the pre-IP demixers, each
+  // (bin, block) by its owner rank.  In the static path this runs on the
+  // highest-numbered threads, concurrently with the Q accumulation below.
   const int per_rank = (nsys + CS - 1) / CS;
   if constexpr (SB && MB_ <= 4) {
-    for (int i = tid; i < per_rank; i += nth) {
+    for (int i = nth - 1 - tid; i < per_rank; i += nth) {
       const int s = rank + CS * i;
-      if (s >= nsys) break;
+      if (s >= nsys) {
+        ldet[i] = 0.0;
+        continue;
+      }
       const int g = s / nb, b = s - g * nb;
       IpWork<MB_>& w = *(IpWork<MB_>*)(smem + sp.ipscr + i * ipscr_bytes<MAXMB>());
       const cd* wb = Wsm + g * wsz + b * MB_ * MB_;
 #pragma unroll
       for (int e = 0; e < MB_ * MB_; ++e) w.Wold[e] = wb[e];
-      det += logdet2_inverse_thread<MB_>(wb, w.Winv);
+      ldet[i] = logdet2_inverse_thread<MB_>(wb, w.Winv);
     }
   } else {
+    double det = 0.0;
     const int warp = tid >> 5, lane = tid & 31;
     for (int i = warp; i < per_rank; i += sp.nwarps) {
       const int s = rank + CS * i;
@@ -712,18 +819,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
       if (lane == 0) det += sing ? -INFINITY : 2.0 * acc;
       __syncwarp();
     }
+    __syncthreads();
+    if (lane == 0) wsum[warp] = det;
+    __syncthreads();
+    if (tid == 0) {
+      double d = 0.0;
+      for (int w = 0; w < sp.nwarps; ++w) d += wsum[w];
+      ldet[0] = d;
+    }
   }
-  // block sum of the owned log-dets (fixed order)
-  det = warp_sum(det);
-  __syncthreads();
-  if ((tid & 31) == 0) wsum[tid >> 5] = det;
-  __syncthreads();
-  if (tid == 0) {
-    double d = 0.0;
-    for (int w = 0; w < sp.nwarps; ++w) d += wsum[w];
-    red[1] = -(double)T * d;
-  }
-  __syncthreads();
   stamp(a, 5);
 
   // Q accumulation: every (bin, block, Hermitian entry r<=c) item sums, for
@@ -789,6 +893,13 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
       red[2 + 2 * dst + 1] = sum.im;
     }
   }
+  __syncthreads();  // owned log-dets are complete
+  if (tid == 0) {
+    double d = 0.0;
+    const int nl = (SB && MB_ <= 4) ? per_rank : 1;
+    for (int i = 0; i < nl; ++i) d += ldet[i];
+    red[1] = -(double)T * d;
+  }
   cluster.sync();
   if (rank == 0 && tid == 0) {
     const double2 c = cluster_pair_sum(cluster, red, -1, CS);  // red[0], red[1]
@@ -821,20 +932,25 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
         w.ok[mu] = chol_thread<MB_>(Qsum + g * a.qper + a.qofs[b] + mu * E, w.L[mu], w.dinv[mu]) ? 1 : 0;
       }
       __syncthreads();
-      for (int i = tid; i < per_rank; i += nth) {
+      // one 4-lane segment per owned system
+      const int l = tid & 3;
+      const unsigned qmask = 0xFu << (tid & 28);
+      for (int i = tid >> 2; i < per_rank; i += nth >> 2) {
         const int s = rank + CS * i;
         if (s >= nsys) break;
         const int g = s / nb, b = s - g * nb;
         IpWork<MB_>& w = *(IpWork<MB_>*)(smem + sp.ipscr + i * ipscr_bytes<MAXMB>());
         cd* wb = Wsm + g * wsz + b * MB_ * MB_;
         const cd* qb = Qsum + g * a.qper + a.qofs[b];
-        if (!ip_sweep_fast<MB_>(wb, w, qb, floor_)) {
+        const bool ok = ip_sweep_quad<MB_>(wb, w, qb, floor_, l, qmask);
+        if (!ok && l == 0) {
           // exact path (engine.cpp:47-49: LU, residual test, pinv) from W_old
 #pragma unroll
           for (int e = 0; e < MB_ * MB_; ++e) wb[e] = w.Wold[e];
           fbs = ip_solve_thread<MB_>(wb, qb, floor_, w.slow);
           if (fbs) atomicAdd(a.fallbacks, fbs);
         }
+        __syncwarp(qmask);
       }
     } else {
       const int warp = tid >> 5, lane = tid & 31;
