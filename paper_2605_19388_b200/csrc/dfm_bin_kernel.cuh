@@ -43,7 +43,8 @@ __host__ __device__ inline SmemPlan plan_smem(const BinArgs& a, int nthreads) {
   p.red = o; o += al((nred + 2) * sizeof(double));
   // one fallback / LU scratch per system owned by this CTA (ceil(G*nb / CS))
   const int nsys = (a.G * a.nb + a.CS - 1) / a.CS;
-  p.ipscr = o; o += (size_t)(nsys > p.nwarps ? nsys : p.nwarps) * ipscr_bytes<MAXMB>();
+  const int nscr = nsys > 1 ? nsys : 1;  // one scratch per owned system
+  p.ipscr = o; o += (size_t)nscr * ipscr_bytes<MAXMB>();
   p.wsum = o; o += al(32 * sizeof(double));
   p.ldet = o; o += al((size_t)(nsys > 1 ? nsys : 1) * sizeof(double));
   // union: {hs, ab, bb} | qpart
@@ -802,7 +803,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
       const int s = rank + CS * i;
       if (s >= nsys) break;
       const int g = s / nb, b = s - g * nb, mb = MBof(b);
-      IpScratch<MAXMB>& sc = *(IpScratch<MAXMB>*)(smem + sp.ipscr + warp * ipscr_bytes<MAXMB>());
+      IpScratch<MAXMB>& sc = *(IpScratch<MAXMB>*)(smem + sp.ipscr + i * ipscr_bytes<MAXMB>());
       const cd* wb = Wsm + g * wsz + WOFF(b);
       for (int e = lane; e < mb * mb; e += 32) sc.S[e] = wb[e];
       __syncwarp();
@@ -960,7 +961,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
         fbs = 0;
         const int g = s / nb, b = s - g * nb, mb = MBof(b);
         const int E = mb * (mb + 1) / 2;
-        IpScratch<MAXMB>& sc = *(IpScratch<MAXMB>*)(smem + sp.ipscr + warp * ipscr_bytes<MAXMB>());
+        IpScratch<MAXMB>& sc = *(IpScratch<MAXMB>*)(smem + sp.ipscr + i * ipscr_bytes<MAXMB>());
         cd* wb = Wsm + g * wsz + WOFF(b);
         for (int mu = 0; mu < mb; ++mu) {
           const cd* qp = Qsum + g * a.qper + a.qofs[b] + mu * E;
@@ -1020,37 +1021,46 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
   }
   __syncthreads();
   stamp(a, 10);
-  // T numerator / denominator (engine.cpp:117-118): one thread per (n, k);
-  // each V row is read once and reused for all G bins of the group
-  for (int q = tid; q < N * K; q += nth) {
-    const int n = q / K, k = q - n * K;
-    double num[kGMax], den[kGMax];
+  // T numerator / denominator (engine.cpp:117-118), warp-cooperative: a warp
+  // takes RB (n, k) rows at a time, its lanes run over the frames (coalesced
+  // V loads, all RB rows in flight), then each row is summed over lanes with
+  // a fixed shuffle tree.  V rows are reused for all G bins of the group.
+  {
+    constexpr int RB = 8;
+    const int warp = tid >> 5, lane = tid & 31, nwarps = nth >> 5;
+    const int nrows = N * K;
+    for (int g = 0; g < gn; ++g)
+      for (int r0 = warp * RB; r0 < nrows; r0 += nwarps * RB) {
+        double num[RB], den[RB];
 #pragma unroll
-    for (int g = 0; g < kGMax; ++g) num[g] = den[g] = 0.0;
-    const double* vr = a.V + (n * K + k) * T + t0;
-    constexpr int kChunk = 8;  // V loads in flight per thread
-    for (int tb = 0; tb < tn; tb += kChunk) {
-      double v[kChunk];
+        for (int j = 0; j < RB; ++j) num[j] = den[j] = 0.0;
+        for (int tb = 0; tb < tn; tb += 32) {
+          const int t = tb + lane;
+          double v[RB];
 #pragma unroll
-      for (int j = 0; j < kChunk; ++j) v[j] = tb + j < tn ? __ldg(vr + tb + j) : 0.0;
+          for (int j = 0; j < RB; ++j) {
+            const int q = r0 + j;
+            v[j] = (q < nrows && t < tn) ? __ldg(a.V + q * T + t0 + t) : 0.0;
+          }
+          if (t < tn)
 #pragma unroll
-      for (int j = 0; j < kChunk; ++j) {
-        const int t = tb + j;
-        if (t < tn)
-#pragma unroll
-          for (int g = 0; g < kGMax; ++g)
-            if (g < gn) {
-              num[g] += ab[(g * N + n) * Tsp + t] * v[j];
-              den[g] += bb[(g * N + n) * Tsp + t] * v[j];
+            for (int j = 0; j < RB; ++j) {
+              const int n = min((r0 + j) / K, N - 1);
+              num[j] += ab[(g * N + n) * Tsp + t] * v[j];
+              den[j] += bb[(g * N + n) * Tsp + t] * v[j];
             }
-      }
-    }
+        }
 #pragma unroll
-    for (int g = 0; g < kGMax; ++g)
-      if (g < gn) {
-        const int o = (g * N + n) * K + k;
-        red[2 + 2 * o] = num[g];
-        red[2 + 2 * o + 1] = den[g];
+        for (int j = 0; j < RB; ++j) {
+          const double x = warp_sum(num[j]);
+          const double y = warp_sum(den[j]);
+          const int q = r0 + j;
+          if (lane == 0 && q < nrows) {
+            const int o = g * N * K + q;
+            red[2 + 2 * o] = x;
+            red[2 + 2 * o + 1] = y;
+          }
+        }
       }
   }
   cluster.sync();
