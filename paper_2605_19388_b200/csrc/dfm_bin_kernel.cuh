@@ -12,8 +12,8 @@ namespace dfm {
 
 // Shared-memory carve-up, identical on host and device.
 struct SmemPlan {
-  size_t xs, ps, es, tsm, lsm, wsm, qsum, red, hs, ab, bb, qpart, ipscr, wsum, ldet, total;
-  int nwarps, nitems, nred;
+  size_t xs, ps, es, tsm, lsm, wsm, qsum, pushA, pushB, hs, ab, bb, qpart, ipscr, wsum, ldet, total;
+  int nwarps, nitems, nA, nB;
 };
 
 template <int MB>
@@ -36,11 +36,16 @@ __host__ __device__ inline SmemPlan plan_smem(const BinArgs& a, int nthreads) {
   p.lsm = o; o += al(G * N * M * sizeof(double));
   p.wsm = o; o += al(G * a.wsz * sizeof(cd));
   p.qsum = o; o += al((size_t)G * a.qper * sizeof(cd));
-  size_t nred = 2 * G * N * M;
-  nred = nred > 2 * (size_t)G * a.qper ? nred : 2 * (size_t)G * a.qper;
-  nred = nred > 2 * G * N * K ? nred : 2 * G * N * K;
-  p.nred = (int)nred;
-  p.red = o; o += al((nred + 2) * sizeof(double));
+  // push buffers: every CTA stores its partials into slot [its rank] of every
+  // peer's buffer, so one cluster barrier completes a reduction
+  size_t nA = 2 * G * N * M;
+  nA = nA > 2 * G * N * K ? nA : 2 * G * N * K;
+  nA = (nA + 1) / 2 * 2;
+  const size_t nB = 2 + 2 * (size_t)G * a.qper;
+  p.nA = (int)nA;
+  p.nB = (int)nB;
+  p.pushA = o; o += al((size_t)a.CS * nA * sizeof(double));
+  p.pushB = o; o += al((size_t)a.CS * nB * sizeof(double));
   // one fallback / LU scratch per system owned by this CTA (ceil(G*nb / CS))
   const int nsys = (a.G * a.nb + a.CS - 1) / a.CS;
   const int nscr = nsys > 1 ? nsys : 1;  // one scratch per owned system
@@ -438,22 +443,23 @@ __device__ bool ip_sweep_fast(cd* W, IpWork<MB>& f, const cd* qb, double floor_)
   return true;
 }
 
-// Sum over the cluster's ranks (in rank order, so every CTA gets the same
-// bits) of the {a, b} pair at red[2 + 2q]: all remote DSMEM loads are issued
-// before the adds.
-__device__ __forceinline__ double2 cluster_pair_sum(cg::cluster_group& cl, double* red, int q, int CS) {
-  constexpr int kMaxCS = 16;
-  double2 v[kMaxCS];
-#pragma unroll
-  for (int r = 0; r < kMaxCS; ++r)
-    if (r < CS) v[r] = *reinterpret_cast<const double2*>(cl.map_shared_rank(red, r) + 2 + 2 * q);
+// Store the pair {x, y} at item q of this rank's slot in every peer's push
+// buffer (fire-and-forget distributed-shared-memory stores).
+__device__ __forceinline__ void push_pair(cg::cluster_group& cl, double* buf, int nslot, int q, double x,
+                                          double y, int rank, int CS) {
+  const double2 v = make_double2(x, y);
+  for (int r = 0; r < CS; ++r)
+    *reinterpret_cast<double2*>(cl.map_shared_rank(buf, r) + rank * nslot + 2 * q) = v;
+}
+// After the barrier: the pair sum over source ranks, in rank order (every
+// CTA of the cluster gets the same bits).
+__device__ __forceinline__ double2 local_pair_sum(const double* buf, int nslot, int q, int CS) {
   double x = 0.0, y = 0.0;
-#pragma unroll
-  for (int r = 0; r < kMaxCS; ++r)
-    if (r < CS) {
-      x += v[r].x;
-      y += v[r].y;
-    }
+  for (int r = 0; r < CS; ++r) {
+    const double2 v = *reinterpret_cast<const double2*>(buf + r * nslot + 2 * q);
+    x += v.x;
+    y += v.y;
+  }
   return make_double2(x, y);
 }
 
@@ -605,7 +611,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
   double* Lsm = (double*)(smem + sp.lsm);  // [g][n][m]
   cd* Wsm = (cd*)(smem + sp.wsm);          // [g][wsz]
   cd* Qsum = (cd*)(smem + sp.qsum);        // [g][qper]
-  double* red = (double*)(smem + sp.red);  // [2 + nred]
+  double* pushA = (double*)(smem + sp.pushA);  // [CS][nA]  Lambda, T partials
+  double* pushB = (double*)(smem + sp.pushB);  // [CS][nB]  cost + Q partials
   double* hs = (double*)(smem + sp.hs);    // [g][n][Tsp]
   double* ab = (double*)(smem + sp.ab);    // [g][n][Tsp]
   double* bb = (double*)(smem + sp.bb);    // [g][n][Tsp]
@@ -720,16 +727,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
         num += hr[t] * z;
         den += hr[t] * ie;
       }
-      red[2 + 2 * q] = num;
-      red[2 + 2 * q + 1] = den;
+      push_pair(cluster, pushA, sp.nA, q, num, den, rank, CS);
     }
     cluster.sync();
     for (int q = tid; q < gn * N * M; q += nth) {
-      const double2 nd = cluster_pair_sum(cluster, red, q, CS);
+      const double2 nd = local_pair_sum(pushA, sp.nA, q, CS);
       double& l = Lsm[q];
       l = fmax(l * sqrt(nd.x / fmax(nd.y, floor_)), floor_);
     }
-    cluster.sync();
+    __syncthreads();
     stamp(a, 3);
     if (rank == 0)
       for (int e = tid; e < gn * N * M; e += nth) a.lam[(size_t)f0 * N * M + e] = Lsm[e];
@@ -773,11 +779,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
   if ((tid & 31) == 0) wsum[tid >> 5] = cost;
   __syncthreads();  // hs is dead from here on: its union slot is reused by qpart
   stamp(a, 4);
-  if (tid == 0) {
-    double c = 0.0;
-    for (int w = 0; w < sp.nwarps; ++w) c += wsum[w];
-    red[0] = c;
-  }
+  double frame_cost = 0.0;  // valid in thread 0
+  if (tid == 0)
+    for (int w = 0; w < sp.nwarps; ++w) frame_cost += wsum[w];
   // 2 ln|det W| (and W^-1 for the fast IP path) of the pre-IP demixers, each
   // (bin, block) by its owner rank.  In the static path this runs on the
   // highest-numbered threads, concurrently with the Q accumulation below.
@@ -890,8 +894,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
       for (int ss = 0; ss < S; ++ss) sum = sum + qpart[(ss * nitems + it) * MAXMB + mu];
       const int E = mb * (mb + 1) / 2;
       const int dst = g * a.qper + a.qofs[b] + mu * E + rem;
-      red[2 + 2 * dst] = sum.re;
-      red[2 + 2 * dst + 1] = sum.im;
+      push_pair(cluster, pushB, sp.nB, 1 + dst, sum.re, sum.im, rank, CS);
     }
   }
   __syncthreads();  // owned log-dets are complete
@@ -899,20 +902,20 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
     double d = 0.0;
     const int nl = (SB && MB_ <= 4) ? per_rank : 1;
     for (int i = 0; i < nl; ++i) d += ldet[i];
-    red[1] = -(double)T * d;
+    push_pair(cluster, pushB, sp.nB, 0, frame_cost, -(double)T * d, rank, CS);
   }
   cluster.sync();
   if (rank == 0 && tid == 0) {
-    const double2 c = cluster_pair_sum(cluster, red, -1, CS);  // red[0], red[1]
+    const double2 c = local_pair_sum(pushB, sp.nB, 0, CS);
     a.cost_out[grp] = c.x + c.y;
   }
   if (a.start) {
     for (int q = tid; q < gn * a.qper; q += nth) {
-      const double2 v = cluster_pair_sum(cluster, red, q, CS);
+      const double2 v = local_pair_sum(pushB, sp.nB, 1 + q, CS);
       Qsum[q] = cd{v.x / (double)T, v.y / (double)T};
     }
   }
-  cluster.sync();
+  __syncthreads();
   stamp(a, 7);
   if (!a.start) return;
 
@@ -974,21 +977,20 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
       }
     }
   }
-  cluster.sync();
+  __syncthreads();
   stamp(a, 8);
-  // gather the systems owned by other ranks; owners write them back to HBM
-  for (int s = 0; s < nsys; ++s) {
-    const int owner = s % CS;
+  // owners push their solved demixers into every peer's Wsm and write HBM
+  for (int s = rank; s < nsys; s += CS) {
     const int g = s / nb, b = s - g * nb, mb = MBof(b);
-    cd* wb = Wsm + g * wsz + WOFF(b);
-    if (owner != rank) {
-      const cd* src = cluster.map_shared_rank(wb, owner);
-      for (int e = tid; e < mb * mb; e += nth) wb[e] = src[e];
-    } else {
-      for (int e = tid; e < mb * mb; e += nth) a.W[(size_t)(f0 + g) * wsz + WOFF(b) + e] = wb[e];
+    const cd* wb = Wsm + g * wsz + WOFF(b);
+    for (int e = tid; e < mb * mb; e += nth) {
+      const cd v = wb[e];
+      a.W[(size_t)(f0 + g) * wsz + WOFF(b) + e] = v;
+      for (int r = 0; r < CS; ++r)
+        if (r != rank) cluster.map_shared_rank(Wsm + g * wsz + WOFF(b), r)[e] = v;
     }
   }
-  cluster.sync();  // peers finished reading before anyone reuses shared memory
+  cluster.sync();
   stamp(a, 9);
 
   // ================================================================ pass C
@@ -1055,20 +1057,16 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
           const double x = warp_sum(num[j]);
           const double y = warp_sum(den[j]);
           const int q = r0 + j;
-          if (lane == 0 && q < nrows) {
-            const int o = g * N * K + q;
-            red[2 + 2 * o] = x;
-            red[2 + 2 * o + 1] = y;
-          }
+          if (lane == 0 && q < nrows) push_pair(cluster, pushA, sp.nA, g * N * K + q, x, y, rank, CS);
         }
       }
   }
   cluster.sync();
   for (int q = tid; q < gn * N * K; q += nth) {
-    const double2 nd = cluster_pair_sum(cluster, red, q, CS);
+    const double2 nd = local_pair_sum(pushA, sp.nA, q, CS);
     Tsm[q] = fmax(Tsm[q] * sqrt(nd.x / fmax(nd.y, floor_)), floor_);
   }
-  cluster.sync();
+  __syncthreads();
   stamp(a, 11);
   if (rank == 0)
     for (int e = tid; e < gn * N * K; e += nth) a.Tf[(size_t)f0 * N * K + e] = Tsm[e];
