@@ -904,6 +904,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
     for (int i = 0; i < nl; ++i) d += ldet[i];
     push_pair(cluster, pushB, sp.nB, 0, frame_cost, -(double)T * d, rank, CS);
   }
+  stamp(a, 14);
   cluster.sync();
   if (rank == 0 && tid == 0) {
     const double2 c = local_pair_sum(pushB, sp.nB, 0, CS);
@@ -1052,15 +1053,22 @@ __global__ void __launch_bounds__(kThreads, 2) k_bin(const BinArgs a) {
               den[j] += bb[(g * N + n) * Tsp + t] * v[j];
             }
         }
+        // every lane gets every row sum; lane j then pushes row j (the CS remote
+        // stores of a row are spread over lanes instead of serialised on lane 0)
+        double px = 0.0, py = 0.0;
 #pragma unroll
         for (int j = 0; j < RB; ++j) {
           const double x = warp_sum(num[j]);
           const double y = warp_sum(den[j]);
-          const int q = r0 + j;
-          if (lane == 0 && q < nrows) push_pair(cluster, pushA, sp.nA, g * N * K + q, x, y, rank, CS);
+          if (lane == j) {
+            px = x;
+            py = y;
+          }
         }
+        if (lane < RB && r0 + lane < nrows) push_pair(cluster, pushA, sp.nA, g * N * K + r0 + lane, px, py, rank, CS);
       }
   }
+  stamp(a, 13);
   cluster.sync();
   for (int q = tid; q < gn * N * K; q += nth) {
     const double2 nd = local_pair_sum(pushA, sp.nA, q, CS);

@@ -63,6 +63,11 @@ def main():
            "phases_us_mean": {p: round(float(d[:, i].mean()), 3) for i, p in enumerate(PHASES)},
            "phases_us_max": {p: round(float(d[:, i].max()), 3) for i, p in enumerate(PHASES)}}
     starts = np.sort(tr[:, 0]) / 1e3
+    raw = buf.reshape(-1, 16).astype(np.int64) - t0
+    out["T_partials_work_us"] = float(((raw[:, 13] - raw[:, 10]) / 1e3).mean())
+    out["T_barrier_wait_us"] = float(((raw[:, 11] - raw[:, 13]) / 1e3).mean())
+    out["Q_work_after_accum_us"] = float(((raw[:, 14] - raw[:, 6]) / 1e3).mean())
+    out["Q_barrier_wait_us"] = float(((raw[:, 7] - raw[:, 14]) / 1e3).mean())
     out["start_percentiles_us"] = [round(float(np.percentile(starts, q)), 1) for q in (0, 10, 25, 50, 75, 90, 100)]
     print(json.dumps(out, indent=1))
 
