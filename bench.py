@@ -52,11 +52,12 @@ def alg_bytes(c) -> float:
 
 
 def alg_bytes_bin_kernel(c) -> float:
-    """Compulsory bytes of the fused bin kernel alone: X once, T/Lambda/W read
-    and written, V read (the V update's own traffic excluded)."""
+    """Compulsory bytes of the per-bin kernel k_em_bin: X once, Lambda and W
+    read and written (its other traffic - H, the T-update weights, X re-reads
+    from L2 - is intermediate, not algorithmic)."""
     F, T, N, K, M = c["F"], c["T"], c["N"], c["K"], sum(c["sizes"])
     S2 = sum(s * s for s in c["sizes"])
-    return 16.0 * F * T * M + 8.0 * (2 * F * K * N + K * T * N + 2 * F * N * M) + 32.0 * F * S2
+    return 16.0 * F * T * M + 16.0 * F * N * M + 32.0 * F * S2
 
 
 def alg_flops(c) -> float:
@@ -229,7 +230,7 @@ def main():
     ap.add_argument("--workload", default="config1", choices=sorted(CONFIGS))
     ap.add_argument("--e2e-iters", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--tiling", default="", help="G,CS override of the bin-kernel tiling")
+    ap.add_argument("--tiling", default="", help="FT,TB override: frame tile of the per-bin kernel and of k_pd")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     c = CONFIGS[args.workload]
@@ -283,9 +284,9 @@ def main():
         ms = lib.dfm_bench_last_ms(ctx)
         import ctypes
 
-        a, b = ctypes.c_double(), ctypes.c_double()
-        lib.dfm_bench_last_split(ctx, ctypes.byref(a), ctypes.byref(b))
-        return ms, a.value, b.value
+        sp = (ctypes.c_double * 5)()
+        lib.dfm_bench_last_split(ctx, sp)
+        return ms, list(sp)
 
     dfm._capi.check(lib.dfm_prime(ctx))
     for _ in range(args.warmup):
@@ -296,12 +297,11 @@ def main():
     torch.cuda.synchronize()
     launches0 = eng.launches()
     sampler = ClockSampler(local).start()
-    t_ms, bin_ms, v_ms = [], [], []
+    t_ms, split = [], []
     for _ in range(args.steps):
-        ms, a, b = step()
+        ms, sp = step()
         t_ms.append(ms)
-        bin_ms.append(a)
-        v_ms.append(b)
+        split.append(sp)
     dfm._capi.check(lib.dfm_sync(ctx))
     torch.cuda.synchronize()
     clocks = sampler.stop()
@@ -349,7 +349,10 @@ def main():
         return
 
     pk = peaks()
-    bin_avg = float(np.mean(bin_ms))
+    split_avg = np.mean(np.array(split), axis=0)
+    names = ["k_em_bin", "k_tupd", "k_pd", "k_vupd", "k_spec"]
+    dom = int(np.argmax(split_avg))
+    bin_avg = float(split_avg[0])
     ab_bin = alg_bytes_bin_kernel(c) * (f1 - f0) / F
     achieved = ab_bin / (bin_avg * 1e-3) / 1e9
     fp64_peak = float(lib.dfm_probe_fp64_tflops(local))
@@ -359,7 +362,7 @@ def main():
     if os.path.exists(prof):
         try:
             with open(prof) as fh:
-                traffic = json.load(fh).get(args.workload, {}).get("k_bin_dram_bytes_per_launch")
+                traffic = json.load(fh).get(args.workload, {}).get("k_em_bin_dram_bytes_per_launch")
         except Exception:
             traffic = None
     line = {
@@ -373,14 +376,15 @@ def main():
                    "tiling": eng.tiling()},
         "iter_per_s": 1e3 / ms_step,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "kernel": "k_bin",
+                     "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "kernel": "k_em_bin",
                      "alg_bytes_per_launch": ab_bin, "kernel_ms": bin_avg, "peak_source": pk["source"]},
         "roofline_fp64": {"bound": "fp64", "achieved": fl, "peak": fp64_peak, "unit": "TFLOP/s",
                           "frac": fl / fp64_peak if fp64_peak > 0 else None,
                           "alg_flops_per_iter": alg_flops(c),
                           "peak_source": "measured in this run (DFMA microbenchmark, dfm_probe_fp64_tflops)"},
         "iteration_roofline": {"alg_bytes_per_iter": alg_bytes(c), "hbm_frac": alg_bytes(c) / (ms_step * 1e-3) / 1e9 / pk["hbm_gbs"]},
-        "kernel_split_ms": {"k_bin": bin_avg, "v_update": float(np.mean(v_ms))},
+        "kernel_split_ms": {n: float(v) for n, v in zip(names, split_avg)},
+        "dominant_kernel": names[dom],
         "e2e": {"value": e2e_value, "unit": "TF-bin*iter/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h),
                 "step": f"Engine.set_obs/set_model (pinned host X + init H2D), Engine.fit({args.e2e_iters}) "

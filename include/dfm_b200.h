@@ -96,30 +96,31 @@ int dfm_nccl_get_unique_id(void* out128);
  * cost_trace: iters+1 entries (initial cost first, FitReport::cost_trace);
  * wall_seconds: iters per-iteration device times (may be NULL);
  * stage_seconds[4] = {w_update, mm_update, eta, decorrelate} (may be NULL;
- * the fused kernels report the bin kernel under w_update and the
- * cross-bin V update under mm_update).  Returns the number of IP
+ * the fused kernels report the whole iteration under w_update).  Returns the number of IP
  * pinv fallbacks (>= 0) or an error code.
  * With a communicator the cost entries are the GLOBAL cost (allreduced). */
 int dfm_fit(dfm_ctx* ctx, int iters, double* cost_trace, double* wall_seconds,
             double* stage_seconds);
 
-/* Benchmark hooks: one steady-state EM iteration (fused bin kernel in
- * "finish previous + start next" mode, then the V update), enqueued on the
- * context stream; dfm_prime runs the first (cost-only) launch.  Device time
+/* Benchmark hooks: one steady-state EM iteration (per-bin kernel in
+ * "finish previous + start next" mode, T update, V weights, V update,
+ * spectrogram), enqueued on the context stream; dfm_prime runs the first
+ * (cost-only) launch.  Device time
  * of the last dfm_bench_step is returned by dfm_bench_last_ms. */
 int dfm_prime(dfm_ctx* ctx);
 int dfm_bench_step(dfm_ctx* ctx);
 int dfm_sync(dfm_ctx* ctx);
 double dfm_bench_last_ms(dfm_ctx* ctx);
-/* Split of the last dfm_bench_step: fused bin kernel vs V update (+ allreduce). */
-int dfm_bench_last_split(dfm_ctx* ctx, double* bin_ms, double* vupd_ms);
+/* Device time of each kernel of the last dfm_bench_step (ms):
+ * {k_em_bin, k_tupd, k_pd, k_vupd (+ allreduce), k_spec}. */
+int dfm_bench_last_split(dfm_ctx* ctx, double* ms5);
 /* Kernel launches issued by the context so far (for the bench's gpu_launches). */
 long long dfm_launch_count(const dfm_ctx* ctx);
 /* Tuning override for the fused bin kernel: bins per CTA group (G) and
  * cluster size (CTAs splitting T).  0 = heuristic. */
 int dfm_set_tiling(dfm_ctx* ctx, int bins_per_cta, int cluster_size);
-/* Profiling aid: per-CTA %globaltimer stamps at the phase boundaries of the
- * bin kernel (16 slots per CTA).  dfm_set_trace returns the buffer length. */
+/* Profiling aid: per-bin %globaltimer stamps at the phase boundaries of the
+ * per-bin kernel (16 slots per CTA).  dfm_set_trace returns the buffer length. */
 int dfm_set_trace(dfm_ctx* ctx, int on);
 int dfm_get_trace(dfm_ctx* ctx, unsigned long long* out, int n);
 /* Use the generic (runtime-shape) bin kernel even when a compile-time-shape

@@ -36,7 +36,7 @@ _SIGS = {
     "dfm_bench_step": (_i, [_vp]),
     "dfm_sync": (_i, [_vp]),
     "dfm_bench_last_ms": (_d, [_vp]),
-    "dfm_bench_last_split": (_i, [_vp, _dp, _dp]),
+    "dfm_bench_last_split": (_i, [_vp, _dp]),
     "dfm_launch_count": (C.c_longlong, [_vp]),
     "dfm_set_tiling": (_i, [_vp, _i, _i]),
     "dfm_get_tiling": (_i, [_vp, _ip, _ip, _ip, _ip, _ip]),

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdfm_b200.so")
 SOURCES = ["dfm_steps.cu", "dfm_engine.cu", "dfm_host.cpp"]
-HEADERS = ["dfm_common.cuh", "dfm_internal.cuh", "dfm_bin_kernel.cuh"]
+HEADERS = ["dfm_common.cuh", "dfm_internal.cuh", "dfm_ip.cuh", "dfm_em.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -1,0 +1,744 @@
+// The EM iteration as five kernels (restates src/engine.cpp:209-270).
+//
+//   k_spec    H = T V for every (bin, source, frame): a bin-tiled GEMM, so V
+//             is read once per tile of bins, not once per bin.
+//   k_em_bin  one CTA per bin, frames streamed from L2 in tiles of FT:
+//             [finish it-1] Lambda update (engine.cpp:135-148) + cost
+//             (:150-165); [start it] Q_mu of all mu from one pass over X
+//             (:42-45), IP sweep (:40-51), decorrelation (:60-69) and the
+//             T-update weights A, B (:89-113) written for k_tupd.
+//   k_tupd    T update (:115-123): per (bin, source) dots over frames.
+//   k_pd      h' = T_new V, eta' (:231-232) and the V-update weights A', B'
+//             (:236) for a tile of bins x frames (V tile shared by the bins).
+//   k_vupd    V update (:125-133), bins summed in order (dfm_bin_kernel.cuh).
+//
+// Every reduction has a fixed order; there are no floating-point atomics.
+#pragma once
+
+namespace dfm {
+
+struct EmArgs {
+  int F, T, M, N, K, nb, wsz;
+  int mb[DFM_MAX_BLOCKS], off[DFM_MAX_BLOCKS], woff[DFM_MAX_BLOCKS];
+  int eofs[DFM_MAX_BLOCKS], qofs[DFM_MAX_BLOCKS];
+  int etot, qper;
+  double floor_;
+  const cd* x;       // [F][T][M]
+  const double* H;   // [F][N][T]
+  double* lam;       // [F][N][M]
+  cd* W;             // [F][wsz]
+  double* Aw;        // [N][F][T] T-update weights (A)
+  double* Bw;        // [N][F][T] T-update weights (B)
+  double* cost_out;  // [F] per-bin cost of this launch's slot
+  int* fallbacks;
+  int finish;  // 1 = cost only (first launch), 2 = Lambda update + cost
+  int start;   // 1 = Q, IP, T-update weights
+  unsigned long long* trace;  // optional [bin][16] phase stamps
+};
+
+struct EmPlan {
+  size_t lsm, wsm, qsum, ipscr, red, wsum, ldet, tile, total;
+  int nwarps, SL, SQ, nitems;
+};
+
+template <int MAXMB>
+__host__ __device__ inline EmPlan plan_em(const EmArgs& a, int FT) {
+  EmPlan p;
+  auto al = [](size_t v) { return (v + 15) / 16 * 16; };
+  const size_t N = a.N, M = a.M;
+  p.nwarps = FT / 32;
+  const int NM = a.N * a.M;
+  p.SL = FT / NM > 1 ? FT / NM : 1;
+  p.nitems = a.etot;
+  p.SQ = FT / a.etot > 1 ? FT / a.etot : 1;
+  size_t o = 0;
+  p.lsm = o; o += al(N * M * sizeof(double));
+  p.wsm = o; o += al((size_t)a.wsz * sizeof(cd));
+  p.qsum = o; o += al((size_t)a.qper * sizeof(cd));
+  p.ipscr = o; o += (size_t)a.nb * ipscr_bytes<MAXMB>();
+  size_t r1 = (size_t)p.SL * NM * 2 * sizeof(double);
+  size_t r2 = (size_t)p.SQ * p.nitems * MAXMB * sizeof(cd);
+  p.red = o; o += al(r1 > r2 ? r1 : r2);
+  p.wsum = o; o += al(64 * sizeof(double));
+  p.ldet = o; o += al((size_t)a.nb * sizeof(double));
+  const size_t tA = (N + 2 * M) * FT * sizeof(double);  // h, z, 1/eta
+  const size_t tB = (3 * M) * FT * sizeof(double);      // x (complex), 1/eta
+  p.tile = o; o += al(tA > tB ? tA : tB);
+  p.total = o;
+  return p;
+}
+
+__device__ __forceinline__ void em_stamp(const EmArgs& a, int phase) {
+  if (a.trace && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[blockIdx.x * 16 + phase] = t;
+  }
+}
+
+template <int MB_, int NB_, int NS_, int MAXMB>
+__global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
+  constexpr bool SB = MB_ > 0 && NB_ > 0;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int f = blockIdx.x;
+  const int tid = threadIdx.x, FT = blockDim.x;
+  const int M = SB ? MB_ * NB_ : a.M;
+  const int nb = SB ? NB_ : a.nb;
+  const int N = NS_ > 0 ? NS_ : a.N;
+  const int T = a.T;
+  const int wsz = SB ? MB_ * MB_ * NB_ : a.wsz;
+  auto MBof = [&](int b) { return SB ? MB_ : a.mb[b]; };
+  auto OFF = [&](int b) { return SB ? b * MB_ : a.off[b]; };
+  auto WOFF = [&](int b) { return SB ? b * MB_ * MB_ : a.woff[b]; };
+  const EmPlan sp = plan_em<MAXMB>(a, FT);
+  double* Lsm = (double*)(smem + sp.lsm);
+  cd* Wsm = (cd*)(smem + sp.wsm);
+  cd* Qsum = (cd*)(smem + sp.qsum);
+  double* red = (double*)(smem + sp.red);
+  double* wsum = (double*)(smem + sp.wsum);
+  double* ldet = (double*)(smem + sp.ldet);
+  double* tile = (double*)(smem + sp.tile);
+  const double floor_ = a.floor_;
+  const int ntiles = (T + FT - 1) / FT;
+  const cd* xf = a.x + (size_t)f * T * M;
+  const double* Hf = a.H + (size_t)f * N * T;
+  em_stamp(a, 0);
+
+  for (int e = tid; e < N * M; e += FT) Lsm[e] = a.lam[(size_t)f * N * M + e];
+  for (int e = tid; e < wsz; e += FT) Wsm[e] = a.W[(size_t)f * wsz + e];
+  __syncthreads();
+
+  auto load_h = [&](int t, double* h) {
+#pragma unroll
+    for (int n = 0; n < kMaxN; ++n) h[n] = n < N ? __ldg(Hf + n * T + t) : 0.0;
+  };
+  // |W^H x|^2 of one frame for block b; x read from global (L2)
+  auto power_block = [&](int b, const cd* xt, double* P) {
+    const int mb = MBof(b), off = OFF(b);
+    const cd* wb = Wsm + WOFF(b);
+    if constexpr (SB) {
+      cd xv[MB_];
+#pragma unroll
+      for (int q = 0; q < MB_; ++q) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(xt + off + q));
+        xv[q] = cd{v.x, v.y};
+      }
+#pragma unroll
+      for (int mu = 0; mu < MB_; ++mu) {
+        cd s{0.0, 0.0};
+#pragma unroll
+        for (int q = 0; q < MB_; ++q) s = s + cmulc(wb[mu * MB_ + q], xv[q]);
+        P[mu] = norm2(s);
+      }
+    } else {
+      for (int mu = 0; mu < mb; ++mu) {
+        cd s{0.0, 0.0};
+        for (int q = 0; q < mb; ++q) {
+          const double2 v = __ldg(reinterpret_cast<const double2*>(xt + off + q));
+          s = s + cmulc(wb[mu * mb + q], cd{v.x, v.y});
+        }
+        P[mu] = norm2(s);
+      }
+    }
+  };
+
+  // ================================================================ pass A
+  // finish iteration i-1: Lambda update with eta = max(h Lambda_old, floor)
+  if (a.finish == 2) {
+    double* hs = tile;               // [N][FT]
+    double* zs = tile + N * FT;      // [M][FT]
+    double* is = zs + M * FT;        // [M][FT]
+    const int NM = N * M, SL = sp.SL;
+    const bool item_thread = tid < NM * SL;
+    const int item = item_thread ? tid % NM : 0, sl = item_thread ? tid / NM : 0;
+    const int in_ = item / M, im = item - in_ * M;
+    double num = 0.0, den = 0.0;
+    for (int tl = 0; tl < ntiles; ++tl) {
+      const int t = tl * FT + tid;
+      const int tn = min(FT, T - tl * FT);
+      if (tid < tn) {
+        double h[kMaxN];
+        load_h(t, h);
+#pragma unroll
+        for (int n = 0; n < kMaxN; ++n)
+          if (n < N) hs[n * FT + tid] = h[n];
+        const cd* xt = xf + (size_t)t * M;
+#pragma unroll
+        for (int b = 0; b < nb; ++b) {
+          double P[MAXMB];
+          power_block(b, xt, P);
+          const int off = OFF(b), mb = MBof(b);
+#pragma unroll
+          for (int mu = 0; mu < MAXMB; ++mu)
+            if (mu < mb) {
+              const int m = off + mu;
+              double raw = 0.0;
+#pragma unroll
+              for (int n = 0; n < kMaxN; ++n)
+                if (n < N) raw += h[n] * Lsm[n * M + m];
+              const double ie = 1.0 / fmax(raw, floor_);
+              is[m * FT + tid] = ie;
+              zs[m * FT + tid] = P[mu] * ie * ie;
+            }
+        }
+      }
+      __syncthreads();
+      if (item_thread) {
+        const double* hr = hs + in_ * FT;
+        const double* zr = zs + im * FT;
+        const double* er = is + im * FT;
+#pragma unroll 4
+        for (int tt = sl; tt < tn; tt += SL) {
+          num += hr[tt] * zr[tt];
+          den += hr[tt] * er[tt];
+        }
+      }
+      __syncthreads();
+    }
+    if (item_thread) {
+      red[2 * (sl * NM + item)] = num;
+      red[2 * (sl * NM + item) + 1] = den;
+    }
+    __syncthreads();
+    for (int q = tid; q < NM; q += FT) {
+      double nu = 0.0, de = 0.0;
+      for (int s = 0; s < SL; ++s) {
+        nu += red[2 * (s * NM + q)];
+        de += red[2 * (s * NM + q) + 1];
+      }
+      double& l = Lsm[q];
+      l = fmax(l * sqrt(nu / fmax(de, floor_)), floor_);
+      a.lam[(size_t)f * N * M + q] = l;
+    }
+    __syncthreads();
+  }
+  em_stamp(a, 1);
+
+  // ================================================================ pass B
+  // eta with the current Lambda -> cost terms of iteration i-1 and the IP
+  // weights; Q_mu accumulation over the frame tiles
+  double cost = 0.0;
+  LogAcc lacc;
+  const int nitems = sp.nitems, SQ = sp.SQ;
+  const bool qthread = a.start && tid < nitems * SQ;
+  const int qitem = qthread ? tid % nitems : 0, qs = qthread ? tid / nitems : 0;
+  int qb_ = 0, qr = 0, qc = 0;
+  if (qthread) {
+    int rem = qitem;
+    if constexpr (SB) {
+      constexpr int E = MB_ * (MB_ + 1) / 2;
+      qb_ = rem / E;
+      rem -= qb_ * E;
+    } else {
+      while (qb_ + 1 < nb && rem >= a.eofs[qb_ + 1]) ++qb_;
+      rem -= a.eofs[qb_];
+    }
+    decode_entry(rem, qr, qc);
+  }
+  cd qacc[MAXMB];
+#pragma unroll
+  for (int mu = 0; mu < MAXMB; ++mu) qacc[mu] = cd{0.0, 0.0};
+  // log-det (+ W^-1 for the fast IP path) of the pre-IP demixers: threads
+  // with no Q item take one (bin, block) system each
+  {
+    const int first_free = a.start ? nitems * SQ : 0;
+    const int nfree = FT - first_free;
+    auto do_logdet = [&](int b) {
+      if constexpr (SB && MB_ <= 4) {
+        IpWork<MB_>& w = *(IpWork<MB_>*)(smem + sp.ipscr + b * ipscr_bytes<MAXMB>());
+        const cd* wb = Wsm + b * MB_ * MB_;
+#pragma unroll
+        for (int e = 0; e < MB_ * MB_; ++e) w.Wold[e] = wb[e];
+        ldet[b] = logdet2_inverse_thread<MB_>(wb, w.Winv);
+      } else {
+        cd* scr = (cd*)(smem + sp.ipscr + b * ipscr_bytes<MAXMB>());
+        ldet[b] = 2.0 * log_abs_det_serial(MBof(b), Wsm + WOFF(b), scr);
+      }
+    };
+    if (nfree > 0) {
+      if (tid >= first_free)
+        for (int b = tid - first_free; b < nb; b += nfree) do_logdet(b);
+    } else {
+      for (int b = tid; b < nb; b += FT) do_logdet(b);
+    }
+  }
+  {
+    cd* xsm = (cd*)tile;                              // [M][FT]
+    double* is = tile + 2 * (size_t)M * FT;           // [M][FT]
+    for (int tl = 0; tl < ntiles; ++tl) {
+      const int t = tl * FT + tid;
+      const int tn = min(FT, T - tl * FT);
+      if (tid < tn) {
+        double h[kMaxN];
+        load_h(t, h);
+        const cd* xt = xf + (size_t)t * M;
+        for (int b = 0; b < nb; ++b) {
+          double P[MAXMB];
+          power_block(b, xt, P);
+          const int off = OFF(b), mb = MBof(b);
+#pragma unroll
+          for (int mu = 0; mu < MAXMB; ++mu)
+            if (mu < mb) {
+              const int m = off + mu;
+              double raw = 0.0;
+#pragma unroll
+              for (int n = 0; n < kMaxN; ++n)
+                if (n < N) raw += h[n] * Lsm[n * M + m];
+              const double ie = 1.0 / fmax(raw, floor_);
+              cost += P[mu] * ie;
+              lacc.mul(fmax(raw, 1e-300));
+              if (a.start) {
+                is[m * FT + tid] = ie;
+                const double2 v = __ldg(reinterpret_cast<const double2*>(xt + m));
+                xsm[m * FT + tid] = cd{v.x, v.y};
+              }
+            }
+        }
+        lacc.renorm();
+      }
+      if (a.start) {
+        __syncthreads();
+        if (qthread) {
+          const int mb = MBof(qb_), off = OFF(qb_);
+          const cd* xr = xsm + (off + qr) * FT;
+          const cd* xc = xsm + (off + qc) * FT;
+          const double* ew = is + off * FT;
+#pragma unroll 2
+          for (int tt = qs; tt < tn; tt += SQ) {
+            const cd pr = xr[tt] * conjg(xc[tt]);
+#pragma unroll
+            for (int mu = 0; mu < MAXMB; ++mu)
+              if (mu < mb) qacc[mu] = qacc[mu] + pr * ew[mu * FT + tt];
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
+  em_stamp(a, 2);
+  // cost of iteration i-1: frame terms (fixed-order block reduction) minus
+  // T * sum 2 ln|det W| (engine.cpp:253)
+  cost += lacc.value();
+  cost = warp_sum(cost);
+  if ((tid & 31) == 0) wsum[tid >> 5] = cost;
+  if (a.start && qthread) {
+    cd* qp = (cd*)red;
+#pragma unroll
+    for (int mu = 0; mu < MAXMB; ++mu) qp[(qs * nitems + qitem) * MAXMB + mu] = qacc[mu];
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double c = 0.0;
+    for (int w = 0; w < sp.nwarps; ++w) c += wsum[w];
+    double d = 0.0;
+    for (int b = 0; b < nb; ++b) d += ldet[b];
+    a.cost_out[f] = c - (double)T * d;
+  }
+  if (!a.start) return;
+  for (int idx = tid; idx < nitems * MAXMB; idx += FT) {
+    const int it = idx / MAXMB, mu = idx - it * MAXMB;
+    int rem = it, b = 0;
+    if constexpr (SB) {
+      constexpr int E = MB_ * (MB_ + 1) / 2;
+      b = rem / E;
+      rem -= b * E;
+    } else {
+      while (b + 1 < nb && rem >= a.eofs[b + 1]) ++b;
+      rem -= a.eofs[b];
+    }
+    const int mb = MBof(b);
+    if (mu >= mb) continue;
+    const cd* qp = (const cd*)red;
+    cd sum{0.0, 0.0};
+    for (int s = 0; s < SQ; ++s) sum = sum + qp[(s * nitems + it) * MAXMB + mu];
+    const int E = mb * (mb + 1) / 2;
+    Qsum[a.qofs[b] + mu * E + rem] = cd{sum.re / (double)T, sum.im / (double)T};
+  }
+  __syncthreads();
+  em_stamp(a, 3);
+
+  // ============================================================ IP sweep
+  {
+    int fbs = 0;
+    if constexpr (SB && MB_ <= 4) {
+      constexpr int E = MB_ * (MB_ + 1) / 2;
+      for (int idx = tid; idx < nb * MB_; idx += FT) {
+        const int b = idx / MB_, mu = idx - b * MB_;
+        IpWork<MB_>& w = *(IpWork<MB_>*)(smem + sp.ipscr + b * ipscr_bytes<MAXMB>());
+        w.ok[mu] = chol_thread<MB_>(Qsum + a.qofs[b] + mu * E, w.L[mu], w.dinv[mu]) ? 1 : 0;
+      }
+      __syncthreads();
+      const int l = tid & 3;
+      const unsigned qmask = 0xFu << (tid & 28);
+      for (int b = tid >> 2; b < nb; b += FT >> 2) {
+        IpWork<MB_>& w = *(IpWork<MB_>*)(smem + sp.ipscr + b * ipscr_bytes<MAXMB>());
+        cd* wb = Wsm + b * MB_ * MB_;
+        const cd* qb = Qsum + a.qofs[b];
+        const bool ok = ip_sweep_quad<MB_>(wb, w, qb, floor_, l, qmask);
+        if (!ok && l == 0) {
+          // exact path (engine.cpp:47-49: LU, residual test, pinv) from W_old
+#pragma unroll
+          for (int e = 0; e < MB_ * MB_; ++e) wb[e] = w.Wold[e];
+          const int fb = ip_solve_thread<MB_>(wb, qb, floor_, w.slow);
+          if (fb) atomicAdd(a.fallbacks, fb);
+        }
+        __syncwarp(qmask);
+      }
+    } else {
+      const int warp = tid >> 5, lane = tid & 31;
+      for (int b = warp; b < nb; b += sp.nwarps) {
+        const int mb = MBof(b);
+        const int E = mb * (mb + 1) / 2;
+        IpScratch<MAXMB>& sc = *(IpScratch<MAXMB>*)(smem + sp.ipscr + b * ipscr_bytes<MAXMB>());
+        cd* wb = Wsm + WOFF(b);
+        fbs = 0;
+        for (int mu = 0; mu < mb; ++mu) {
+          const cd* qp = Qsum + a.qofs[b] + mu * E;
+          auto qget = [&](int r, int c) {
+            return r <= c ? qp[c * (c + 1) / 2 + r] : conjg(qp[r * (r + 1) / 2 + c]);
+          };
+          fbs += ip_column_warp<MAXMB>(mb, wb, mu, qget, floor_, sc);
+        }
+        if (lane == 0 && fbs) atomicAdd(a.fallbacks, fbs);
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < wsz; e += FT) a.W[(size_t)f * wsz + e] = Wsm[e];
+  em_stamp(a, 4);
+
+  // ================================================================ pass C
+  // P = |W_new^H x|^2 and the T-update weights with the pre-update eta
+  // (engine.cpp:100-109), written per (source, bin, frame) for k_tupd
+  for (int t = tid; t < T; t += FT) {
+    double h[kMaxN];
+    load_h(t, h);
+    const cd* xt = xf + (size_t)t * M;
+    double A[kMaxN], B[kMaxN];
+#pragma unroll
+    for (int n = 0; n < kMaxN; ++n) A[n] = B[n] = 0.0;
+    for (int b = 0; b < nb; ++b) {
+      double P[MAXMB];
+      power_block(b, xt, P);
+      const int off = OFF(b), mb = MBof(b);
+#pragma unroll
+      for (int mu = 0; mu < MAXMB; ++mu)
+        if (mu < mb) {
+          const int m = off + mu;
+          double raw = 0.0;
+#pragma unroll
+          for (int n = 0; n < kMaxN; ++n)
+            if (n < N) raw += h[n] * Lsm[n * M + m];
+          const double ie = 1.0 / fmax(raw, floor_);
+          const double z = P[mu] * ie * ie;
+#pragma unroll
+          for (int n = 0; n < kMaxN; ++n)
+            if (n < N) {
+              const double l = Lsm[n * M + m];
+              A[n] += z * l;
+              B[n] += ie * l;
+            }
+        }
+    }
+#pragma unroll
+    for (int n = 0; n < kMaxN; ++n)
+      if (n < N) {
+        const size_t o = ((size_t)n * a.F + f) * T + t;
+        a.Aw[o] = A[n];
+        a.Bw[o] = B[n];
+      }
+  }
+  em_stamp(a, 5);
+}
+
+// ------------------------------------------------------------------ k_spec
+// H[f][n][t] = sum_k T[f][n][k] V[n][k][t]  (engine.cpp:71-81).  CTA tile:
+// 16 bins x 64 frames of one source; V tile and T rows staged in shared
+// memory; each thread owns 4 frames of one bin.
+constexpr int kSpecFB = 16, kSpecTB = 64;
+__global__ void __launch_bounds__(256) k_spec(int F, int T, int N, int K, const double* __restrict__ Tf,
+                                             const double* __restrict__ V, double* __restrict__ H) {
+  extern __shared__ __align__(16) double sspec[];
+  double* Vs = sspec;                  // [K][TB]
+  double* Ts = sspec + K * kSpecTB;    // [FB][K]
+  const int n = blockIdx.z;
+  const int t0 = blockIdx.x * kSpecTB, f0 = blockIdx.y * kSpecFB;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < K * kSpecTB; e += 256) {
+    const int k = e / kSpecTB, tt = e - k * kSpecTB;
+    Vs[e] = t0 + tt < T ? V[((size_t)n * K + k) * T + t0 + tt] : 0.0;
+  }
+  for (int e = tid; e < kSpecFB * K; e += 256) {
+    const int fi = e / K, k = e - fi * K;
+    Ts[e] = f0 + fi < F ? Tf[((size_t)(f0 + fi) * N + n) * K + k] : 0.0;
+  }
+  __syncthreads();
+  const int fi = tid / 16, tj = tid % 16;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const double* tr = Ts + fi * K;
+  for (int k = 0; k < K; ++k) {
+    const double tv = tr[k];
+    const double* vr = Vs + k * kSpecTB + tj;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j] += tv * vr[16 * j];
+  }
+  const int f = f0 + fi;
+  if (f < F)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int t = t0 + tj + 16 * j;
+      if (t < T) H[((size_t)f * N + n) * T + t] = acc[j];
+    }
+}
+
+// ------------------------------------------------------------------ k_tupd
+// T[f][n][k] <- max(T * sqrt(sum_t A V / max(sum_t B V, floor)), floor)
+// (engine.cpp:115-123).  CTA: 8 bins of one source; thread (bin, k, parity)
+// sums over frames of one parity in 128-frame chunks staged in shared
+// memory; the two parities are added in a fixed order.
+constexpr int kTupdFB = 8, kTupdTC = 128, kTupdVS = kTupdTC + 1;  // padded V row stride
+__global__ void __launch_bounds__(256) k_tupd(int F, int T, int N, int K, double* __restrict__ Tf,
+                                             const double* __restrict__ V, const double* __restrict__ Aw,
+                                             const double* __restrict__ Bw, double floor_) {
+  extern __shared__ __align__(16) double stup[];
+  double* As = stup;                       // [FB][TC]
+  double* Bs = As + kTupdFB * kTupdTC;     // [FB][TC]
+  double* Vs = Bs + kTupdFB * kTupdTC;     // [K][VS]
+  const int n = blockIdx.y, f0 = blockIdx.x * kTupdFB;
+  const int tid = threadIdx.x;
+  const int fi = tid / 32, lane = tid & 31;
+  const int par = lane >> 4;
+  constexpr int KPT = 4;  // k values per thread: k = (lane & 15) + 16 j
+  double num[KPT], den[KPT];
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) num[j] = den[j] = 0.0;
+  for (int tc = 0; tc < T; tc += kTupdTC) {
+    const int tn = min(kTupdTC, T - tc);
+    __syncthreads();
+    for (int e = tid; e < kTupdFB * kTupdTC; e += 256) {
+      const int fr = e / kTupdTC, tt = e - fr * kTupdTC;
+      const bool ok = f0 + fr < F && tt < tn;
+      const size_t o = ((size_t)n * F + f0 + fr) * T + tc + tt;
+      As[e] = ok ? Aw[o] : 0.0;
+      Bs[e] = ok ? Bw[o] : 0.0;
+    }
+    for (int e = tid; e < K * kTupdTC; e += 256) {
+      const int k = e / kTupdTC, tt = e - k * kTupdTC;
+      Vs[k * kTupdVS + tt] = tt < tn ? V[((size_t)n * K + k) * T + tc + tt] : 0.0;
+    }
+    __syncthreads();
+    const double* ar = As + fi * kTupdTC;
+    const double* br = Bs + fi * kTupdTC;
+#pragma unroll 2
+    for (int tt = par; tt < tn; tt += 2) {
+      const double av = ar[tt], bv = br[tt];
+#pragma unroll
+      for (int j = 0; j < KPT; ++j) {
+        const int k = (lane & 15) + 16 * j;
+        if (k < K) {
+          const double v = Vs[k * kTupdVS + tt];
+          num[j] += av * v;
+          den[j] += bv * v;
+        }
+      }
+    }
+  }
+  const int f = f0 + fi;
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) {
+    const double on = __shfl_down_sync(0xffffffffu, num[j], 16);
+    const double od = __shfl_down_sync(0xffffffffu, den[j], 16);
+    const int k = (lane & 15) + 16 * j;
+    if (par == 0 && k < K && f < F) {
+      const double nu = num[j] + on, de = den[j] + od;
+      double* tp = Tf + ((size_t)f * N + n) * K + k;
+      *tp = fmax(*tp * sqrt(nu / fmax(de, floor_)), floor_);
+    }
+  }
+}
+
+// -------------------------------------------------------------------- k_pd
+// For a tile of bins x frames: h' = T_new V (V tile shared by the bins),
+// eta' = max(h' Lambda, floor), P = |W^H x|^2, and the V-update weights
+// A'_n = sum_m Lambda z, B'_n = sum_m Lambda / eta' (engine.cpp:231-237).
+constexpr int kPdFB = 4;
+template <int MB_, int NB_, int NS_, int NK_, int MAXMB>
+__global__ void __launch_bounds__(256) k_pd(const EmArgs a, const double* __restrict__ Tf,
+                                           const double* __restrict__ V, int TB) {
+  constexpr bool SB = MB_ > 0 && NB_ > 0;
+  extern __shared__ __align__(16) unsigned char spd[];
+  const int M = SB ? MB_ * NB_ : a.M;
+  const int nb = SB ? NB_ : a.nb;
+  const int N = NS_ > 0 ? NS_ : a.N;
+  const int K = NK_ > 0 ? NK_ : a.K;
+  const int T = a.T;
+  const int wsz = SB ? MB_ * MB_ * NB_ : a.wsz;
+  auto MBof = [&](int b) { return SB ? MB_ : a.mb[b]; };
+  auto OFF = [&](int b) { return SB ? b * MB_ : a.off[b]; };
+  auto WOFF = [&](int b) { return SB ? b * MB_ * MB_ : a.woff[b]; };
+  double* Vs = (double*)spd;                     // [N][K][TB]
+  double* Ts = Vs + (size_t)N * K * TB;          // [FB][N][K]
+  double* Ls = Ts + kPdFB * N * K;               // [FB][N][M]
+  cd* Ws = (cd*)(Ls + kPdFB * N * M + (((kPdFB * N * M) & 1) ? 1 : 0));  // [FB][wsz]
+  const int t0 = blockIdx.x * TB, f0 = blockIdx.y * kPdFB;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int fn = min(kPdFB, a.F - f0);
+  for (int e = tid; e < N * K * TB; e += nth) {
+    const int row = e / TB, tt = e - row * TB;
+    Vs[e] = t0 + tt < T ? V[(size_t)row * T + t0 + tt] : 0.0;
+  }
+  for (int e = tid; e < fn * N * K; e += nth) Ts[e] = Tf[(size_t)f0 * N * K + e];
+  for (int e = tid; e < fn * N * M; e += nth) Ls[e] = a.lam[(size_t)f0 * N * M + e];
+  for (int e = tid; e < fn * wsz; e += nth) Ws[e] = a.W[(size_t)f0 * wsz + e];
+  __syncthreads();
+  const int fi = tid / TB, tt = tid - fi * TB;
+  const int t = t0 + tt, f = f0 + fi;
+  if (fi >= fn || t >= T) return;
+  double h[kMaxN];
+#pragma unroll
+  for (int n = 0; n < kMaxN; ++n) {
+    double s = 0.0;
+    if (n < N) {
+      const double* tr = Ts + (fi * N + n) * K;
+      const double* vr = Vs + (size_t)n * K * TB + tt;
+      if constexpr (NK_ > 0) {
+#pragma unroll
+        for (int k = 0; k < NK_; ++k) s += tr[k] * vr[k * TB];
+      } else {
+        for (int k = 0; k < K; ++k) s += tr[k] * vr[k * TB];
+      }
+    }
+    h[n] = s;
+  }
+  const double* Lf = Ls + fi * N * M;
+  const cd* Wf = Ws + fi * wsz;
+  const cd* xt = a.x + ((size_t)f * T + t) * M;
+  double A[kMaxN], B[kMaxN];
+#pragma unroll
+  for (int n = 0; n < kMaxN; ++n) A[n] = B[n] = 0.0;
+  for (int b = 0; b < nb; ++b) {
+    const int mb = MBof(b), off = OFF(b);
+    const cd* wb = Wf + WOFF(b);
+    double P[MAXMB];
+    if constexpr (SB) {
+      cd xv[MB_];
+#pragma unroll
+      for (int q = 0; q < MB_; ++q) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(xt + off + q));
+        xv[q] = cd{v.x, v.y};
+      }
+#pragma unroll
+      for (int mu = 0; mu < MB_; ++mu) {
+        cd s{0.0, 0.0};
+#pragma unroll
+        for (int q = 0; q < MB_; ++q) s = s + cmulc(wb[mu * MB_ + q], xv[q]);
+        P[mu] = norm2(s);
+      }
+    } else {
+      for (int mu = 0; mu < mb; ++mu) {
+        cd s{0.0, 0.0};
+        for (int q = 0; q < mb; ++q) {
+          const double2 v = __ldg(reinterpret_cast<const double2*>(xt + off + q));
+          s = s + cmulc(wb[mu * mb + q], cd{v.x, v.y});
+        }
+        P[mu] = norm2(s);
+      }
+    }
+#pragma unroll
+    for (int mu = 0; mu < MAXMB; ++mu)
+      if (mu < mb) {
+        const int m = off + mu;
+        double raw = 0.0;
+#pragma unroll
+        for (int n = 0; n < kMaxN; ++n)
+          if (n < N) raw += h[n] * Lf[n * M + m];
+        const double ie = 1.0 / fmax(raw, a.floor_);
+        const double z = P[mu] * ie * ie;
+#pragma unroll
+        for (int n = 0; n < kMaxN; ++n)
+          if (n < N) {
+            const double l = Lf[n * M + m];
+            A[n] += z * l;
+            B[n] += ie * l;
+          }
+      }
+  }
+#pragma unroll
+  for (int n = 0; n < kMaxN; ++n)
+    if (n < N) {
+      const size_t o = ((size_t)n * a.F + f) * T + t;
+      a.Aw[o] = A[n];
+      a.Bw[o] = B[n];
+    }
+}
+
+// V update (engine.cpp:125-133), the only cross-bin reduction.  Grid:
+// (frame tiles of 32, sources, k-groups of KPT); the 8 warps of a CTA each
+// sum a contiguous range of bins, then the partials are added in warp order
+// (deterministic, no atomics).  numden == nullptr: apply in place; else write
+// {num, den} for the cross-GPU allreduce.
+constexpr int kVupdWarps = 8;
+constexpr int kVupdKPT = 8;
+__global__ void __launch_bounds__(32 * kVupdWarps) k_vupd(int F, int T, int N, int K, const double* __restrict__ Tf,
+                                                         const double* __restrict__ Ap,
+                                                         const double* __restrict__ Bp, double* __restrict__ V,
+                                                         double* __restrict__ numden, double floor_) {
+  __shared__ double part[kVupdWarps][2][kVupdKPT][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = blockIdx.x * 32 + lane;
+  const int n = blockIdx.y;
+  const int k0 = blockIdx.z * kVupdKPT;
+  const int kn = min(kVupdKPT, K - k0);
+  const int chunk = (F + kVupdWarps - 1) / kVupdWarps;
+  const int fa = warp * chunk, fe = min(F, fa + chunk);
+  double num[kVupdKPT], den[kVupdKPT];
+#pragma unroll
+  for (int j = 0; j < kVupdKPT; ++j) num[j] = den[j] = 0.0;
+  if (t < T) {
+    const double* ar = Ap + (size_t)n * F * T + t;
+    const double* br = Bp + (size_t)n * F * T + t;
+#pragma unroll 2
+    for (int f = fa; f < fe; ++f) {
+      const double av = __ldg(ar + (size_t)f * T), bv = __ldg(br + (size_t)f * T);
+      const double* tr = Tf + ((size_t)f * N + n) * K + k0;
+#pragma unroll
+      for (int j = 0; j < kVupdKPT; ++j)
+        if (j < kn) {
+          const double tv = __ldg(tr + j);
+          num[j] += tv * av;
+          den[j] += tv * bv;
+        }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kVupdKPT; ++j) {
+    part[warp][0][j][lane] = num[j];
+    part[warp][1][j][lane] = den[j];
+  }
+  __syncthreads();
+  if (t >= T) return;
+  for (int j = warp; j < kn; j += kVupdWarps) {
+    double sn = 0.0, sd = 0.0;
+#pragma unroll
+    for (int w = 0; w < kVupdWarps; ++w) {
+      sn += part[w][0][j][lane];
+      sd += part[w][1][j][lane];
+    }
+    const size_t o = ((size_t)n * K + k0 + j) * T + t;
+    if (numden) {
+      numden[o] = sn;
+      numden[(size_t)N * K * T + o] = sd;
+    } else {
+      V[o] = fmax(V[o] * sqrt(sn / fmax(sd, floor_)), floor_);
+    }
+  }
+}
+
+__global__ void k_vapply(size_t nkt, const double* __restrict__ numden, double* __restrict__ V,
+                         double floor_) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= nkt) return;
+  V[i] = fmax(V[i] * sqrt(numden[i] / fmax(numden[nkt + i], floor_)), floor_);
+}
+
+}  // namespace dfm

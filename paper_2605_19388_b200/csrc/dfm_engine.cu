@@ -1,28 +1,26 @@
-// Fused sm_100a engine for the distributed-FastMNMF EM loop
-// (restates src/engine.cpp:167-272 of the reference).
+// B200 engine for the distributed-FastMNMF EM loop (restates
+// src/engine.cpp:167-272 of the reference).
 //
-// One EM iteration = two kernels:
-//   k_bin  — one thread-block CLUSTER per group of G frequency bins; the
-//            cluster's CS CTAs split the frames, each keeping its slice of
-//            X (and every per-frame intermediate) resident in shared memory
-//            for the whole launch.  Reductions over frames (Lambda, Q, T,
-//            cost) go through distributed shared memory in a fixed rank
-//            order, so every CTA of a cluster ends with bit-identical
-//            reduced values and applies the small per-bin updates
-//            redundantly.  A launch finishes iteration i-1 (Lambda update,
-//            eta refresh, cost; engine.cpp:246-253) and starts iteration i
-//            (IP sweep, decorrelation, T update, V-update weights;
-//            engine.cpp:212-237) — legal because both halves are bin-local.
-//   k_vupd — the only cross-bin reduction (engine.cpp:125-133): V numerator
-//            and denominator summed over bins in bin order (deterministic),
-//            applied in place — or written out for the NCCL allreduce when
-//            the bins are sharded over GPUs.
+// One EM iteration = five kernels on one stream (dfm_em.cuh):
+//   k_em_bin  per-bin work that needs no V: finish iteration i-1 (Lambda
+//             update, cost; engine.cpp:246-253) and start iteration i (Q_mu,
+//             IP sweep, decorrelation, T-update weights; :212-227).  One CTA
+//             per bin, frames streamed from L2 in tiles, every bin resident
+//             in one wave.
+//   k_tupd    T update (:115-123)
+//   k_pd      h' = T V, eta', V-update weights (:231-237), V tile shared by
+//             a tile of bins
+//   k_vupd    V update (:125-133) - the only cross-bin reduction; with a
+//             communicator it writes {num, den}, one ncclAllReduce follows
+//             and k_vapply updates V identically on every rank
+//   k_spec    H = T V for the next iteration (bin-tiled GEMM)
+// A launch of k_em_bin finishes the previous iteration and starts the next,
+// which is legal because both halves are bin-local.
 //
 // Device layouts (converted once per dfm_set_model / dfm_get_model):
 //   x  [F][T][M] cd  | Tf [F][N][K] | V [N][K][T] | lam [F][N][M]
-//   W  [F][wsz] cd (blocks packed per bin, col-major)
-//   Ap, Bp [N][F][T] (V-update weights)   cost_part [launch][group]
-#include <cooperative_groups.h>
+//   W  [F][wsz] cd (blocks packed per bin, col-major) | H [F][N][T]
+//   Aw, Bw [N][F][T] (T- then V-update weights)   cost_part [launch][bin]
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -36,40 +34,13 @@
 
 #include "dfm_internal.cuh"
 
-namespace cg = cooperative_groups;
-
 namespace dfm {
-
-constexpr int kGMax = 4;      // bins per CTA group, upper bound
-constexpr int kMaxN = 8;      // sources held in registers
-constexpr int kMaxK = 64;     // NMF bases
-constexpr int kThreads = 256; // max threads per CTA of k_bin
-
-struct BinArgs {
-  int F, T, M, N, K, nb, wsz;
-  int mb[DFM_MAX_BLOCKS], off[DFM_MAX_BLOCKS], woff[DFM_MAX_BLOCKS];
-  int eofs[DFM_MAX_BLOCKS];  // offset of block b among one bin's packed Q entries (items)
-  int qofs[DFM_MAX_BLOCKS];  // offset of block b inside one bin's Q slab (complex)
-  int etot, qper;            // sum_b E_b, sum_b mb*E_b
-  int G, CS, Ts, Tsp;
-  double floor_;
-  const cd* x;
-  double* Tf;
-  const double* V;
-  double* lam;
-  cd* W;
-  double* Ap;
-  double* Bp;
-  double* cost_out;  // [ngroups] slot of this launch
-  int* fallbacks;
-  int finish;  // 1 = cost only (first launch), 2 = Lambda update + cost
-  int start;   // 1 = IP + T update + V weights
-  unsigned long long* trace;  // optional per-CTA phase timestamps [cta][16]
-};
-
+constexpr int kMaxN = 8;   // sources held in registers
+constexpr int kMaxK = 64;  // NMF bases
 }  // namespace dfm
 
-#include "dfm_bin_kernel.cuh"
+#include "dfm_ip.cuh"
+#include "dfm_em.cuh"
 
 using namespace dfm;
 
@@ -126,27 +97,29 @@ struct dfm_ctx {
   Layout L;
   cudaStream_t stream = nullptr;
   DBuf<cd> x, W;
-  DBuf<double> Tf, V, lam, Ap, Bp, numden, cost_part, cost_sum;
+  DBuf<double> Tf, V, lam, H, Aw, Bw, numden, cost_part, cost_sum;
   DBuf<int> fallbacks;
-  int G = 1, CS = 1, Ts = 1, Tsp = 1, threads = 256, smem = 0, maxmb = 4, ngroups = 1;
-  int kmaxmb = 4;           // MAXMB of the selected k_bin instantiation
-  void (*kbin)(BinArgs) = nullptr;
+  int maxmb = 4;
+  int kmaxmb = 4;  // MAXMB of the selected instantiations
+  void (*kem)(EmArgs) = nullptr;
+  void (*kpd)(EmArgs, const double*, const double*, int) = nullptr;
   bool force_generic = false;
-  int req_G = 0, req_CS = 0;
+  int FT = 128, TB = 64, smem_em = 0, smem_pd = 0, smem_tupd = 0, smem_spec = 0;
+  int req_FT = 0, req_TB = 0;
   DBuf<unsigned long long> trace;
   bool tracing = false;
   ncclComm_t comm = nullptr;
   int nranks = 1, rank = 0;
   long long launches = 0;
-  cudaEvent_t eb0 = nullptr, eb1 = nullptr, ebm = nullptr;
+  cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   bool has_obs = false, has_model = false;
   std::vector<cudaEvent_t> iter_ev;
 };
 
 namespace {
 
-BinArgs make_args(dfm_ctx* c) {
-  BinArgs a;
+EmArgs make_args(dfm_ctx* c) {
+  EmArgs a;
   std::memset(&a, 0, sizeof(a));
   a.F = c->F;
   a.T = c->T;
@@ -168,140 +141,146 @@ BinArgs make_args(dfm_ctx* c) {
   }
   a.etot = e;
   a.qper = q;
-  a.G = c->G;
-  a.CS = c->CS;
-  a.Ts = c->Ts;
-  a.Tsp = c->Tsp;
   a.floor_ = c->floor_;
   a.x = c->x.p;
-  a.Tf = c->Tf.p;
-  a.V = c->V.p;
+  a.H = c->H.p;
   a.lam = c->lam.p;
   a.W = c->W.p;
-  a.Ap = c->Ap.p;
-  a.Bp = c->Bp.p;
+  a.Aw = c->Aw.p;
+  a.Bw = c->Bw.p;
   a.fallbacks = c->fallbacks.p;
   return a;
 }
 
-size_t plan_total(const BinArgs& a, int threads, int kmaxmb) {
+size_t em_smem(const EmArgs& a, int FT, int kmaxmb) {
   switch (kmaxmb) {
-    case 2: return plan_smem<2>(a, threads).total;
-    case 4: return plan_smem<4>(a, threads).total;
-    case 12: return plan_smem<12>(a, threads).total;
-    default: return plan_smem<DFM_MAX_MB>(a, threads).total;
+    case 2: return plan_em<2>(a, FT).total;
+    case 4: return plan_em<4>(a, FT).total;
+    case 12: return plan_em<12>(a, FT).total;
+    default: return plan_em<DFM_MAX_MB>(a, FT).total;
   }
 }
 
-// Kernel selection: a compile-time-shape instantiation when the layout is
-// uniform and matches one (BASELINE configs 0-3), else the generic kernel.
-void select_kernel(dfm_ctx* c) {
+// Kernel selection: compile-time-shape instantiations for uniform layouts of
+// the BASELINE configurations (0-3), else the generic kernels.
+void select_kernels(dfm_ctx* c) {
   bool uniform = true;
   for (int b = 1; b < c->L.nb; ++b) uniform = uniform && c->L.mb[b] == c->L.mb[0];
-  const int mb = c->L.mb[0], nb = c->L.nb, N = c->N;
-  c->kbin = nullptr;
+  const int mb = c->L.mb[0], nb = c->L.nb, N = c->N, K = c->K;
+  c->kem = nullptr;
+  c->kpd = nullptr;
   if (uniform && !c->force_generic) {
-    if (mb == 4 && nb == 3 && N == 5 && c->K == 16) { c->kbin = k_bin<4, 3, 5, 16, 4>; c->kmaxmb = 4; }
-    else if (mb == 2 && nb == 2 && N == 3 && c->K == 4) { c->kbin = k_bin<2, 2, 3, 4, 2>; c->kmaxmb = 2; }
-    else if (mb == 4 && nb == 8 && N == 8 && c->K == 32) { c->kbin = k_bin<4, 8, 8, 32, 4>; c->kmaxmb = 4; }
-    else if (mb == 12 && nb == 1 && N == 5 && c->K == 16) { c->kbin = k_bin<12, 1, 5, 16, 12>; c->kmaxmb = 12; }
+    if (mb == 4 && nb == 3 && N == 5 && K == 16) {
+      c->kem = k_em_bin<4, 3, 5, 4>; c->kpd = k_pd<4, 3, 5, 16, 4>; c->kmaxmb = 4;
+    } else if (mb == 2 && nb == 2 && N == 3 && K == 4) {
+      c->kem = k_em_bin<2, 2, 3, 2>; c->kpd = k_pd<2, 2, 3, 4, 2>; c->kmaxmb = 2;
+    } else if (mb == 4 && nb == 8 && N == 8 && K == 32) {
+      c->kem = k_em_bin<4, 8, 8, 4>; c->kpd = k_pd<4, 8, 8, 32, 4>; c->kmaxmb = 4;
+    } else if (mb == 12 && nb == 1 && N == 5 && K == 16) {
+      c->kem = k_em_bin<12, 1, 5, 12>; c->kpd = k_pd<12, 1, 5, 16, 12>; c->kmaxmb = 12;
+    }
   }
-  if (!c->kbin) {
-    if (c->maxmb <= 4) { c->kbin = k_bin<0, 0, 0, 0, 4>; c->kmaxmb = 4; }
-    else { c->kbin = k_bin<0, 0, 0, 0, DFM_MAX_MB>; c->kmaxmb = DFM_MAX_MB; }
+  if (!c->kem) {
+    if (c->maxmb <= 4) {
+      c->kem = k_em_bin<0, 0, 0, 4>; c->kpd = k_pd<0, 0, 0, 0, 4>; c->kmaxmb = 4;
+    } else {
+      c->kem = k_em_bin<0, 0, 0, DFM_MAX_MB>; c->kpd = k_pd<0, 0, 0, 0, DFM_MAX_MB>; c->kmaxmb = DFM_MAX_MB;
+    }
   }
 }
 
-size_t smem_for(dfm_ctx* c, int G, int CS, int& Ts, int& Tsp, int& threads) {
-  Ts = (c->T + CS - 1) / CS;
-  Tsp = Ts | 1;
-  threads = std::min(kThreads, std::max(64, (G * Ts + 31) / 32 * 32));
-  BinArgs a;
-  {
-    const int sG = c->G, sCS = c->CS, sTs = c->Ts, sTsp = c->Tsp;
-    c->G = G;
-    c->CS = CS;
-    c->Ts = Ts;
-    c->Tsp = Tsp;
-    a = make_args(c);
-    c->G = sG;
-    c->CS = sCS;
-    c->Ts = sTs;
-    c->Tsp = sTsp;
-  }
-  return plan_total(a, threads, c->kmaxmb);
-}
-
-// Tiling heuristic: keep each CTA's frame slice resident (<= ~113 KB so two
-// clusters' CTAs share an SM), prefer more bins per group (V reuse) and
-// enough CTAs to fill 148 SMs twice.
+// Tiling: the frame tile FT of k_em_bin minimises (waves of resident CTAs)
+// x (tiles per CTA); the frame tile TB of k_pd keeps its V tile <= 64 KB.
 bool choose_tiling(dfm_ctx* c) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-  struct Cand {
-    int G, CS;
-    size_t smem;
-    double score;
-  } best{1, 1, 0, -1e30};
-  const int csl[] = {1, 2, 4, 8, 16};
-  for (int G = 1; G <= kGMax; ++G)
-    for (int CS : csl) {
-      if (c->req_G && G != c->req_G) continue;
-      if (c->req_CS && CS != c->req_CS) continue;
-      if (CS > c->T) continue;
-      int Ts, Tsp, thr;
-      const size_t sm = smem_for(c, G, CS, Ts, Tsp, thr);
-      if (sm > 227 * 1024) continue;
-      const int ngroups = (c->F + G - 1) / G;
-      const double ctas = (double)ngroups * CS;
-      const int per_sm = std::max(1, (int)((228 * 1024) / (sm + 1024)));
-      double score = 0.0;
-      score += std::min(1.0, ctas / (2.0 * sms)) * 4.0;  // fill the machine
-      score += per_sm >= 2 ? 2.0 : 0.0;                   // two CTAs per SM
-      score += 0.5 * G;                                   // V reuse across bins
-      score -= CS > 8 ? 1.0 : 0.0;                        // non-portable cluster
-      score -= 0.05 * CS;                                 // cluster sync cost
-      score += std::min(1.0, (double)(G * Ts) / 256.0);   // busy threads
-      if (score > best.score) best = Cand{G, CS, sm, score};
+  const EmArgs a = make_args(c);
+  double best = 1e30;
+  int bestFT = 0;
+  for (int FT : {256, 128, 64, 32}) {
+    if (c->req_FT && FT != c->req_FT) continue;
+    const size_t sm = em_smem(a, FT, c->kmaxmb);
+    if (sm > 227 * 1024) continue;
+    const int by_smem = (int)((228 * 1024) / (sm + 1024));
+    const int by_regs = 65536 / (FT * 128);
+    const int per_sm = std::max(1, std::min({by_smem, by_regs, 2048 / FT, 32}));
+    const double waves = std::ceil((double)c->F / (sms * per_sm));
+    const double score = waves * std::ceil((double)c->T / FT) + 0.01 * FT / 256.0;
+    if (score < best) {
+      best = score;
+      bestFT = FT;
     }
-  if (best.score == -1e30) {
-    set_error("no feasible tiling (shared memory exceeds 227 KB per CTA)");
+  }
+  if (!bestFT) {
+    set_error("no feasible frame tile for the bin kernel (shared memory)");
     return false;
   }
-  c->G = best.G;
-  c->CS = best.CS;
-  c->smem = (int)smem_for(c, c->G, c->CS, c->Ts, c->Tsp, c->threads);
-  c->ngroups = (c->F + c->G - 1) / c->G;
+  c->FT = bestFT;
+  c->smem_em = (int)em_smem(a, c->FT, c->kmaxmb);
+  int TB = c->req_TB ? c->req_TB : 64;
+  while (TB > 8 && (size_t)c->N * c->K * TB * 8 > 64 * 1024) TB /= 2;
+  c->TB = TB;
+  c->smem_pd = (int)(((size_t)c->N * c->K * TB + kPdFB * c->N * c->K + kPdFB * c->N * c->M + 1) * 8 +
+                     (size_t)kPdFB * c->L.wsz * 16 + 16);
+  c->smem_tupd = (int)((2 * kTupdFB * kTupdTC + (size_t)c->K * kTupdVS) * 8);
+  c->smem_spec = (int)(((size_t)c->K * kSpecTB + kSpecFB * c->K) * 8);
+  if (c->smem_pd > 227 * 1024) {
+    set_error("k_pd tile does not fit in shared memory");
+    return false;
+  }
   return true;
 }
 
-void launch_bin(dfm_ctx* c, int finish, int start, int slot) {
-  BinArgs a = make_args(c);
+void set_kernel_attrs(dfm_ctx* c) {
+  DFM_CK(cudaFuncSetAttribute(c->kem, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_em));
+  DFM_CK(cudaFuncSetAttribute(c->kpd, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_pd));
+  DFM_CK(cudaFuncSetAttribute(k_tupd, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_tupd));
+  DFM_CK(cudaFuncSetAttribute(k_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_spec));
+}
+
+void ensure_cost(dfm_ctx* c, int slots) {
+  if (c->cost_part.n < (size_t)slots * c->F) c->cost_part.alloc((size_t)slots * c->F);
+}
+
+void launch_spec(dfm_ctx* c) {
+  const dim3 grid((c->T + kSpecTB - 1) / kSpecTB, (c->F + kSpecFB - 1) / kSpecFB, c->N);
+  k_spec<<<grid, 256, c->smem_spec, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->V.p, c->H.p);
+  DFM_CK_LAUNCH();
+  c->launches++;
+}
+
+void launch_em(dfm_ctx* c, int finish, int start, int slot) {
+  EmArgs a = make_args(c);
   a.finish = finish;
   a.start = start;
-  a.cost_out = c->cost_part.p + (size_t)slot * c->ngroups;
+  a.cost_out = c->cost_part.p + (size_t)slot * c->F;
   a.trace = c->tracing ? c->trace.p : nullptr;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(c->ngroups * c->CS);
-  cfg.blockDim = dim3(c->threads);
-  cfg.dynamicSmemBytes = c->smem;
-  cfg.stream = c->stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = c->CS;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  DFM_CK(cudaLaunchKernelEx(&cfg, c->kbin, a));
+  c->kem<<<c->F, c->FT, c->smem_em, c->stream>>>(a);
+  DFM_CK_LAUNCH();
+  c->launches++;
+}
+
+void launch_tupd(dfm_ctx* c) {
+  const dim3 grid((c->F + kTupdFB - 1) / kTupdFB, c->N);
+  k_tupd<<<grid, 256, c->smem_tupd, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->V.p, c->Aw.p, c->Bw.p,
+                                                  c->floor_);
+  DFM_CK_LAUNCH();
+  c->launches++;
+}
+
+void launch_pd(dfm_ctx* c) {
+  EmArgs a = make_args(c);
+  const dim3 grid((c->T + c->TB - 1) / c->TB, (c->F + kPdFB - 1) / kPdFB);
+  c->kpd<<<grid, kPdFB * c->TB, c->smem_pd, c->stream>>>(a, c->Tf.p, c->V.p, c->TB);
+  DFM_CK_LAUNCH();
   c->launches++;
 }
 
 void launch_vupd(dfm_ctx* c) {
   const dim3 grid((c->T + 31) / 32, c->N, (c->K + kVupdKPT - 1) / kVupdKPT);
   const bool sharded = c->comm != nullptr && c->nranks > 1;
-  k_vupd<<<grid, 32 * kVupdWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->Ap.p, c->Bp.p, c->V.p,
-                                      sharded ? c->numden.p : nullptr, c->floor_);
+  k_vupd<<<grid, 32 * kVupdWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->Aw.p, c->Bw.p, c->V.p,
+                                                   sharded ? c->numden.p : nullptr, c->floor_);
   DFM_CK_LAUNCH();
   c->launches++;
   if (sharded) {
@@ -313,13 +292,16 @@ void launch_vupd(dfm_ctx* c) {
   }
 }
 
-void ensure_cost(dfm_ctx* c, int slots) {
-  if (c->cost_part.n < (size_t)slots * c->ngroups) c->cost_part.alloc((size_t)slots * c->ngroups);
-}
-
-void set_kernel_attrs(dfm_ctx* c) {
-  DFM_CK(cudaFuncSetAttribute(c->kbin, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem));
-  DFM_CK(cudaFuncSetAttribute(c->kbin, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+// The "start" half of an iteration after k_em_bin: T update, V-update
+// weights, V update, and the spectrogram for the next k_em_bin.
+void launch_rest(dfm_ctx* c, cudaEvent_t* ev) {
+  launch_tupd(c);
+  if (ev) DFM_CK(cudaEventRecord(ev[2], c->stream));
+  launch_pd(c);
+  if (ev) DFM_CK(cudaEventRecord(ev[3], c->stream));
+  launch_vupd(c);
+  if (ev) DFM_CK(cudaEventRecord(ev[4], c->stream));
+  launch_spec(c);
 }
 
 }  // namespace
@@ -370,19 +352,18 @@ dfm_ctx* dfm_create(int F, int T, int nblocks, const int* block_sizes, int N, in
     c->L = L;
     c->maxmb = 1;
     for (int b = 0; b < L.nb; ++b) c->maxmb = std::max(c->maxmb, L.mb[b]);
-    select_kernel(c);
+    select_kernels(c);
     DFM_CK(cudaSetDevice(device));
     DFM_CK(cudaStreamCreate(&c->stream));
-    DFM_CK(cudaEventCreate(&c->eb0));
-    DFM_CK(cudaEventCreate(&c->eb1));
-    DFM_CK(cudaEventCreate(&c->ebm));
+    for (auto& e : c->ev) DFM_CK(cudaEventCreate(&e));
     c->x.alloc((size_t)c->F * T * c->M);
     c->W.alloc((size_t)c->F * L.wsz);
     c->Tf.alloc((size_t)c->F * N * K);
     c->V.alloc((size_t)N * K * T);
     c->lam.alloc((size_t)c->F * N * c->M);
-    c->Ap.alloc((size_t)N * c->F * T);
-    c->Bp.alloc((size_t)N * c->F * T);
+    c->H.alloc((size_t)c->F * N * T);
+    c->Aw.alloc((size_t)N * c->F * T);
+    c->Bw.alloc((size_t)N * c->F * T);
     c->numden.alloc(2 * (size_t)N * K * T);
     c->fallbacks.alloc(1);
     DFM_CK(cudaMemset(c->fallbacks.p, 0, sizeof(int)));
@@ -401,9 +382,8 @@ void dfm_destroy(dfm_ctx* c) {
   cudaSetDevice(c->device);
   if (c->comm) nccl().CommDestroy(c->comm);
   for (auto e : c->iter_ev) cudaEventDestroy(e);
-  if (c->eb0) cudaEventDestroy(c->eb0);
-  if (c->eb1) cudaEventDestroy(c->eb1);
-  if (c->ebm) cudaEventDestroy(c->ebm);
+  for (auto e : c->ev)
+    if (e) cudaEventDestroy(e);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -538,20 +518,20 @@ int dfm_fit(dfm_ctx* c, int iters, double* cost_trace, double* wall_seconds, dou
     c->iter_ev.push_back(e);
   }
   // launch i (0..iters): finish iteration i-1 (cost-only for i = 0), start iteration i
+  launch_spec(c);
   for (int i = 0; i <= iters; ++i) {
     DFM_CK(cudaEventRecord(c->iter_ev[i], c->stream));
-    launch_bin(c, i == 0 ? 1 : 2, i < iters ? 1 : 0, i);
-    if (i < iters) launch_vupd(c);
+    launch_em(c, i == 0 ? 1 : 2, i < iters ? 1 : 0, i);
+    if (i < iters) launch_rest(c, nullptr);
   }
-  DFM_CK(cudaEventRecord(c->iter_ev[iters + 1], c->stream));
-  std::vector<double> part((size_t)(iters + 1) * c->ngroups);
+  std::vector<double> part((size_t)(iters + 1) * c->F);
   c->cost_part.download(part.data(), part.size(), c->stream);
   int fb = 0;
   c->fallbacks.download(&fb, 1, c->stream);
   DFM_CK(cudaStreamSynchronize(c->stream));
   std::vector<double> cost(iters + 1, 0.0);
   for (int i = 0; i <= iters; ++i)
-    for (int g = 0; g < c->ngroups; ++g) cost[i] += part[(size_t)i * c->ngroups + g];
+    for (int f = 0; f < c->F; ++f) cost[i] += part[(size_t)i * c->F + f];
   if (c->comm && c->nranks > 1) {
     if (c->cost_sum.n < (size_t)iters + 1) c->cost_sum.alloc(iters + 1);
     c->cost_sum.upload(cost.data(), iters + 1, c->stream);
@@ -582,8 +562,9 @@ int dfm_prime(dfm_ctx* c) {
   DFM_API_BEGIN
   DFM_CK(cudaSetDevice(c->device));
   ensure_cost(c, 2);
-  launch_bin(c, 1, 1, 0);
-  launch_vupd(c);
+  launch_spec(c);
+  launch_em(c, 1, 1, 0);
+  launch_rest(c, nullptr);
   return DFM_OK;
   DFM_API_END
 }
@@ -591,11 +572,11 @@ int dfm_prime(dfm_ctx* c) {
 int dfm_bench_step(dfm_ctx* c) {
   if (!c) return DFM_ERR_ARG;
   DFM_API_BEGIN
-  DFM_CK(cudaEventRecord(c->eb0, c->stream));
-  launch_bin(c, 2, 1, 1);
-  DFM_CK(cudaEventRecord(c->ebm, c->stream));
-  launch_vupd(c);
-  DFM_CK(cudaEventRecord(c->eb1, c->stream));
+  DFM_CK(cudaEventRecord(c->ev[0], c->stream));
+  launch_em(c, 2, 1, 1);
+  DFM_CK(cudaEventRecord(c->ev[1], c->stream));
+  launch_rest(c, c->ev);
+  DFM_CK(cudaEventRecord(c->ev[5], c->stream));
   return DFM_OK;
   DFM_API_END
 }
@@ -610,38 +591,38 @@ int dfm_sync(dfm_ctx* c) {
 
 double dfm_bench_last_ms(dfm_ctx* c) {
   if (!c) return -1.0;
-  if (cudaEventSynchronize(c->eb1) != cudaSuccess) return -1.0;
+  if (cudaEventSynchronize(c->ev[5]) != cudaSuccess) return -1.0;
   float ms = 0.f;
-  if (cudaEventElapsedTime(&ms, c->eb0, c->eb1) != cudaSuccess) return -1.0;
+  if (cudaEventElapsedTime(&ms, c->ev[0], c->ev[5]) != cudaSuccess) return -1.0;
   return ms;
 }
 
-int dfm_bench_last_split(dfm_ctx* c, double* bin_ms, double* vupd_ms) {
-  if (!c) return DFM_ERR_ARG;
+int dfm_bench_last_split(dfm_ctx* c, double* ms5) {
+  if (!c || !ms5) return DFM_ERR_ARG;
   DFM_API_BEGIN
-  DFM_CK(cudaEventSynchronize(c->eb1));
-  float a = 0.f, b = 0.f;
-  DFM_CK(cudaEventElapsedTime(&a, c->eb0, c->ebm));
-  DFM_CK(cudaEventElapsedTime(&b, c->ebm, c->eb1));
-  if (bin_ms) *bin_ms = a;
-  if (vupd_ms) *vupd_ms = b;
+  DFM_CK(cudaEventSynchronize(c->ev[5]));
+  for (int i = 0; i < 5; ++i) {
+    float v = 0.f;
+    DFM_CK(cudaEventElapsedTime(&v, c->ev[i], c->ev[i + 1]));
+    ms5[i] = v;
+  }
   return DFM_OK;
   DFM_API_END
 }
 
 long long dfm_launch_count(const dfm_ctx* c) { return c ? c->launches : -1; }
 
-int dfm_set_tiling(dfm_ctx* c, int bins_per_cta, int cluster_size) {
-  if (!c || bins_per_cta < 0 || bins_per_cta > kGMax || cluster_size < 0 || cluster_size > 16)
+int dfm_set_tiling(dfm_ctx* c, int frame_tile, int pd_frames) {
+  if (!c || frame_tile < 0 || frame_tile > 256 || (frame_tile & 31) || pd_frames < 0 || pd_frames > 64)
     return DFM_ERR_ARG;
   DFM_API_BEGIN
   DFM_CK(cudaSetDevice(c->device));
-  const int oG = c->req_G, oCS = c->req_CS;
-  c->req_G = bins_per_cta;
-  c->req_CS = cluster_size;
+  const int oFT = c->req_FT, oTB = c->req_TB;
+  c->req_FT = frame_tile;
+  c->req_TB = pd_frames;
   if (!choose_tiling(c)) {
-    c->req_G = oG;
-    c->req_CS = oCS;
+    c->req_FT = oFT;
+    c->req_TB = oTB;
     choose_tiling(c);
     return DFM_ERR_UNSUPPORTED;
   }
@@ -656,7 +637,7 @@ int dfm_set_trace(dfm_ctx* c, int on) {
   DFM_CK(cudaSetDevice(c->device));
   c->tracing = on != 0;
   if (c->tracing) {
-    c->trace.alloc((size_t)c->ngroups * c->CS * 16);
+    c->trace.alloc((size_t)c->F * 16);
     DFM_CK(cudaMemset(c->trace.p, 0, sizeof(unsigned long long) * c->trace.n));
   }
   return (int)std::min<size_t>(c->trace.n, 0x7fffffff);
@@ -679,20 +660,20 @@ int dfm_force_generic(dfm_ctx* c, int on) {
   DFM_API_BEGIN
   DFM_CK(cudaSetDevice(c->device));
   c->force_generic = on != 0;
-  select_kernel(c);
+  select_kernels(c);
   if (!choose_tiling(c)) return DFM_ERR_UNSUPPORTED;
   set_kernel_attrs(c);
   return DFM_OK;
   DFM_API_END
 }
 
-int dfm_get_tiling(const dfm_ctx* c, int* G, int* CS, int* Ts, int* threads, int* smem) {
+int dfm_get_tiling(const dfm_ctx* c, int* frame_tile, int* pd_frames, int* ctas, int* threads, int* smem) {
   if (!c) return DFM_ERR_ARG;
-  if (G) *G = c->G;
-  if (CS) *CS = c->CS;
-  if (Ts) *Ts = c->Ts;
-  if (threads) *threads = c->threads;
-  if (smem) *smem = c->smem;
+  if (frame_tile) *frame_tile = c->FT;
+  if (pd_frames) *pd_frames = c->TB;
+  if (ctas) *ctas = c->F;
+  if (threads) *threads = c->FT;
+  if (smem) *smem = c->smem_em;
   return DFM_OK;
 }
 

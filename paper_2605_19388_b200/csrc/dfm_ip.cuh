@@ -1,0 +1,501 @@
+// Small dense solvers of the IP update and shared device helpers of the EM
+// kernels (engine.cpp:17-58; hermlin.cpp:19-23).  Included by dfm_engine.cu.
+#pragma once
+
+namespace dfm {
+
+template <int MB>
+struct IpWork;
+template <int MAXMB>
+__host__ __device__ inline size_t ipscr_bytes();
+
+__device__ __forceinline__ void decode_entry(int e, int& r, int& c) {
+  c = 0;
+  while ((c + 1) * (c + 2) / 2 <= e) ++c;
+  r = e - c * (c + 1) / 2;
+}
+
+// ln(prod v) accumulated as mantissa product x 2^exponent-sum: one log per
+// thread instead of one per (frame, mic) (engine.cpp:155, sum of ln eta).
+struct LogAcc {
+  double mant = 1.0;
+  int ex = 0;
+  __device__ __forceinline__ void mul(double v) {  // v > 0, normal
+    const int hi = __double2hiint(v), lo = __double2loint(v);
+    ex += ((hi >> 20) & 0x7ff) - 1023;
+    mant *= __hiloint2double((hi & 0x800fffff) | 0x3ff00000, lo);
+  }
+  __device__ __forceinline__ void renorm() {
+    const int hi = __double2hiint(mant), lo = __double2loint(mant);
+    ex += ((hi >> 20) & 0x7ff) - 1023;
+    mant = __hiloint2double((hi & 0x800fffff) | 0x3ff00000, lo);
+  }
+  __device__ __forceinline__ double value() const { return log(mant) + (double)ex * 0.69314718055994530942; }
+};
+
+// Single-thread IP update of one (bin, block) system with MB <= 4 held in
+// registers (engine.cpp:44-51): S = W^H Q_mu, partial-pivot LU, solve for
+// e_mu, pinv fallback when u is not finite or ||S u - e|| > 1e-6,
+// u /= sqrt(max(Re(u^H Q u), floor)).  The residual is formed as
+// W^H (Q u) - e, sharing Q u with the normaliser.  W: shared MB x MB
+// col-major (updated in place); qb: packed upper triangles of Q_0..Q_{MB-1}.
+template <int MB>
+__device__ int ip_solve_thread(cd* W, const cd* qb, double floor_, IpScratch<MB>& scr) {
+  constexpr int E = MB * (MB + 1) / 2;
+  int fb = 0;
+#pragma unroll 1
+  for (int mu = 0; mu < MB; ++mu) {
+    const cd* qp = qb + mu * E;
+    auto Q = [&](int r, int c) -> cd { return r <= c ? qp[c * (c + 1) / 2 + r] : conjg(qp[r * (r + 1) / 2 + c]); };
+    cd L[MB][MB];
+#pragma unroll
+    for (int r = 0; r < MB; ++r)
+#pragma unroll
+      for (int c = 0; c < MB; ++c) {
+        cd s{0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < MB; ++k) s = s + cmulc(W[r * MB + k], Q(k, c));
+        L[r][c] = s;
+      }
+    int perm[MB];
+    cd inv[MB];
+#pragma unroll
+    for (int k = 0; k < MB; ++k) {
+      int piv = k;
+      double best = norm2(L[k][k]);
+#pragma unroll
+      for (int r = k + 1; r < MB; ++r) {
+        const double v = norm2(L[r][k]);
+        if (v > best) {
+          best = v;
+          piv = r;
+        }
+      }
+      perm[k] = piv;
+#pragma unroll
+      for (int r = k + 1; r < MB; ++r)
+        if (piv == r)
+#pragma unroll
+          for (int c = 0; c < MB; ++c) {
+            const cd t = L[k][c];
+            L[k][c] = L[r][c];
+            L[r][c] = t;
+          }
+      if (best != 0.0) {
+        const double id = 1.0 / best;
+        inv[k] = cd{L[k][k].re * id, -L[k][k].im * id};
+#pragma unroll
+        for (int r = k + 1; r < MB; ++r) L[r][k] = L[r][k] * inv[k];
+      } else {
+        inv[k] = cd{INFINITY, 0.0};  // singular: the solve goes non-finite -> pinv
+      }
+#pragma unroll
+      for (int r = k + 1; r < MB; ++r)
+#pragma unroll
+        for (int c = k + 1; c < MB; ++c) L[r][c] = L[r][c] - L[r][k] * L[k][c];
+    }
+    cd u[MB];
+#pragma unroll
+    for (int q = 0; q < MB; ++q) u[q] = cd{q == mu ? 1.0 : 0.0, 0.0};
+#pragma unroll
+    for (int k = 0; k < MB; ++k)
+#pragma unroll
+      for (int r = k + 1; r < MB; ++r)
+        if (perm[k] == r) {
+          const cd t = u[k];
+          u[k] = u[r];
+          u[r] = t;
+        }
+#pragma unroll
+    for (int r = 1; r < MB; ++r)
+#pragma unroll
+      for (int c = 0; c < r; ++c) u[r] = u[r] - L[r][c] * u[c];
+#pragma unroll
+    for (int r = MB - 1; r >= 0; --r) {
+#pragma unroll
+      for (int c = r + 1; c < MB; ++c) u[r] = u[r] - L[r][c] * u[c];
+      u[r] = u[r] * inv[r];
+    }
+    bool fin = true;
+#pragma unroll
+    for (int q = 0; q < MB; ++q) fin = fin && cfinite(u[q]);
+    cd qu[MB];
+    double r2 = 0.0;
+    if (fin) {
+#pragma unroll
+      for (int a = 0; a < MB; ++a) {
+        cd s{0.0, 0.0};
+#pragma unroll
+        for (int c = 0; c < MB; ++c) s = s + Q(a, c) * u[c];
+        qu[a] = s;
+      }
+#pragma unroll
+      for (int a = 0; a < MB; ++a) {
+        cd s{0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < MB; ++k) s = s + cmulc(W[a * MB + k], qu[k]);
+        if (a == mu) s.re -= 1.0;
+        r2 += norm2(s);
+      }
+    }
+    if (!fin || sqrt(r2) > 1e-6) {
+      fb += 1;
+      for (int a = 0; a < MB; ++a)
+        for (int c = 0; c < MB; ++c) {
+          cd s{0.0, 0.0};
+          for (int k = 0; k < MB; ++k) s = s + cmulc(W[a * MB + k], Q(k, c));
+          scr.S0[c * MB + a] = s;
+        }
+      for (int q = 0; q < MB; ++q) scr.e[q] = cd{q == mu ? 1.0 : 0.0, 0.0};
+      pinv_solve_serial(MB, scr.S0, scr.V, scr.e, scr.u);
+#pragma unroll
+      for (int q = 0; q < MB; ++q) u[q] = scr.u[q];
+#pragma unroll
+      for (int a = 0; a < MB; ++a) {
+        cd s{0.0, 0.0};
+#pragma unroll
+        for (int c = 0; c < MB; ++c) s = s + Q(a, c) * u[c];
+        qu[a] = s;
+      }
+    }
+    double nq = 0.0;
+#pragma unroll
+    for (int a = 0; a < MB; ++a) nq += cmulc(u[a], qu[a]).re;
+    const double sc = sqrt(fmax(nq, floor_));
+#pragma unroll
+    for (int a = 0; a < MB; ++a) W[mu * MB + a] = cdivr(u[a], sc);
+  }
+  return fb;
+}
+
+template <int MAXMB>
+__host__ __device__ inline size_t ipscr_bytes() {
+  if constexpr (MAXMB <= 4)
+    return (sizeof(IpWork<MAXMB>) + 15) / 16 * 16;
+  else
+    return (sizeof(IpScratch<MAXMB>) + 15) / 16 * 16;
+}
+
+// Per owned (bin, block) system scratch of the fast IP path (MB <= 4).
+template <int MB>
+struct IpWork {
+  IpScratch<MB> slow;            // exact LU + pinv path (fallback)
+  cd Winv[MB * MB];              // W^-1, col-major
+  cd Wold[MB * MB];              // W before the sweep (restored on fallback)
+  cd L[MB][MB * (MB + 1) / 2];   // Cholesky factor of each Q_mu, packed lower
+  double dinv[MB][MB];           // 1 / L(c, c)
+  int ok[MB];
+};
+
+// 2 ln|det W| (engine.cpp:17-26, :161-165) and W^-1 from one partial-pivot
+// LU held in registers, one thread.  A singular W gives -inf (the fit then
+// records a +inf cost, engine.hpp:41-43) and a non-finite inverse, which
+// sends the IP sweep to the exact fallback.
+template <int MB>
+__device__ double logdet2_inverse_thread(const cd* W, cd* Winv) {
+  cd L[MB][MB];
+#pragma unroll
+  for (int r = 0; r < MB; ++r)
+#pragma unroll
+    for (int c = 0; c < MB; ++c) L[r][c] = W[c * MB + r];
+  double acc = 0.0;
+  bool sing = false;
+  int perm[MB];
+  cd inv[MB];
+#pragma unroll
+  for (int k = 0; k < MB; ++k) {
+    int piv = k;
+    double best = norm2(L[k][k]);
+#pragma unroll
+    for (int r = k + 1; r < MB; ++r) {
+      const double v = norm2(L[r][k]);
+      if (v > best) {
+        best = v;
+        piv = r;
+      }
+    }
+    perm[k] = piv;
+#pragma unroll
+    for (int r = k + 1; r < MB; ++r)
+      if (piv == r)
+#pragma unroll
+        for (int c = 0; c < MB; ++c) {
+          const cd t = L[k][c];
+          L[k][c] = L[r][c];
+          L[r][c] = t;
+        }
+    if (best != 0.0) {
+      const double id = 1.0 / best;
+      inv[k] = cd{L[k][k].re * id, -L[k][k].im * id};
+#pragma unroll
+      for (int r = k + 1; r < MB; ++r) L[r][k] = L[r][k] * inv[k];
+      acc += 0.5 * log(best);
+    } else {
+      sing = true;
+      inv[k] = cd{INFINITY, 0.0};
+    }
+#pragma unroll
+    for (int r = k + 1; r < MB; ++r)
+#pragma unroll
+      for (int c = k + 1; c < MB; ++c) L[r][c] = L[r][c] - L[r][k] * L[k][c];
+  }
+#pragma unroll 1
+  for (int col = 0; col < MB; ++col) {
+    cd v[MB];
+#pragma unroll
+    for (int r = 0; r < MB; ++r) v[r] = cd{r == col ? 1.0 : 0.0, 0.0};
+#pragma unroll
+    for (int k = 0; k < MB; ++k)
+#pragma unroll
+      for (int r = k + 1; r < MB; ++r)
+        if (perm[k] == r) {
+          const cd t = v[k];
+          v[k] = v[r];
+          v[r] = t;
+        }
+#pragma unroll
+    for (int r = 1; r < MB; ++r)
+#pragma unroll
+      for (int c = 0; c < r; ++c) v[r] = v[r] - L[r][c] * v[c];
+#pragma unroll
+    for (int r = MB - 1; r >= 0; --r) {
+#pragma unroll
+      for (int c = r + 1; c < MB; ++c) v[r] = v[r] - L[r][c] * v[c];
+      v[r] = v[r] * inv[r];
+    }
+#pragma unroll
+    for (int r = 0; r < MB; ++r) Winv[col * MB + r] = v[r];
+  }
+  return sing ? -INFINITY : 2.0 * acc;
+}
+
+// Cholesky Q_mu = L L^H of one weighted covariance (Hermitian, packed upper
+// triangle qp), one thread; false when Q_mu is not numerically positive
+// definite (the exact fallback then decides, as the reference's LU would).
+template <int MB>
+__device__ bool chol_thread(const cd* qp, cd* L, double* dinv) {
+  auto Q = [&](int r, int c) -> cd { return r <= c ? qp[c * (c + 1) / 2 + r] : conjg(qp[r * (r + 1) / 2 + c]); };
+  auto Li = [](int r, int c) { return r * (r + 1) / 2 + c; };
+#pragma unroll
+  for (int c = 0; c < MB; ++c) {
+    double d = Q(c, c).re;
+#pragma unroll
+    for (int k = 0; k < c; ++k) d -= norm2(L[Li(c, k)]);
+    if (!(d > 0.0) || !isfinite(d)) return false;
+    const double lc = sqrt(d);
+    dinv[c] = 1.0 / lc;
+    L[Li(c, c)] = cd{lc, 0.0};
+#pragma unroll
+    for (int r = c + 1; r < MB; ++r) {
+      cd s = Q(r, c);
+#pragma unroll
+      for (int k = 0; k < c; ++k) s = s - L[Li(r, k)] * conjg(L[Li(c, k)]);
+      L[Li(r, c)] = s * dinv[c];
+    }
+  }
+  return true;
+}
+
+// Fast IP sweep of one system (engine.cpp:40-51 for mu = 0..MB-1):
+//   u = (W^H Q_mu)^-1 e_mu = Q_mu^-1 W^-H e_mu  (two triangular solves),
+//   u /= sqrt(max(Re(u^H Q u), floor)),  W[:, mu] = u,
+//   W^-1 refreshed by Sherman-Morrison for the replaced column.
+// Every column still passes the reference's test ||W^H Q u - e_mu|| <= 1e-6
+// (with the current W, as engine.cpp:47-49); any failure returns false and
+// the caller reruns the exact LU + pinv sweep from W_old.
+template <int MB>
+__device__ bool ip_sweep_fast(cd* W, IpWork<MB>& f, const cd* qb, double floor_) {
+  constexpr int E = MB * (MB + 1) / 2;
+#pragma unroll
+  for (int mu = 0; mu < MB; ++mu)
+    if (!f.ok[mu]) return false;
+  auto Li = [](int r, int c) { return r * (r + 1) / 2 + c; };
+#pragma unroll 1
+  for (int mu = 0; mu < MB; ++mu) {
+    const cd* qp = qb + mu * E;
+    auto Q = [&](int r, int c) -> cd { return r <= c ? qp[c * (c + 1) / 2 + r] : conjg(qp[r * (r + 1) / 2 + c]); };
+    const cd* L = f.L[mu];
+    const double* di = f.dinv[mu];
+    cd u[MB];
+    // L y = W^-H e_mu  (b_k = conj(Winv(mu, k)))
+#pragma unroll
+    for (int r = 0; r < MB; ++r) {
+      cd s = conjg(f.Winv[r * MB + mu]);
+#pragma unroll
+      for (int c = 0; c < r; ++c) s = s - L[Li(r, c)] * u[c];
+      u[r] = s * di[r];
+    }
+    // L^H u = y
+#pragma unroll
+    for (int r = MB - 1; r >= 0; --r) {
+      cd s = u[r];
+#pragma unroll
+      for (int c = r + 1; c < MB; ++c) s = s - cmulc(L[Li(c, r)], u[c]);
+      u[r] = s * di[r];
+    }
+    cd qu[MB];
+    bool fin = true;
+#pragma unroll
+    for (int a = 0; a < MB; ++a) {
+      fin = fin && cfinite(u[a]);
+      cd s{0.0, 0.0};
+#pragma unroll
+      for (int c = 0; c < MB; ++c) s = s + Q(a, c) * u[c];
+      qu[a] = s;
+    }
+    double r2 = 0.0, nq = 0.0;
+#pragma unroll
+    for (int a = 0; a < MB; ++a) {
+      cd s{0.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < MB; ++k) s = s + cmulc(W[a * MB + k], qu[k]);
+      if (a == mu) s.re -= 1.0;
+      r2 += norm2(s);
+      nq += cmulc(u[a], qu[a]).re;
+    }
+    if (!fin || !(sqrt(r2) <= 1e-6)) return false;
+    const double sc = sqrt(fmax(nq, floor_));
+    cd d[MB];
+#pragma unroll
+    for (int a = 0; a < MB; ++a) {
+      u[a] = cdivr(u[a], sc);
+      d[a] = u[a] - W[mu * MB + a];
+    }
+    // Sherman-Morrison: (W + d e_mu^T)^-1 = W^-1 - z (e_mu^T W^-1) / (1 + z_mu), z = W^-1 d
+    cd z[MB];
+#pragma unroll
+    for (int r = 0; r < MB; ++r) {
+      cd s{0.0, 0.0};
+#pragma unroll
+      for (int c = 0; c < MB; ++c) s = s + f.Winv[c * MB + r] * d[c];
+      z[r] = s;
+    }
+    const cd den = cd{1.0 + z[mu].re, z[mu].im};
+    const double dn = norm2(den);
+    if (!(dn > 0.0)) return false;
+    const cd iden{den.re / dn, -den.im / dn};
+    cd row[MB];
+#pragma unroll
+    for (int c = 0; c < MB; ++c) row[c] = f.Winv[c * MB + mu] * iden;
+#pragma unroll
+    for (int c = 0; c < MB; ++c)
+#pragma unroll
+      for (int r = 0; r < MB; ++r) f.Winv[c * MB + r] = f.Winv[c * MB + r] - z[r] * row[c];
+#pragma unroll
+    for (int a = 0; a < MB; ++a) W[mu * MB + a] = u[a];
+  }
+  return true;
+}
+
+// Quad-cooperative version of ip_sweep_fast: the MB (<= 4) lanes of one
+// 4-lane segment own rows l of the triangular solves, of Q u, of the
+// residual and of the Sherman-Morrison update, exchanging values with
+// width-4 shuffles.  Same algebra and the same reference residual test as
+// ip_sweep_fast; every early exit is uniform across the quad.
+__device__ __forceinline__ cd shfl4(unsigned mask, cd v, int src) {
+  return cd{__shfl_sync(mask, v.re, src, 4), __shfl_sync(mask, v.im, src, 4)};
+}
+
+template <int MB>
+__device__ bool ip_sweep_quad(cd* W, IpWork<MB>& f, const cd* qb, double floor_, int l, unsigned mask) {
+  constexpr int E = MB * (MB + 1) / 2;
+  bool okall = true;
+#pragma unroll
+  for (int mu = 0; mu < MB; ++mu) okall = okall && f.ok[mu];
+  if (!okall) return false;
+  auto Li = [](int r, int c) { return r * (r + 1) / 2 + c; };
+  const bool act = l < MB;
+  const int la = act ? l : 0;
+#pragma unroll 1
+  for (int mu = 0; mu < MB; ++mu) {
+    const cd* L = f.L[mu];
+    const double* di = f.dinv[mu];
+    const cd* qp = qb + mu * E;
+    auto Q = [&](int r, int c) -> cd { return r <= c ? qp[c * (c + 1) / 2 + r] : conjg(qp[r * (r + 1) / 2 + c]); };
+    // forward: L y = b, b_l = conj(Winv(mu, l))
+    cd acc = act ? conjg(f.Winv[la * MB + mu]) : cd{0.0, 0.0};
+    cd y{0.0, 0.0};
+#pragma unroll
+    for (int c = 0; c < MB; ++c) {
+      if (l == c) y = acc * di[c];
+      const cd yc = shfl4(mask, y, c);
+      if (act && l > c) acc = acc - L[Li(la, c)] * yc;
+    }
+    // backward: L^H u = y
+    acc = y;
+    cd u{0.0, 0.0};
+#pragma unroll
+    for (int c = MB - 1; c >= 0; --c) {
+      if (l == c) u = acc * di[c];
+      const cd uc = shfl4(mask, u, c);
+      if (act && l < c) acc = acc - cmulc(L[Li(c, la)], uc);
+    }
+    cd uv[MB];
+    bool fin = true;
+#pragma unroll
+    for (int c = 0; c < MB; ++c) {
+      uv[c] = shfl4(mask, u, c);
+      fin = fin && cfinite(uv[c]);
+    }
+    cd qu{0.0, 0.0};
+    if (act)
+#pragma unroll
+      for (int c = 0; c < MB; ++c) qu = qu + Q(la, c) * uv[c];
+    cd quv[MB];
+#pragma unroll
+    for (int c = 0; c < MB; ++c) quv[c] = shfl4(mask, qu, c);
+    double r2 = 0.0, nq = 0.0;
+    if (act) {
+      cd r{0.0, 0.0};
+#pragma unroll
+      for (int k = 0; k < MB; ++k) r = r + cmulc(W[la * MB + k], quv[k]);
+      if (l == mu) r.re -= 1.0;
+      r2 = norm2(r);
+      nq = cmulc(u, qu).re;
+    }
+    r2 += __shfl_xor_sync(mask, r2, 1, 4);
+    r2 += __shfl_xor_sync(mask, r2, 2, 4);
+    nq += __shfl_xor_sync(mask, nq, 1, 4);
+    nq += __shfl_xor_sync(mask, nq, 2, 4);
+    if (!fin || !(sqrt(r2) <= 1e-6)) return false;
+    const double sc = sqrt(fmax(nq, floor_));
+    const cd un = cdivr(u, sc);
+    const cd d = act ? un - W[mu * MB + la] : cd{0.0, 0.0};
+    cd dv[MB];
+#pragma unroll
+    for (int c = 0; c < MB; ++c) dv[c] = shfl4(mask, d, c);
+    cd z{0.0, 0.0};
+    if (act)
+#pragma unroll
+      for (int c = 0; c < MB; ++c) z = z + f.Winv[c * MB + la] * dv[c];
+    const cd zmu = shfl4(mask, z, mu);
+    const cd den{1.0 + zmu.re, zmu.im};
+    const double dn = norm2(den);
+    if (!(dn > 0.0)) return false;
+    const cd iden{den.re / dn, -den.im / dn};
+    cd row[MB];
+#pragma unroll
+    for (int c = 0; c < MB; ++c) row[c] = f.Winv[c * MB + mu] * iden;
+    __syncwarp(mask);
+    if (act) {
+#pragma unroll
+      for (int c = 0; c < MB; ++c) f.Winv[c * MB + la] = f.Winv[c * MB + la] - z * row[c];
+      W[mu * MB + la] = un;
+    }
+    __syncwarp(mask);
+  }
+  return true;
+}
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gmem_src) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+
+}  // namespace dfm

@@ -495,14 +495,14 @@ class Engine:
         check(self.lib.dfm_wiener(self.ctx, _ptr(img)), "wiener")
         return img
 
-    def set_tiling(self, bins_per_cta: int = 0, cluster_size: int = 0) -> None:
-        check(self.lib.dfm_set_tiling(self.ctx, bins_per_cta, cluster_size), "set_tiling")
+    def set_tiling(self, frame_tile: int = 0, pd_frames: int = 0) -> None:
+        """Frame tile (threads per CTA) of the per-bin kernel and of k_pd; 0 = heuristic."""
+        check(self.lib.dfm_set_tiling(self.ctx, frame_tile, pd_frames), "set_tiling")
 
     def tiling(self) -> dict:
         v = [C.c_int() for _ in range(5)]
         check(self.lib.dfm_get_tiling(self.ctx, *[C.byref(a) for a in v]))
-        return dict(zip(("bins_per_cta", "cluster_size", "frames_per_cta", "threads", "smem_bytes"),
-                        [a.value for a in v]))
+        return dict(zip(("frame_tile", "pd_frames", "ctas", "threads", "smem_bytes"), [a.value for a in v]))
 
     def launches(self) -> int:
         return int(self.lib.dfm_launch_count(self.ctx))

@@ -175,16 +175,16 @@ def test_engine_trajectory_matches_oracle(dfm, oracle, F, T, sizes, N, K, iters)
         assert _rel(a, b) < 1e-7
 
 
-@pytest.mark.parametrize("G,CS", [(1, 1), (2, 1), (1, 2), (3, 4), (4, 8), (2, 16)])
-def test_engine_tilings_agree(dfm, oracle, G, CS):
+@pytest.mark.parametrize("FT,TB", [(32, 8), (64, 16), (128, 32), (256, 64), (96, 64)])
+def test_engine_tilings_agree(dfm, oracle, FT, TB):
     F, T, sizes, N, K, iters = 11, 70, [4, 4, 4], 5, 8, 10
     layout = dfm.BlockLayout(sizes)
     x = dfm.generate_mixture(1, F, T, layout.total, N, K, 9)
     init = dfm.random_init(F, T, layout, N, K, 2)
     with dfm.Engine(F, T, layout, N, K) as eng:
-        eng.set_tiling(G, CS)
+        eng.set_tiling(FT, TB)
         t = eng.tiling()
-        assert (t["bins_per_cta"], t["cluster_size"]) == (G, CS)
+        assert (t["frame_tile"], t["pd_frames"]) == (FT, TB)
         eng.set_obs(x)
         eng.set_model(init.nmf, init.w0, init.lambda0)
         cost, _, _, _ = eng.fit(iters)

@@ -16,8 +16,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-PHASES = ["stage", "A:frames", "A:lambda-reduce", "B:frames", "B:logdet", "B:Q-accum", "B:Q-reduce",
-          "IP", "W-gather", "C:frames", "C:T-reduce", "D:frames"]
+PHASES = ["A:lambda (tiles + reduce)", "B:cost+Q (tiles)", "B:Q-reduce", "IP", "C:T-weights"]
 
 
 def main():
@@ -39,8 +38,8 @@ def main():
     if args.generic:
         dfm._capi.check(lib.dfm_force_generic(eng.ctx, 1))
     if args.tiling:
-        g, cs = (int(v) for v in args.tiling.split(","))
-        eng.set_tiling(g, cs)
+        ft, tb = (int(v) for v in args.tiling.split(","))
+        eng.set_tiling(ft, tb)
     eng.set_obs(x)
     eng.set_model(init.nmf, init.w0, init.lambda0)
     dfm._capi.check(lib.dfm_prime(eng.ctx))
@@ -50,24 +49,23 @@ def main():
     dfm._capi.check(lib.dfm_l2_flush(0))
     dfm._capi.check(lib.dfm_bench_step(eng.ctx))
     ms = lib.dfm_bench_last_ms(eng.ctx)
+    sp = (ctypes.c_double * 5)()
+    lib.dfm_bench_last_split(eng.ctx, sp)
     buf = np.zeros(n, dtype=np.uint64)
     dfm._capi.check(lib.dfm_get_trace(eng.ctx, buf.ctypes.data_as(ctypes.c_void_p), n))
-    tr = buf.reshape(-1, 16)[:, :13].astype(np.int64)
+    tr = buf.reshape(-1, 16)[:, :6].astype(np.int64)
     t0 = tr[:, 0].min()
     tr = tr - t0
     d = np.diff(tr, axis=1) / 1e3  # us
-    life = (tr[:, 12] - tr[:, 0]) / 1e3
-    out = {"workload": args.workload, "tiling": eng.tiling(), "step_ms": ms, "ctas": int(tr.shape[0]),
-           "span_us": float(tr[:, 12].max() / 1e3), "cta_life_us_mean": float(life.mean()),
+    life = (tr[:, 5] - tr[:, 0]) / 1e3
+    out = {"workload": args.workload, "tiling": eng.tiling(), "step_ms": ms,
+           "kernels_ms": dict(zip(["k_em_bin", "k_tupd", "k_pd", "k_vupd", "k_spec"], [round(v, 4) for v in sp])),
+           "ctas": int(tr.shape[0]),
+           "span_us": float(tr[:, 5].max() / 1e3), "cta_life_us_mean": float(life.mean()),
            "cta_life_us_max": float(life.max()),
            "phases_us_mean": {p: round(float(d[:, i].mean()), 3) for i, p in enumerate(PHASES)},
            "phases_us_max": {p: round(float(d[:, i].max()), 3) for i, p in enumerate(PHASES)}}
     starts = np.sort(tr[:, 0]) / 1e3
-    raw = buf.reshape(-1, 16).astype(np.int64) - t0
-    out["T_partials_work_us"] = float(((raw[:, 13] - raw[:, 10]) / 1e3).mean())
-    out["T_barrier_wait_us"] = float(((raw[:, 11] - raw[:, 13]) / 1e3).mean())
-    out["Q_work_after_accum_us"] = float(((raw[:, 14] - raw[:, 6]) / 1e3).mean())
-    out["Q_barrier_wait_us"] = float(((raw[:, 7] - raw[:, 14]) / 1e3).mean())
     out["start_percentiles_us"] = [round(float(np.percentile(starts, q)), 1) for q in (0, 10, 25, 50, 75, 90, 100)]
     print(json.dumps(out, indent=1))
 
