@@ -524,6 +524,7 @@ int dfm_fit(dfm_ctx* c, int iters, double* cost_trace, double* wall_seconds, dou
     launch_em(c, i == 0 ? 1 : 2, i < iters ? 1 : 0, i);
     if (i < iters) launch_rest(c, nullptr);
   }
+  DFM_CK(cudaEventRecord(c->iter_ev[iters + 1], c->stream));
   std::vector<double> part((size_t)(iters + 1) * c->F);
   c->cost_part.download(part.data(), part.size(), c->stream);
   int fb = 0;
