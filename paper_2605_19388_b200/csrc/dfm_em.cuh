@@ -61,8 +61,9 @@ __host__ __device__ inline EmPlan plan_em(const EmArgs& a, int FT) {
   p.red = o; o += al(r1 > r2 ? r1 : r2);
   p.wsum = o; o += al(64 * sizeof(double));
   p.ldet = o; o += al((size_t)a.nb * sizeof(double));
-  const size_t tA = (N + 2 * M) * FT * sizeof(double);  // h, z, 1/eta
-  const size_t tB = (3 * M) * FT * sizeof(double);      // x (complex), 1/eta
+  const size_t FTp = FT + 1;  // odd row stride: conflict-free item-parallel reads
+  const size_t tA = (N + 2 * M) * FTp * sizeof(double);  // h, z, 1/eta
+  const size_t tB = (3 * M) * FTp * sizeof(double);      // x (complex), 1/eta
   p.tile = o; o += al(tA > tB ? tA : tB);
   p.total = o;
   return p;
@@ -145,9 +146,10 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
   // ================================================================ pass A
   // finish iteration i-1: Lambda update with eta = max(h Lambda_old, floor)
   if (a.finish == 2) {
-    double* hs = tile;               // [N][FT]
-    double* zs = tile + N * FT;      // [M][FT]
-    double* is = zs + M * FT;        // [M][FT]
+    const int FTp = FT + 1;
+    double* hs = tile;               // [N][FTp]
+    double* zs = tile + N * FTp;     // [M][FTp]
+    double* is = zs + M * FTp;       // [M][FTp]
     const int NM = N * M, SL = sp.SL;
     const bool item_thread = tid < NM * SL;
     const int item = item_thread ? tid % NM : 0, sl = item_thread ? tid / NM : 0;
@@ -161,7 +163,7 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
         load_h(t, h);
 #pragma unroll
         for (int n = 0; n < kMaxN; ++n)
-          if (n < N) hs[n * FT + tid] = h[n];
+          if (n < N) hs[n * FTp + tid] = h[n];
         const cd* xt = xf + (size_t)t * M;
 #pragma unroll
         for (int b = 0; b < nb; ++b) {
@@ -177,16 +179,16 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
               for (int n = 0; n < kMaxN; ++n)
                 if (n < N) raw += h[n] * Lsm[n * M + m];
               const double ie = 1.0 / fmax(raw, floor_);
-              is[m * FT + tid] = ie;
-              zs[m * FT + tid] = P[mu] * ie * ie;
+              is[m * FTp + tid] = ie;
+              zs[m * FTp + tid] = P[mu] * ie * ie;
             }
         }
       }
       __syncthreads();
       if (item_thread) {
-        const double* hr = hs + in_ * FT;
-        const double* zr = zs + im * FT;
-        const double* er = is + im * FT;
+        const double* hr = hs + in_ * FTp;
+        const double* zr = zs + im * FTp;
+        const double* er = is + im * FTp;
 #pragma unroll 4
         for (int tt = sl; tt < tn; tt += SL) {
           num += hr[tt] * zr[tt];
@@ -263,8 +265,9 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
     }
   }
   {
-    cd* xsm = (cd*)tile;                              // [M][FT]
-    double* is = tile + 2 * (size_t)M * FT;           // [M][FT]
+    const int FTp = FT + 1;
+    cd* xsm = (cd*)tile;                              // [M][FTp]
+    double* is = tile + 2 * (size_t)M * FTp;          // [M][FTp]
     for (int tl = 0; tl < ntiles; ++tl) {
       const int t = tl * FT + tid;
       const int tn = min(FT, T - tl * FT);
@@ -288,9 +291,9 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
               cost += P[mu] * ie;
               lacc.mul(fmax(raw, 1e-300));
               if (a.start) {
-                is[m * FT + tid] = ie;
+                is[m * FTp + tid] = ie;
                 const double2 v = __ldg(reinterpret_cast<const double2*>(xt + m));
-                xsm[m * FT + tid] = cd{v.x, v.y};
+                xsm[m * FTp + tid] = cd{v.x, v.y};
               }
             }
         }
@@ -300,15 +303,15 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
         __syncthreads();
         if (qthread) {
           const int mb = MBof(qb_), off = OFF(qb_);
-          const cd* xr = xsm + (off + qr) * FT;
-          const cd* xc = xsm + (off + qc) * FT;
-          const double* ew = is + off * FT;
+          const cd* xr = xsm + (off + qr) * FTp;
+          const cd* xc = xsm + (off + qc) * FTp;
+          const double* ew = is + off * FTp;
 #pragma unroll 2
           for (int tt = qs; tt < tn; tt += SQ) {
             const cd pr = xr[tt] * conjg(xc[tt]);
 #pragma unroll
             for (int mu = 0; mu < MAXMB; ++mu)
-              if (mu < mb) qacc[mu] = qacc[mu] + pr * ew[mu * FT + tt];
+              if (mu < mb) qacc[mu] = qacc[mu] + pr * ew[mu * FTp + tt];
           }
         }
         __syncthreads();
