@@ -151,10 +151,7 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
     double* zs = tile + N * FTp;     // [M][FTp]
     double* is = zs + M * FTp;       // [M][FTp]
     const int NM = N * M, SL = sp.SL;
-    const bool item_thread = tid < NM * SL;
-    const int item = item_thread ? tid % NM : 0, sl = item_thread ? tid / NM : 0;
-    const int in_ = item / M, im = item - in_ * M;
-    double num = 0.0, den = 0.0;
+    for (int u = tid; u < NM * SL; u += FT) red[2 * u] = red[2 * u + 1] = 0.0;
     for (int tl = 0; tl < ntiles; ++tl) {
       const int t = tl * FT + tid;
       const int tn = min(FT, T - tl * FT);
@@ -185,23 +182,25 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
         }
       }
       __syncthreads();
-      if (item_thread) {
+      // (n, m) units: each sums its frames of the tile (stride SL), then adds
+      // the tile partial to its running sum (tile order: deterministic)
+      for (int u = tid; u < NM * SL; u += FT) {
+        const int item = u % NM, sl = u / NM;
+        const int in_ = item / M, im = item - in_ * M;
         const double* hr = hs + in_ * FTp;
         const double* zr = zs + im * FTp;
         const double* er = is + im * FTp;
+        double num = 0.0, den = 0.0;
 #pragma unroll 4
         for (int tt = sl; tt < tn; tt += SL) {
           num += hr[tt] * zr[tt];
           den += hr[tt] * er[tt];
         }
+        red[2 * u] += num;
+        red[2 * u + 1] += den;
       }
       __syncthreads();
     }
-    if (item_thread) {
-      red[2 * (sl * NM + item)] = num;
-      red[2 * (sl * NM + item) + 1] = den;
-    }
-    __syncthreads();
     for (int q = tid; q < NM; q += FT) {
       double nu = 0.0, de = 0.0;
       for (int s = 0; s < SL; ++s) {
@@ -222,24 +221,9 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
   double cost = 0.0;
   LogAcc lacc;
   const int nitems = sp.nitems, SQ = sp.SQ;
-  const bool qthread = a.start && tid < nitems * SQ;
-  const int qitem = qthread ? tid % nitems : 0, qs = qthread ? tid / nitems : 0;
-  int qb_ = 0, qr = 0, qc = 0;
-  if (qthread) {
-    int rem = qitem;
-    if constexpr (SB) {
-      constexpr int E = MB_ * (MB_ + 1) / 2;
-      qb_ = rem / E;
-      rem -= qb_ * E;
-    } else {
-      while (qb_ + 1 < nb && rem >= a.eofs[qb_ + 1]) ++qb_;
-      rem -= a.eofs[qb_];
-    }
-    decode_entry(rem, qr, qc);
-  }
-  cd qacc[MAXMB];
-#pragma unroll
-  for (int mu = 0; mu < MAXMB; ++mu) qacc[mu] = cd{0.0, 0.0};
+  cd* qpart = (cd*)red;  // [SQ][nitems][MAXMB] running sums over tiles
+  if (a.start)
+    for (int e = tid; e < SQ * nitems * MAXMB; e += FT) qpart[e] = cd{0.0, 0.0};
   // log-det (+ W^-1 for the fast IP path) of the pre-IP demixers: threads
   // with no Q item take one (bin, block) system each
   {
@@ -301,11 +285,26 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
       }
       if (a.start) {
         __syncthreads();
-        if (qthread) {
+        // (block, entry r<=c) units accumulate all mu of their block
+        for (int u = tid; u < nitems * SQ; u += FT) {
+          const int qitem = u % nitems, qs = u / nitems;
+          int rem = qitem, qb_ = 0, qr, qc;
+          if constexpr (SB) {
+            constexpr int E = MB_ * (MB_ + 1) / 2;
+            qb_ = rem / E;
+            rem -= qb_ * E;
+          } else {
+            while (qb_ + 1 < nb && rem >= a.eofs[qb_ + 1]) ++qb_;
+            rem -= a.eofs[qb_];
+          }
+          decode_entry(rem, qr, qc);
           const int mb = MBof(qb_), off = OFF(qb_);
           const cd* xr = xsm + (off + qr) * FTp;
           const cd* xc = xsm + (off + qc) * FTp;
           const double* ew = is + off * FTp;
+          cd qacc[MAXMB];
+#pragma unroll
+          for (int mu = 0; mu < MAXMB; ++mu) qacc[mu] = cd{0.0, 0.0};
 #pragma unroll 2
           for (int tt = qs; tt < tn; tt += SQ) {
             const cd pr = xr[tt] * conjg(xc[tt]);
@@ -313,6 +312,10 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
             for (int mu = 0; mu < MAXMB; ++mu)
               if (mu < mb) qacc[mu] = qacc[mu] + pr * ew[mu * FTp + tt];
           }
+          cd* dst = qpart + (size_t)u * MAXMB;
+#pragma unroll
+          for (int mu = 0; mu < MAXMB; ++mu)
+            if (mu < mb) dst[mu] = dst[mu] + qacc[mu];
         }
         __syncthreads();
       }
@@ -324,11 +327,6 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
   cost += lacc.value();
   cost = warp_sum(cost);
   if ((tid & 31) == 0) wsum[tid >> 5] = cost;
-  if (a.start && qthread) {
-    cd* qp = (cd*)red;
-#pragma unroll
-    for (int mu = 0; mu < MAXMB; ++mu) qp[(qs * nitems + qitem) * MAXMB + mu] = qacc[mu];
-  }
   __syncthreads();
   if (tid == 0) {
     double c = 0.0;
@@ -351,9 +349,8 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
     }
     const int mb = MBof(b);
     if (mu >= mb) continue;
-    const cd* qp = (const cd*)red;
     cd sum{0.0, 0.0};
-    for (int s = 0; s < SQ; ++s) sum = sum + qp[(s * nitems + it) * MAXMB + mu];
+    for (int s = 0; s < SQ; ++s) sum = sum + qpart[(s * nitems + it) * MAXMB + mu];
     const int E = mb * (mb + 1) / 2;
     Qsum[a.qofs[b] + mu * E + rem] = cd{sum.re / (double)T, sum.im / (double)T};
   }
