@@ -197,8 +197,9 @@ bool choose_tiling(dfm_ctx* c) {
   const EmArgs a = make_args(c);
   double best = 1e30;
   int bestFT = 0;
-  for (int FT : {256, 128, 64, 32}) {
-    if (c->req_FT && FT != c->req_FT) continue;
+  std::vector<int> cands = {256, 128, 64, 32};
+  if (c->req_FT) cands = {c->req_FT};
+  for (int FT : cands) {
     const size_t sm = em_smem(a, FT, c->kmaxmb);
     if (sm > 227 * 1024) continue;
     const int by_smem = (int)((228 * 1024) / (sm + 1024));
