@@ -1,16 +1,16 @@
 // The EM iteration as five kernels (restates src/engine.cpp:209-270).
 //
-//   k_spec    H = T V for every (bin, source, frame): a bin-tiled GEMM, so V
-//             is read once per tile of bins, not once per bin.
+//   k_spec_mma  H = T V for every (bin, source, frame) on the FP64 tensor
+//             cores (DMMA), so V is read once per 8-bin tile, not per bin.
 //   k_em_bin  one CTA per bin, frames streamed from L2 in tiles of FT:
 //             [finish it-1] Lambda update (engine.cpp:135-148) + cost
 //             (:150-165); [start it] Q_mu of all mu from one pass over X
 //             (:42-45), IP sweep (:40-51), decorrelation (:60-69) and the
 //             T-update weights A, B (:89-113) written for k_tupd.
-//   k_tupd    T update (:115-123): per (bin, source) dots over frames.
-//   k_pd      h' = T_new V, eta' (:231-232) and the V-update weights A', B'
-//             (:236) for a tile of bins x frames (V tile shared by the bins).
-//   k_vupd    V update (:125-133), bins summed in order (dfm_bin_kernel.cuh).
+//   k_tupd_mma  T update (:115-123): per (bin, source) dots over frames (DMMA).
+//   k_pdw     pass D: eta' from h' = T_new V (a second k_spec_mma) and the
+//             V-update weights A', B' (:231-237), elementwise over (bin, frame).
+//   k_vupd_mma  V update (:125-133), bins summed in a fixed order (DMMA).
 //
 // Every reduction has a fixed order; there are no floating-point atomics.
 #pragma once
@@ -451,171 +451,241 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
   em_stamp(a, 5);
 }
 
-// ------------------------------------------------------------------ k_spec
-// H[f][n][t] = sum_k T[f][n][k] V[n][k][t]  (engine.cpp:71-81).  CTA tile:
-// 16 bins x 64 frames of one source; V tile and T rows staged in shared
-// memory; each thread owns 4 frames of one bin.
-constexpr int kSpecFB = 16, kSpecTB = 64;
-__global__ void __launch_bounds__(256) k_spec(int F, int T, int N, int K, const double* __restrict__ Tf,
-                                             const double* __restrict__ V, double* __restrict__ H) {
-  extern __shared__ __align__(16) double sspec[];
-  double* Vs = sspec;                  // [K][TB]
-  double* Ts = sspec + K * kSpecTB;    // [FB][K]
-  const int n = blockIdx.z;
-  const int t0 = blockIdx.x * kSpecTB, f0 = blockIdx.y * kSpecFB;
-  const int tid = threadIdx.x;
-  for (int e = tid; e < K * kSpecTB; e += 256) {
-    const int k = e / kSpecTB, tt = e - k * kSpecTB;
-    Vs[e] = t0 + tt < T ? V[((size_t)n * K + k) * T + t0 + tt] : 0.0;
-  }
-  for (int e = tid; e < kSpecFB * K; e += 256) {
-    const int fi = e / K, k = e - fi * K;
-    Ts[e] = f0 + fi < F ? Tf[((size_t)(f0 + fi) * N + n) * K + k] : 0.0;
-  }
-  __syncthreads();
-  const int fi = tid / 16, tj = tid % 16;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  const double* tr = Ts + fi * K;
-  for (int k = 0; k < K; ++k) {
-    const double tv = tr[k];
-    const double* vr = Vs + k * kSpecTB + tj;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[j] += tv * vr[16 * j];
-  }
-  const int f = f0 + fi;
-  if (f < F)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int t = t0 + tj + 16 * j;
-      if (t < T) H[((size_t)f * N + n) * T + t] = acc[j];
-    }
+__global__ void k_vapply(size_t nkt, const double* __restrict__ numden, double* __restrict__ V,
+                         double floor_) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= nkt) return;
+  V[i] = fmax(V[i] * sqrt(numden[i] / fmax(numden[nkt + i], floor_)), floor_);
 }
 
-// ------------------------------------------------------------------ k_tupd
-// T[f][n][k] <- max(T * sqrt(sum_t A V / max(sum_t B V, floor)), floor)
-// (engine.cpp:115-123).  CTA: 8 bins of one source; thread (bin, k, parity)
-// sums over frames of one parity in 128-frame chunks staged in shared
-// memory; the two parities are added in a fixed order.
-constexpr int kTupdFB = 8, kTupdTC = 128, kTupdVS = kTupdTC + 1;  // padded V row stride
-__global__ void __launch_bounds__(256) k_tupd(int F, int T, int N, int K, double* __restrict__ Tf,
-                                             const double* __restrict__ V, const double* __restrict__ Aw,
-                                             const double* __restrict__ Bw, double floor_) {
-  extern __shared__ __align__(16) double stup[];
-  double* As = stup;                       // [FB][TC]
-  double* Bs = As + kTupdFB * kTupdTC;     // [FB][TC]
-  double* Vs = Bs + kTupdFB * kTupdTC;     // [K][VS]
-  const int n = blockIdx.y, f0 = blockIdx.x * kTupdFB;
-  const int tid = threadIdx.x;
-  const int fi = tid / 32, lane = tid & 31;
-  const int par = lane >> 4;
-  constexpr int KPT = 4;  // k values per thread: k = (lane & 15) + 16 j
-  double num[KPT], den[KPT];
+}  // namespace dfm
+
+// ===========================================================================
+// FP64 tensor-core (DMMA, mma.sync.m8n8k4.f64) kernels for the three
+// contractions of the iteration.  Fragment layout of m8n8k4 (lane = 4 g + q):
+//   A (8x4, row): a = A[g][q]     B (4x8, col): b = B[q][g]
+//   C (8x8):      c0 = C[g][2q],  c1 = C[g][2q + 1]
+// Operands beyond the problem edge are zero.  Every accumulation order is
+// fixed (k-steps in order, split partials summed in warp order).
+namespace dfm {
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// H[f][n][t] = sum_k T[f][n][k] V[n][k][t]  (engine.cpp:71-81).  Per source a
+// (F x K) x (K x T) product; a warp owns 8 bins x 32 frames, the CTA 8 warps
+// along the frames.
+constexpr int kSpecMaxKs = kMaxK / 4;
+__global__ void __launch_bounds__(256) k_spec_mma(int F, int T, int N, int K, const double* __restrict__ Tf,
+                                                 const double* __restrict__ V, double* __restrict__ H) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int n = blockIdx.z, f0 = blockIdx.y * 8;
+  const int t0 = (blockIdx.x * 8 + warp) * 32;
+  if (t0 >= T) return;
+  const int ks = (K + 3) / 4;
+  const int f = f0 + g;
+  double a[kSpecMaxKs];
 #pragma unroll
-  for (int j = 0; j < KPT; ++j) num[j] = den[j] = 0.0;
-  for (int tc = 0; tc < T; tc += kTupdTC) {
-    const int tn = min(kTupdTC, T - tc);
-    __syncthreads();
-    for (int e = tid; e < kTupdFB * kTupdTC; e += 256) {
-      const int fr = e / kTupdTC, tt = e - fr * kTupdTC;
-      const bool ok = f0 + fr < F && tt < tn;
-      const size_t o = ((size_t)n * F + f0 + fr) * T + tc + tt;
-      As[e] = ok ? Aw[o] : 0.0;
-      Bs[e] = ok ? Bw[o] : 0.0;
+  for (int s = 0; s < kSpecMaxKs; ++s) {
+    const int k = 4 * s + q;
+    a[s] = (s < ks && f < F && k < K) ? __ldg(Tf + ((size_t)f * N + n) * K + k) : 0.0;
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int tb = t0 + 8 * j;
+    double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+    for (int s = 0; s < kSpecMaxKs; ++s)
+      if (s < ks) {
+        const int k = 4 * s + q, t = tb + g;
+        const double b = (k < K && t < T) ? __ldg(V + ((size_t)n * K + k) * T + t) : 0.0;
+        dmma(c0, c1, a[s], b);
+      }
+    const int t = tb + 2 * q;
+    if (f < F) {
+      double* hp = H + ((size_t)f * N + n) * T;
+      if (t < T) hp[t] = c0;
+      if (t + 1 < T) hp[t + 1] = c1;
     }
-    for (int e = tid; e < K * kTupdTC; e += 256) {
-      const int k = e / kTupdTC, tt = e - k * kTupdTC;
-      Vs[k * kTupdVS + tt] = tt < tn ? V[((size_t)n * K + k) * T + tc + tt] : 0.0;
-    }
-    __syncthreads();
-    const double* ar = As + fi * kTupdTC;
-    const double* br = Bs + fi * kTupdTC;
+  }
+}
+
+// T update (engine.cpp:115-123): num[f][k] = sum_t A[n][f][t] V[n][k][t],
+// den likewise with B.  CTA = (8 bins, source); its 4 warps split the frames,
+// partials are added in warp order, then the multiplicative update.
+constexpr int kTupdWarps = 4;
+constexpr int kMaxKt = kMaxK / 8;
+__global__ void __launch_bounds__(32 * kTupdWarps) k_tupd_mma(int F, int T, int N, int K, double* __restrict__ Tf,
+                                                             const double* __restrict__ V,
+                                                             const double* __restrict__ Aw,
+                                                             const double* __restrict__ Bw, double floor_) {
+  __shared__ double part[kTupdWarps][2][kMaxKt][64];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int n = blockIdx.y, f0 = blockIdx.x * 8;
+  const int kt = (K + 7) / 8;
+  const int steps = (T + 3) / 4;
+  const int per = (steps + kTupdWarps - 1) / kTupdWarps;
+  const int s0 = warp * per, s1 = min(steps, s0 + per);
+  double num[kMaxKt][2], den[kMaxKt][2];
+#pragma unroll
+  for (int j = 0; j < kMaxKt; ++j) num[j][0] = num[j][1] = den[j][0] = den[j][1] = 0.0;
+  const int f = f0 + g;
+  const double* ar = Aw + ((size_t)n * F + (f < F ? f : 0)) * T;
+  const double* br = Bw + ((size_t)n * F + (f < F ? f : 0)) * T;
 #pragma unroll 2
-    for (int tt = par; tt < tn; tt += 2) {
-      const double av = ar[tt], bv = br[tt];
+  for (int s = s0; s < s1; ++s) {
+    const int t = 4 * s + q;
+    const bool ok = f < F && t < T;
+    const double av = ok ? __ldg(ar + t) : 0.0;
+    const double bv = ok ? __ldg(br + t) : 0.0;
 #pragma unroll
-      for (int j = 0; j < KPT; ++j) {
-        const int k = (lane & 15) + 16 * j;
-        if (k < K) {
-          const double v = Vs[k * kTupdVS + tt];
-          num[j] += av * v;
-          den[j] += bv * v;
+    for (int j = 0; j < kMaxKt; ++j)
+      if (j < kt) {
+        const int k = 8 * j + g;
+        const double vb = (k < K && t < T) ? __ldg(V + ((size_t)n * K + k) * T + t) : 0.0;
+        dmma(num[j][0], num[j][1], av, vb);
+        dmma(den[j][0], den[j][1], bv, vb);
+      }
+  }
+#pragma unroll
+  for (int j = 0; j < kMaxKt; ++j)
+    if (j < kt) {
+      part[warp][0][j][2 * lane] = num[j][0];
+      part[warp][0][j][2 * lane + 1] = num[j][1];
+      part[warp][1][j][2 * lane] = den[j][0];
+      part[warp][1][j][2 * lane + 1] = den[j][1];
+    }
+  __syncthreads();
+  if (warp != 0 || f >= F) return;
+#pragma unroll
+  for (int j = 0; j < kMaxKt; ++j)
+    if (j < kt)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int k = 8 * j + 2 * q + i;
+        if (k >= K) continue;
+        double nu = 0.0, de = 0.0;
+#pragma unroll
+        for (int w = 0; w < kTupdWarps; ++w) {
+          nu += part[w][0][j][2 * lane + i];
+          de += part[w][1][j][2 * lane + i];
+        }
+        double* tp = Tf + ((size_t)f * N + n) * K + k;
+        *tp = fmax(*tp * sqrt(nu / fmax(de, floor_)), floor_);
+      }
+}
+
+// V update (engine.cpp:125-133): num[k][t] = sum_f T[f][n][k] A'[n][f][t].
+// CTA = (8 frames, source); its 4 warps split the bins, partials are added
+// in warp order; apply in place or write {num, den} for the allreduce.
+constexpr int kVupdMWarps = 4;
+__global__ void __launch_bounds__(32 * kVupdMWarps) k_vupd_mma(int F, int T, int N, int K,
+                                                              const double* __restrict__ Tf,
+                                                              const double* __restrict__ Aw,
+                                                              const double* __restrict__ Bw,
+                                                              double* __restrict__ V, double* __restrict__ numden,
+                                                              double floor_) {
+  __shared__ double part[kVupdMWarps][2][kMaxKt][64];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int n = blockIdx.y, t0 = blockIdx.x * 8;
+  const int kt = (K + 7) / 8;
+  const int steps = (F + 3) / 4;
+  const int per = (steps + kVupdMWarps - 1) / kVupdMWarps;
+  const int s0 = warp * per, s1 = min(steps, s0 + per);
+  double num[kMaxKt][2], den[kMaxKt][2];
+#pragma unroll
+  for (int j = 0; j < kMaxKt; ++j) num[j][0] = num[j][1] = den[j][0] = den[j][1] = 0.0;
+  const int tb = t0 + g;
+#pragma unroll 2
+  for (int s = s0; s < s1; ++s) {
+    const int f = 4 * s + q;
+    const bool okb = f < F && tb < T;
+    const double av = okb ? __ldg(Aw + ((size_t)n * F + f) * T + tb) : 0.0;
+    const double bv = okb ? __ldg(Bw + ((size_t)n * F + f) * T + tb) : 0.0;
+#pragma unroll
+    for (int j = 0; j < kMaxKt; ++j)
+      if (j < kt) {
+        const int k = 8 * j + g;
+        const double ta = (f < F && k < K) ? __ldg(Tf + ((size_t)f * N + n) * K + k) : 0.0;
+        dmma(num[j][0], num[j][1], ta, av);
+        dmma(den[j][0], den[j][1], ta, bv);
+      }
+  }
+#pragma unroll
+  for (int j = 0; j < kMaxKt; ++j)
+    if (j < kt) {
+      part[warp][0][j][2 * lane] = num[j][0];
+      part[warp][0][j][2 * lane + 1] = num[j][1];
+      part[warp][1][j][2 * lane] = den[j][0];
+      part[warp][1][j][2 * lane + 1] = den[j][1];
+    }
+  __syncthreads();
+  if (warp != 0) return;
+#pragma unroll
+  for (int j = 0; j < kMaxKt; ++j)
+    if (j < kt)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int k = 8 * j + g, t = t0 + 2 * q + i;
+        if (k >= K || t >= T) continue;
+        double nu = 0.0, de = 0.0;
+#pragma unroll
+        for (int w = 0; w < kVupdMWarps; ++w) {
+          nu += part[w][0][j][2 * lane + i];
+          de += part[w][1][j][2 * lane + i];
+        }
+        const size_t o = ((size_t)n * K + k) * T + t;
+        if (numden) {
+          numden[o] = nu;
+          numden[(size_t)N * K * T + o] = de;
+        } else {
+          V[o] = fmax(V[o] * sqrt(nu / fmax(de, floor_)), floor_);
         }
       }
-    }
-  }
-  const int f = f0 + fi;
-#pragma unroll
-  for (int j = 0; j < KPT; ++j) {
-    const double on = __shfl_down_sync(0xffffffffu, num[j], 16);
-    const double od = __shfl_down_sync(0xffffffffu, den[j], 16);
-    const int k = (lane & 15) + 16 * j;
-    if (par == 0 && k < K && f < F) {
-      const double nu = num[j] + on, de = den[j] + od;
-      double* tp = Tf + ((size_t)f * N + n) * K + k;
-      *tp = fmax(*tp * sqrt(nu / fmax(de, floor_)), floor_);
-    }
-  }
 }
 
-// -------------------------------------------------------------------- k_pd
-// For a tile of bins x frames: h' = T_new V (V tile shared by the bins),
-// eta' = max(h' Lambda, floor), P = |W^H x|^2, and the V-update weights
-// A'_n = sum_m Lambda z, B'_n = sum_m Lambda / eta' (engine.cpp:231-237).
-constexpr int kPdFB = 4;
-template <int MB_, int NB_, int NS_, int NK_, int MAXMB>
-__global__ void __launch_bounds__(256) k_pd(const EmArgs a, const double* __restrict__ Tf,
-                                           const double* __restrict__ V, int TB) {
+// Pass D as an elementwise kernel over (bin, frame): h' from H (= T_new V by
+// k_spec_mma), eta' = max(h' Lambda, floor), P = |W^H x|^2, and the V-update
+// weights A'_n = sum_m Lambda z, B'_n = sum_m Lambda / eta' (engine.cpp:231-237).
+template <int MB_, int NB_, int NS_, int MAXMB>
+__global__ void __launch_bounds__(128) k_pdw(const EmArgs a) {
   constexpr bool SB = MB_ > 0 && NB_ > 0;
-  extern __shared__ __align__(16) unsigned char spd[];
+  __shared__ double Ls[kMaxN * 64];
+  __shared__ cd Ws[DFM_MAX_MB * DFM_MAX_MB * 4];
   const int M = SB ? MB_ * NB_ : a.M;
   const int nb = SB ? NB_ : a.nb;
   const int N = NS_ > 0 ? NS_ : a.N;
-  const int K = NK_ > 0 ? NK_ : a.K;
   const int T = a.T;
   const int wsz = SB ? MB_ * MB_ * NB_ : a.wsz;
   auto MBof = [&](int b) { return SB ? MB_ : a.mb[b]; };
   auto OFF = [&](int b) { return SB ? b * MB_ : a.off[b]; };
   auto WOFF = [&](int b) { return SB ? b * MB_ * MB_ : a.woff[b]; };
-  double* Vs = (double*)spd;                     // [N][K][TB]
-  double* Ts = Vs + (size_t)N * K * TB;          // [FB][N][K]
-  double* Ls = Ts + kPdFB * N * K;               // [FB][N][M]
-  cd* Ws = (cd*)(Ls + kPdFB * N * M + (((kPdFB * N * M) & 1) ? 1 : 0));  // [FB][wsz]
-  const int t0 = blockIdx.x * TB, f0 = blockIdx.y * kPdFB;
-  const int tid = threadIdx.x, nth = blockDim.x;
-  const int fn = min(kPdFB, a.F - f0);
-  for (int e = tid; e < N * K * TB; e += nth) {
-    const int row = e / TB, tt = e - row * TB;
-    Vs[e] = t0 + tt < T ? V[(size_t)row * T + t0 + tt] : 0.0;
-  }
-  for (int e = tid; e < fn * N * K; e += nth) Ts[e] = Tf[(size_t)f0 * N * K + e];
-  for (int e = tid; e < fn * N * M; e += nth) Ls[e] = a.lam[(size_t)f0 * N * M + e];
-  for (int e = tid; e < fn * wsz; e += nth) Ws[e] = a.W[(size_t)f0 * wsz + e];
+  const int f = blockIdx.y, t = blockIdx.x * blockDim.x + threadIdx.x;
+  const double* Lg = a.lam + (size_t)f * N * M;
+  const cd* Wg = a.W + (size_t)f * wsz;
+  const bool smemL = N * M <= kMaxN * 64, smemW = wsz <= DFM_MAX_MB * DFM_MAX_MB * 4;
+  if (smemL)
+    for (int e = threadIdx.x; e < N * M; e += blockDim.x) Ls[e] = Lg[e];
+  if (smemW)
+    for (int e = threadIdx.x; e < wsz; e += blockDim.x) Ws[e] = Wg[e];
   __syncthreads();
-  const int fi = tid / TB, tt = tid - fi * TB;
-  const int t = t0 + tt, f = f0 + fi;
-  if (fi >= fn || t >= T) return;
+  if (t >= T) return;
+  const double* Lf = smemL ? Ls : Lg;
+  const cd* Wf = smemW ? Ws : Wg;
   double h[kMaxN];
 #pragma unroll
-  for (int n = 0; n < kMaxN; ++n) {
-    double s = 0.0;
-    if (n < N) {
-      const double* tr = Ts + (fi * N + n) * K;
-      const double* vr = Vs + (size_t)n * K * TB + tt;
-      if constexpr (NK_ > 0) {
-#pragma unroll
-        for (int k = 0; k < NK_; ++k) s += tr[k] * vr[k * TB];
-      } else {
-        for (int k = 0; k < K; ++k) s += tr[k] * vr[k * TB];
-      }
-    }
-    h[n] = s;
-  }
-  const double* Lf = Ls + fi * N * M;
-  const cd* Wf = Ws + fi * wsz;
+  for (int n = 0; n < kMaxN; ++n) h[n] = n < N ? __ldg(a.H + ((size_t)f * N + n) * T + t) : 0.0;
   const cd* xt = a.x + ((size_t)f * T + t) * M;
   double A[kMaxN], B[kMaxN];
 #pragma unroll
   for (int n = 0; n < kMaxN; ++n) A[n] = B[n] = 0.0;
+#pragma unroll
   for (int b = 0; b < nb; ++b) {
     const int mb = MBof(b), off = OFF(b);
     const cd* wb = Wf + WOFF(b);
@@ -623,23 +693,23 @@ __global__ void __launch_bounds__(256) k_pd(const EmArgs a, const double* __rest
     if constexpr (SB) {
       cd xv[MB_];
 #pragma unroll
-      for (int q = 0; q < MB_; ++q) {
-        const double2 v = __ldg(reinterpret_cast<const double2*>(xt + off + q));
-        xv[q] = cd{v.x, v.y};
+      for (int qq = 0; qq < MB_; ++qq) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(xt + off + qq));
+        xv[qq] = cd{v.x, v.y};
       }
 #pragma unroll
       for (int mu = 0; mu < MB_; ++mu) {
         cd s{0.0, 0.0};
 #pragma unroll
-        for (int q = 0; q < MB_; ++q) s = s + cmulc(wb[mu * MB_ + q], xv[q]);
+        for (int qq = 0; qq < MB_; ++qq) s = s + cmulc(wb[mu * MB_ + qq], xv[qq]);
         P[mu] = norm2(s);
       }
     } else {
       for (int mu = 0; mu < mb; ++mu) {
         cd s{0.0, 0.0};
-        for (int q = 0; q < mb; ++q) {
-          const double2 v = __ldg(reinterpret_cast<const double2*>(xt + off + q));
-          s = s + cmulc(wb[mu * mb + q], cd{v.x, v.y});
+        for (int qq = 0; qq < mb; ++qq) {
+          const double2 v = __ldg(reinterpret_cast<const double2*>(xt + off + qq));
+          s = s + cmulc(wb[mu * mb + qq], cd{v.x, v.y});
         }
         P[mu] = norm2(s);
       }
@@ -670,75 +740,6 @@ __global__ void __launch_bounds__(256) k_pd(const EmArgs a, const double* __rest
       a.Aw[o] = A[n];
       a.Bw[o] = B[n];
     }
-}
-
-// V update (engine.cpp:125-133), the only cross-bin reduction.  Grid:
-// (frame tiles of 32, sources, k-groups of KPT); the 8 warps of a CTA each
-// sum a contiguous range of bins, then the partials are added in warp order
-// (deterministic, no atomics).  numden == nullptr: apply in place; else write
-// {num, den} for the cross-GPU allreduce.
-constexpr int kVupdWarps = 8;
-constexpr int kVupdKPT = 8;
-__global__ void __launch_bounds__(32 * kVupdWarps) k_vupd(int F, int T, int N, int K, const double* __restrict__ Tf,
-                                                         const double* __restrict__ Ap,
-                                                         const double* __restrict__ Bp, double* __restrict__ V,
-                                                         double* __restrict__ numden, double floor_) {
-  __shared__ double part[kVupdWarps][2][kVupdKPT][32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int t = blockIdx.x * 32 + lane;
-  const int n = blockIdx.y;
-  const int k0 = blockIdx.z * kVupdKPT;
-  const int kn = min(kVupdKPT, K - k0);
-  const int chunk = (F + kVupdWarps - 1) / kVupdWarps;
-  const int fa = warp * chunk, fe = min(F, fa + chunk);
-  double num[kVupdKPT], den[kVupdKPT];
-#pragma unroll
-  for (int j = 0; j < kVupdKPT; ++j) num[j] = den[j] = 0.0;
-  if (t < T) {
-    const double* ar = Ap + (size_t)n * F * T + t;
-    const double* br = Bp + (size_t)n * F * T + t;
-#pragma unroll 2
-    for (int f = fa; f < fe; ++f) {
-      const double av = __ldg(ar + (size_t)f * T), bv = __ldg(br + (size_t)f * T);
-      const double* tr = Tf + ((size_t)f * N + n) * K + k0;
-#pragma unroll
-      for (int j = 0; j < kVupdKPT; ++j)
-        if (j < kn) {
-          const double tv = __ldg(tr + j);
-          num[j] += tv * av;
-          den[j] += tv * bv;
-        }
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < kVupdKPT; ++j) {
-    part[warp][0][j][lane] = num[j];
-    part[warp][1][j][lane] = den[j];
-  }
-  __syncthreads();
-  if (t >= T) return;
-  for (int j = warp; j < kn; j += kVupdWarps) {
-    double sn = 0.0, sd = 0.0;
-#pragma unroll
-    for (int w = 0; w < kVupdWarps; ++w) {
-      sn += part[w][0][j][lane];
-      sd += part[w][1][j][lane];
-    }
-    const size_t o = ((size_t)n * K + k0 + j) * T + t;
-    if (numden) {
-      numden[o] = sn;
-      numden[(size_t)N * K * T + o] = sd;
-    } else {
-      V[o] = fmax(V[o] * sqrt(sn / fmax(sd, floor_)), floor_);
-    }
-  }
-}
-
-__global__ void k_vapply(size_t nkt, const double* __restrict__ numden, double* __restrict__ V,
-                         double floor_) {
-  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (i >= nkt) return;
-  V[i] = fmax(V[i] * sqrt(numden[i] / fmax(numden[nkt + i], floor_)), floor_);
 }
 
 }  // namespace dfm

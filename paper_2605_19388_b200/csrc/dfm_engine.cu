@@ -7,13 +7,13 @@
 //             IP sweep, decorrelation, T-update weights; :212-227).  One CTA
 //             per bin, frames streamed from L2 in tiles, every bin resident
 //             in one wave.
-//   k_tupd    T update (:115-123)
-//   k_pd      h' = T V, eta', V-update weights (:231-237), V tile shared by
-//             a tile of bins
-//   k_vupd    V update (:125-133) - the only cross-bin reduction; with a
+//   k_tupd_mma  T update (:115-123) on the FP64 tensor cores (DMMA)
+//   k_spec_mma + k_pdw  h' = T_new V (DMMA), then eta' and the V-update
+//             weights (:231-237) elementwise over (bin, frame)
+//   k_vupd_mma  V update (:125-133) - the only cross-bin reduction; with a
 //             communicator it writes {num, den}, one ncclAllReduce follows
 //             and k_vapply updates V identically on every rank
-//   k_spec    H = T V for the next iteration (bin-tiled GEMM)
+//   k_spec_mma  H = T V for the next iteration
 // A launch of k_em_bin finishes the previous iteration and starts the next,
 // which is legal because both halves are bin-local.
 //
@@ -102,9 +102,9 @@ struct dfm_ctx {
   int maxmb = 4;
   int kmaxmb = 4;  // MAXMB of the selected instantiations
   void (*kem)(EmArgs) = nullptr;
-  void (*kpd)(EmArgs, const double*, const double*, int) = nullptr;
+  void (*kpdw)(EmArgs) = nullptr;
   bool force_generic = false;
-  int FT = 128, TB = 64, smem_em = 0, smem_pd = 0, smem_tupd = 0, smem_spec = 0;
+  int FT = 128, TB = 128, smem_em = 0;
   int req_FT = 0, req_TB = 0;
   DBuf<unsigned long long> trace;
   bool tracing = false;
@@ -168,29 +168,28 @@ void select_kernels(dfm_ctx* c) {
   for (int b = 1; b < c->L.nb; ++b) uniform = uniform && c->L.mb[b] == c->L.mb[0];
   const int mb = c->L.mb[0], nb = c->L.nb, N = c->N, K = c->K;
   c->kem = nullptr;
-  c->kpd = nullptr;
   if (uniform && !c->force_generic) {
     if (mb == 4 && nb == 3 && N == 5 && K == 16) {
-      c->kem = k_em_bin<4, 3, 5, 4>; c->kpd = k_pd<4, 3, 5, 16, 4>; c->kmaxmb = 4;
+      c->kem = k_em_bin<4, 3, 5, 4>; c->kpdw = k_pdw<4, 3, 5, 4>; c->kmaxmb = 4;
     } else if (mb == 2 && nb == 2 && N == 3 && K == 4) {
-      c->kem = k_em_bin<2, 2, 3, 2>; c->kpd = k_pd<2, 2, 3, 4, 2>; c->kmaxmb = 2;
+      c->kem = k_em_bin<2, 2, 3, 2>; c->kpdw = k_pdw<2, 2, 3, 2>; c->kmaxmb = 2;
     } else if (mb == 4 && nb == 8 && N == 8 && K == 32) {
-      c->kem = k_em_bin<4, 8, 8, 4>; c->kpd = k_pd<4, 8, 8, 32, 4>; c->kmaxmb = 4;
+      c->kem = k_em_bin<4, 8, 8, 4>; c->kpdw = k_pdw<4, 8, 8, 4>; c->kmaxmb = 4;
     } else if (mb == 12 && nb == 1 && N == 5 && K == 16) {
-      c->kem = k_em_bin<12, 1, 5, 12>; c->kpd = k_pd<12, 1, 5, 16, 12>; c->kmaxmb = 12;
+      c->kem = k_em_bin<12, 1, 5, 12>; c->kpdw = k_pdw<12, 1, 5, 12>; c->kmaxmb = 12;
     }
   }
   if (!c->kem) {
     if (c->maxmb <= 4) {
-      c->kem = k_em_bin<0, 0, 0, 4>; c->kpd = k_pd<0, 0, 0, 0, 4>; c->kmaxmb = 4;
+      c->kem = k_em_bin<0, 0, 0, 4>; c->kpdw = k_pdw<0, 0, 0, 4>; c->kmaxmb = 4;
     } else {
-      c->kem = k_em_bin<0, 0, 0, DFM_MAX_MB>; c->kpd = k_pd<0, 0, 0, 0, DFM_MAX_MB>; c->kmaxmb = DFM_MAX_MB;
+      c->kem = k_em_bin<0, 0, 0, DFM_MAX_MB>; c->kpdw = k_pdw<0, 0, 0, DFM_MAX_MB>; c->kmaxmb = DFM_MAX_MB;
     }
   }
 }
 
 // Tiling: the frame tile FT of k_em_bin minimises (waves of resident CTAs)
-// x (tiles per CTA); the frame tile TB of k_pd keeps its V tile <= 64 KB.
+// x (tiles per CTA).
 bool choose_tiling(dfm_ctx* c) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
@@ -218,34 +217,23 @@ bool choose_tiling(dfm_ctx* c) {
   }
   c->FT = bestFT;
   c->smem_em = (int)em_smem(a, c->FT, c->kmaxmb);
-  int TB = c->req_TB ? c->req_TB : 64;
-  while (TB > 8 && (size_t)c->N * c->K * TB * 8 > 64 * 1024) TB /= 2;
-  c->TB = TB;
-  c->smem_pd = (int)(((size_t)c->N * c->K * TB + kPdFB * c->N * c->K + kPdFB * c->N * c->M + 1) * 8 +
-                     (size_t)kPdFB * c->L.wsz * 16 + 16);
-  c->smem_tupd = (int)((2 * kTupdFB * kTupdTC + (size_t)c->K * kTupdVS) * 8);
-  c->smem_spec = (int)(((size_t)c->K * kSpecTB + kSpecFB * c->K) * 8);
-  if (c->smem_pd > 227 * 1024) {
-    set_error("k_pd tile does not fit in shared memory");
-    return false;
-  }
+  c->TB = c->req_TB ? c->req_TB : 128;  // frames per CTA of the elementwise pass D
   return true;
 }
 
 void set_kernel_attrs(dfm_ctx* c) {
   DFM_CK(cudaFuncSetAttribute(c->kem, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_em));
-  DFM_CK(cudaFuncSetAttribute(c->kpd, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_pd));
-  DFM_CK(cudaFuncSetAttribute(k_tupd, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_tupd));
-  DFM_CK(cudaFuncSetAttribute(k_spec, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_spec));
+
 }
 
 void ensure_cost(dfm_ctx* c, int slots) {
   if (c->cost_part.n < (size_t)slots * c->F) c->cost_part.alloc((size_t)slots * c->F);
 }
 
+// H = T V on the FP64 tensor cores (DMMA)
 void launch_spec(dfm_ctx* c) {
-  const dim3 grid((c->T + kSpecTB - 1) / kSpecTB, (c->F + kSpecFB - 1) / kSpecFB, c->N);
-  k_spec<<<grid, 256, c->smem_spec, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->V.p, c->H.p);
+  const dim3 grid((c->T + 255) / 256, (c->F + 7) / 8, c->N);
+  k_spec_mma<<<grid, 256, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->V.p, c->H.p);
   DFM_CK_LAUNCH();
   c->launches++;
 }
@@ -262,26 +250,28 @@ void launch_em(dfm_ctx* c, int finish, int start, int slot) {
 }
 
 void launch_tupd(dfm_ctx* c) {
-  const dim3 grid((c->F + kTupdFB - 1) / kTupdFB, c->N);
-  k_tupd<<<grid, 256, c->smem_tupd, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->V.p, c->Aw.p, c->Bw.p,
-                                                  c->floor_);
+  const dim3 grid((c->F + 7) / 8, c->N);
+  k_tupd_mma<<<grid, 32 * kTupdWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->V.p, c->Aw.p, c->Bw.p,
+                                                       c->floor_);
   DFM_CK_LAUNCH();
   c->launches++;
 }
 
+// pass D: h' = T_new V into H (DMMA), then the elementwise V-update weights
 void launch_pd(dfm_ctx* c) {
+  launch_spec(c);
   EmArgs a = make_args(c);
-  const dim3 grid((c->T + c->TB - 1) / c->TB, (c->F + kPdFB - 1) / kPdFB);
-  c->kpd<<<grid, kPdFB * c->TB, c->smem_pd, c->stream>>>(a, c->Tf.p, c->V.p, c->TB);
+  const dim3 grid((c->T + c->TB - 1) / c->TB, c->F);
+  c->kpdw<<<grid, c->TB, 0, c->stream>>>(a);
   DFM_CK_LAUNCH();
   c->launches++;
 }
 
 void launch_vupd(dfm_ctx* c) {
-  const dim3 grid((c->T + 31) / 32, c->N, (c->K + kVupdKPT - 1) / kVupdKPT);
+  const dim3 grid((c->T + 7) / 8, c->N);
   const bool sharded = c->comm != nullptr && c->nranks > 1;
-  k_vupd<<<grid, 32 * kVupdWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->Aw.p, c->Bw.p, c->V.p,
-                                                   sharded ? c->numden.p : nullptr, c->floor_);
+  k_vupd_mma<<<grid, 32 * kVupdMWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->Aw.p, c->Bw.p,
+                                                         c->V.p, sharded ? c->numden.p : nullptr, c->floor_);
   DFM_CK_LAUNCH();
   c->launches++;
   if (sharded) {
@@ -615,7 +605,8 @@ int dfm_bench_last_split(dfm_ctx* c, double* ms5) {
 long long dfm_launch_count(const dfm_ctx* c) { return c ? c->launches : -1; }
 
 int dfm_set_tiling(dfm_ctx* c, int frame_tile, int pd_frames) {
-  if (!c || frame_tile < 0 || frame_tile > 256 || (frame_tile & 31) || pd_frames < 0 || pd_frames > 64)
+  if (!c || frame_tile < 0 || frame_tile > 256 || (frame_tile & 31) || pd_frames < 0 || pd_frames > 128 ||
+      (pd_frames & 31))
     return DFM_ERR_ARG;
   DFM_API_BEGIN
   DFM_CK(cudaSetDevice(c->device));
