@@ -479,102 +479,116 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 // (F x K) x (K x T) product; a warp owns 8 bins x 32 frames, the CTA 8 warps
 // along the frames.
 constexpr int kSpecMaxKs = kMaxK / 4;
-__global__ void __launch_bounds__(256) k_spec_mma(int F, int T, int N, int K, const double* __restrict__ Tf,
-                                                 const double* __restrict__ V, double* __restrict__ H) {
+constexpr int kSpecWarps = 4;
+__global__ void __launch_bounds__(32 * kSpecWarps) k_spec_mma(int F, int T, int N, int K, const double* __restrict__ Tf,
+                                                             const double* __restrict__ V, double* __restrict__ H) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
   const int n = blockIdx.z, f0 = blockIdx.y * 8;
-  const int t0 = (blockIdx.x * 8 + warp) * 32;
-  if (t0 >= T) return;
+  const int tb = (blockIdx.x * kSpecWarps + warp) * 8;
+  if (tb >= T) return;
   const int ks = (K + 3) / 4;
-  const int f = f0 + g;
-  double a[kSpecMaxKs];
+  const int f = f0 + g, tl = tb + g;
+  double a[kSpecMaxKs], b[kSpecMaxKs];
 #pragma unroll
   for (int s = 0; s < kSpecMaxKs; ++s) {
     const int k = 4 * s + q;
-    a[s] = (s < ks && f < F && k < K) ? __ldg(Tf + ((size_t)f * N + n) * K + k) : 0.0;
+    const bool ok = s < ks && k < K;
+    a[s] = (ok && f < F) ? __ldg(Tf + ((size_t)f * N + n) * K + k) : 0.0;
+    b[s] = (ok && tl < T) ? __ldg(V + ((size_t)n * K + k) * T + tl) : 0.0;
   }
+  double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int tb = t0 + 8 * j;
-    double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-    for (int s = 0; s < kSpecMaxKs; ++s)
-      if (s < ks) {
-        const int k = 4 * s + q, t = tb + g;
-        const double b = (k < K && t < T) ? __ldg(V + ((size_t)n * K + k) * T + t) : 0.0;
-        dmma(c0, c1, a[s], b);
-      }
-    const int t = tb + 2 * q;
-    if (f < F) {
-      double* hp = H + ((size_t)f * N + n) * T;
-      if (t < T) hp[t] = c0;
-      if (t + 1 < T) hp[t + 1] = c1;
-    }
+  for (int s = 0; s < kSpecMaxKs; ++s)
+    if (s < ks) dmma(c0, c1, a[s], b[s]);
+  const int t = tb + 2 * q;
+  if (f < F) {
+    double* hp = H + ((size_t)f * N + n) * T;
+    if (t < T) hp[t] = c0;
+    if (t + 1 < T) hp[t + 1] = c1;
   }
 }
 
 // T update (engine.cpp:115-123): num[f][k] = sum_t A[n][f][t] V[n][k][t],
 // den likewise with B.  CTA = (8 bins, source); its 4 warps split the frames,
 // partials are added in warp order, then the multiplicative update.
-constexpr int kTupdWarps = 4;
+constexpr int kTupdWarps = 8;
 constexpr int kMaxKt = kMaxK / 8;
+template <int KT>
 __global__ void __launch_bounds__(32 * kTupdWarps) k_tupd_mma(int F, int T, int N, int K, double* __restrict__ Tf,
                                                              const double* __restrict__ V,
                                                              const double* __restrict__ Aw,
                                                              const double* __restrict__ Bw, double floor_) {
-  __shared__ double part[kTupdWarps][2][kMaxKt][64];
+  __shared__ double part[kTupdWarps / 2][2][KT][64];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
   const int n = blockIdx.y, f0 = blockIdx.x * 8;
-  const int kt = (K + 7) / 8;
+  constexpr int kt = KT;
   const int steps = (T + 3) / 4;
   const int per = (steps + kTupdWarps - 1) / kTupdWarps;
   const int s0 = warp * per, s1 = min(steps, s0 + per);
-  double num[kMaxKt][2], den[kMaxKt][2];
+  double num[KT][2], den[KT][2];
 #pragma unroll
-  for (int j = 0; j < kMaxKt; ++j) num[j][0] = num[j][1] = den[j][0] = den[j][1] = 0.0;
+  for (int j = 0; j < KT; ++j) num[j][0] = num[j][1] = den[j][0] = den[j][1] = 0.0;
   const int f = f0 + g;
   const double* ar = Aw + ((size_t)n * F + (f < F ? f : 0)) * T;
   const double* br = Bw + ((size_t)n * F + (f < F ? f : 0)) * T;
-#pragma unroll 2
-  for (int s = s0; s < s1; ++s) {
-    const int t = 4 * s + q;
-    const bool ok = f < F && t < T;
-    const double av = ok ? __ldg(ar + t) : 0.0;
-    const double bv = ok ? __ldg(br + t) : 0.0;
+  constexpr int U = 4;  // k-steps whose operands are loaded before their DMMAs
+  for (int sb = s0; sb < s1; sb += U) {
+    double av[U], bv[U], vb[U][KT];
 #pragma unroll
-    for (int j = 0; j < kMaxKt; ++j)
-      if (j < kt) {
+    for (int u = 0; u < U; ++u) {
+      const int t = 4 * (sb + u) + q;
+      const bool ok = sb + u < s1 && t < T;
+      av[u] = (ok && f < F) ? __ldg(ar + t) : 0.0;
+      bv[u] = (ok && f < F) ? __ldg(br + t) : 0.0;
+#pragma unroll
+      for (int j = 0; j < KT; ++j) {
         const int k = 8 * j + g;
-        const double vb = (k < K && t < T) ? __ldg(V + ((size_t)n * K + k) * T + t) : 0.0;
-        dmma(num[j][0], num[j][1], av, vb);
-        dmma(den[j][0], den[j][1], bv, vb);
+        vb[u][j] = (j < kt && ok && k < K) ? __ldg(V + ((size_t)n * K + k) * T + t) : 0.0;
       }
-  }
-#pragma unroll
-  for (int j = 0; j < kMaxKt; ++j)
-    if (j < kt) {
-      part[warp][0][j][2 * lane] = num[j][0];
-      part[warp][0][j][2 * lane + 1] = num[j][1];
-      part[warp][1][j][2 * lane] = den[j][0];
-      part[warp][1][j][2 * lane + 1] = den[j][1];
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int j = 0; j < KT; ++j)
+        if (j < kt) {
+          dmma(num[j][0], num[j][1], av[u], vb[u][j]);
+          dmma(den[j][0], den[j][1], bv[u], vb[u][j]);
+        }
+  }
+  // fixed-order tree over the warps: w += w + h for h = W/2, W/4, ..., 1
+#pragma unroll
+  for (int h = kTupdWarps / 2; h >= 1; h >>= 1) {
+    if (warp >= h && warp < 2 * h)
+#pragma unroll
+      for (int j = 0; j < KT; ++j) {
+        part[warp - h][0][j][2 * lane] = num[j][0];
+        part[warp - h][0][j][2 * lane + 1] = num[j][1];
+        part[warp - h][1][j][2 * lane] = den[j][0];
+        part[warp - h][1][j][2 * lane + 1] = den[j][1];
+      }
+    __syncthreads();
+    if (warp < h)
+#pragma unroll
+      for (int j = 0; j < KT; ++j) {
+        num[j][0] += part[warp][0][j][2 * lane];
+        num[j][1] += part[warp][0][j][2 * lane + 1];
+        den[j][0] += part[warp][1][j][2 * lane];
+        den[j][1] += part[warp][1][j][2 * lane + 1];
+      }
+    __syncthreads();
+  }
   __syncthreads();
   if (warp != 0 || f >= F) return;
 #pragma unroll
-  for (int j = 0; j < kMaxKt; ++j)
+  for (int j = 0; j < KT; ++j)
     if (j < kt)
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         const int k = 8 * j + 2 * q + i;
         if (k >= K) continue;
-        double nu = 0.0, de = 0.0;
-#pragma unroll
-        for (int w = 0; w < kTupdWarps; ++w) {
-          nu += part[w][0][j][2 * lane + i];
-          de += part[w][1][j][2 * lane + i];
-        }
+        const double nu = num[j][i], de = den[j][i];
         double* tp = Tf + ((size_t)f * N + n) * K + k;
         *tp = fmax(*tp * sqrt(nu / fmax(de, floor_)), floor_);
       }
@@ -583,63 +597,82 @@ __global__ void __launch_bounds__(32 * kTupdWarps) k_tupd_mma(int F, int T, int 
 // V update (engine.cpp:125-133): num[k][t] = sum_f T[f][n][k] A'[n][f][t].
 // CTA = (8 frames, source); its 4 warps split the bins, partials are added
 // in warp order; apply in place or write {num, den} for the allreduce.
-constexpr int kVupdMWarps = 4;
+constexpr int kVupdMWarps = 8;
+template <int KT>
 __global__ void __launch_bounds__(32 * kVupdMWarps) k_vupd_mma(int F, int T, int N, int K,
                                                               const double* __restrict__ Tf,
                                                               const double* __restrict__ Aw,
                                                               const double* __restrict__ Bw,
                                                               double* __restrict__ V, double* __restrict__ numden,
                                                               double floor_) {
-  __shared__ double part[kVupdMWarps][2][kMaxKt][64];
+  __shared__ double part[kVupdMWarps / 2][2][KT][64];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
   const int n = blockIdx.y, t0 = blockIdx.x * 8;
-  const int kt = (K + 7) / 8;
+  constexpr int kt = KT;
   const int steps = (F + 3) / 4;
   const int per = (steps + kVupdMWarps - 1) / kVupdMWarps;
   const int s0 = warp * per, s1 = min(steps, s0 + per);
-  double num[kMaxKt][2], den[kMaxKt][2];
+  double num[KT][2], den[KT][2];
 #pragma unroll
-  for (int j = 0; j < kMaxKt; ++j) num[j][0] = num[j][1] = den[j][0] = den[j][1] = 0.0;
+  for (int j = 0; j < KT; ++j) num[j][0] = num[j][1] = den[j][0] = den[j][1] = 0.0;
   const int tb = t0 + g;
-#pragma unroll 2
-  for (int s = s0; s < s1; ++s) {
-    const int f = 4 * s + q;
-    const bool okb = f < F && tb < T;
-    const double av = okb ? __ldg(Aw + ((size_t)n * F + f) * T + tb) : 0.0;
-    const double bv = okb ? __ldg(Bw + ((size_t)n * F + f) * T + tb) : 0.0;
+  constexpr int U = 4;
+  for (int sb = s0; sb < s1; sb += U) {
+    double av[U], bv[U], ta[U][KT];
 #pragma unroll
-    for (int j = 0; j < kMaxKt; ++j)
-      if (j < kt) {
+    for (int u = 0; u < U; ++u) {
+      const int f = 4 * (sb + u) + q;
+      const bool okf = sb + u < s1 && f < F;
+      av[u] = (okf && tb < T) ? __ldg(Aw + ((size_t)n * F + f) * T + tb) : 0.0;
+      bv[u] = (okf && tb < T) ? __ldg(Bw + ((size_t)n * F + f) * T + tb) : 0.0;
+#pragma unroll
+      for (int j = 0; j < KT; ++j) {
         const int k = 8 * j + g;
-        const double ta = (f < F && k < K) ? __ldg(Tf + ((size_t)f * N + n) * K + k) : 0.0;
-        dmma(num[j][0], num[j][1], ta, av);
-        dmma(den[j][0], den[j][1], ta, bv);
+        ta[u][j] = (j < kt && okf && k < K) ? __ldg(Tf + ((size_t)f * N + n) * K + k) : 0.0;
       }
-  }
-#pragma unroll
-  for (int j = 0; j < kMaxKt; ++j)
-    if (j < kt) {
-      part[warp][0][j][2 * lane] = num[j][0];
-      part[warp][0][j][2 * lane + 1] = num[j][1];
-      part[warp][1][j][2 * lane] = den[j][0];
-      part[warp][1][j][2 * lane + 1] = den[j][1];
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int j = 0; j < KT; ++j)
+        if (j < kt) {
+          dmma(num[j][0], num[j][1], ta[u][j], av[u]);
+          dmma(den[j][0], den[j][1], ta[u][j], bv[u]);
+        }
+  }
+  // fixed-order tree over the warps: w += w + h for h = W/2, W/4, ..., 1
+#pragma unroll
+  for (int h = kVupdMWarps / 2; h >= 1; h >>= 1) {
+    if (warp >= h && warp < 2 * h)
+#pragma unroll
+      for (int j = 0; j < KT; ++j) {
+        part[warp - h][0][j][2 * lane] = num[j][0];
+        part[warp - h][0][j][2 * lane + 1] = num[j][1];
+        part[warp - h][1][j][2 * lane] = den[j][0];
+        part[warp - h][1][j][2 * lane + 1] = den[j][1];
+      }
+    __syncthreads();
+    if (warp < h)
+#pragma unroll
+      for (int j = 0; j < KT; ++j) {
+        num[j][0] += part[warp][0][j][2 * lane];
+        num[j][1] += part[warp][0][j][2 * lane + 1];
+        den[j][0] += part[warp][1][j][2 * lane];
+        den[j][1] += part[warp][1][j][2 * lane + 1];
+      }
+    __syncthreads();
+  }
   __syncthreads();
   if (warp != 0) return;
 #pragma unroll
-  for (int j = 0; j < kMaxKt; ++j)
+  for (int j = 0; j < KT; ++j)
     if (j < kt)
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         const int k = 8 * j + g, t = t0 + 2 * q + i;
         if (k >= K || t >= T) continue;
-        double nu = 0.0, de = 0.0;
-#pragma unroll
-        for (int w = 0; w < kVupdMWarps; ++w) {
-          nu += part[w][0][j][2 * lane + i];
-          de += part[w][1][j][2 * lane + i];
-        }
+        const double nu = num[j][i], de = den[j][i];
         const size_t o = ((size_t)n * K + k) * T + t;
         if (numden) {
           numden[o] = nu;

@@ -232,8 +232,8 @@ void ensure_cost(dfm_ctx* c, int slots) {
 
 // H = T V on the FP64 tensor cores (DMMA)
 void launch_spec(dfm_ctx* c) {
-  const dim3 grid((c->T + 255) / 256, (c->F + 7) / 8, c->N);
-  k_spec_mma<<<grid, 256, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->V.p, c->H.p);
+  const dim3 grid((c->T + 8 * kSpecWarps - 1) / (8 * kSpecWarps), (c->F + 7) / 8, c->N);
+  k_spec_mma<<<grid, 32 * kSpecWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->V.p, c->H.p);
   DFM_CK_LAUNCH();
   c->launches++;
 }
@@ -251,8 +251,14 @@ void launch_em(dfm_ctx* c, int finish, int start, int slot) {
 
 void launch_tupd(dfm_ctx* c) {
   const dim3 grid((c->F + 7) / 8, c->N);
-  k_tupd_mma<<<grid, 32 * kTupdWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->V.p, c->Aw.p, c->Bw.p,
-                                                       c->floor_);
+  auto kern = k_tupd_mma<8>;
+  switch ((c->K + 7) / 8) {
+    case 1: kern = k_tupd_mma<1>; break;
+    case 2: kern = k_tupd_mma<2>; break;
+    case 3: case 4: kern = k_tupd_mma<4>; break;
+    default: kern = k_tupd_mma<8>; break;
+  }
+  kern<<<grid, 32 * kTupdWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->V.p, c->Aw.p, c->Bw.p, c->floor_);
   DFM_CK_LAUNCH();
   c->launches++;
 }
@@ -270,8 +276,15 @@ void launch_pd(dfm_ctx* c) {
 void launch_vupd(dfm_ctx* c) {
   const dim3 grid((c->T + 7) / 8, c->N);
   const bool sharded = c->comm != nullptr && c->nranks > 1;
-  k_vupd_mma<<<grid, 32 * kVupdMWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->Aw.p, c->Bw.p,
-                                                         c->V.p, sharded ? c->numden.p : nullptr, c->floor_);
+  auto kern = k_vupd_mma<8>;
+  switch ((c->K + 7) / 8) {
+    case 1: kern = k_vupd_mma<1>; break;
+    case 2: kern = k_vupd_mma<2>; break;
+    case 3: case 4: kern = k_vupd_mma<4>; break;
+    default: kern = k_vupd_mma<8>; break;
+  }
+  kern<<<grid, 32 * kVupdMWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->Aw.p, c->Bw.p, c->V.p,
+                                                 sharded ? c->numden.p : nullptr, c->floor_);
   DFM_CK_LAUNCH();
   c->launches++;
   if (sharded) {
