@@ -113,8 +113,9 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
 #pragma unroll
     for (int n = 0; n < kMaxN; ++n) h[n] = n < N ? __ldg(Hf + n * T + t) : 0.0;
   };
-  // |W^H x|^2 of one frame for block b; x read from global (L2)
-  auto power_block = [&](int b, const cd* xt, double* P) {
+  // |W^H x|^2 of one frame for block b; x read from global (L2); the loaded
+  // samples are also stored to xout[q * xstride] when xout is given
+  auto power_block = [&](int b, const cd* xt, double* P, cd* xout = nullptr, int xstride = 0) {
     const int mb = MBof(b), off = OFF(b);
     const cd* wb = Wsm + WOFF(b);
     if constexpr (SB) {
@@ -123,6 +124,7 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
       for (int q = 0; q < MB_; ++q) {
         const double2 v = __ldg(reinterpret_cast<const double2*>(xt + off + q));
         xv[q] = cd{v.x, v.y};
+        if (xout) xout[q * xstride] = xv[q];
       }
 #pragma unroll
       for (int mu = 0; mu < MB_; ++mu) {
@@ -137,6 +139,7 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
         for (int q = 0; q < mb; ++q) {
           const double2 v = __ldg(reinterpret_cast<const double2*>(xt + off + q));
           s = s + cmulc(wb[mu * mb + q], cd{v.x, v.y});
+          if (xout && mu == 0) xout[q * xstride] = cd{v.x, v.y};
         }
         P[mu] = norm2(s);
       }
@@ -259,10 +262,11 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
         double h[kMaxN];
         load_h(t, h);
         const cd* xt = xf + (size_t)t * M;
+#pragma unroll
         for (int b = 0; b < nb; ++b) {
           double P[MAXMB];
-          power_block(b, xt, P);
           const int off = OFF(b), mb = MBof(b);
+          power_block(b, xt, P, a.start ? xsm + off * FTp + tid : nullptr, FTp);
 #pragma unroll
           for (int mu = 0; mu < MAXMB; ++mu)
             if (mu < mb) {
@@ -274,11 +278,7 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
               const double ie = 1.0 / fmax(raw, floor_);
               cost += P[mu] * ie;
               lacc.mul(fmax(raw, 1e-300));
-              if (a.start) {
-                is[m * FTp + tid] = ie;
-                const double2 v = __ldg(reinterpret_cast<const double2*>(xt + m));
-                xsm[m * FTp + tid] = cd{v.x, v.y};
-              }
+              if (a.start) is[m * FTp + tid] = ie;
             }
         }
         lacc.renorm();
