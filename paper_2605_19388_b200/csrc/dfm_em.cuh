@@ -479,33 +479,42 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 // (F x K) x (K x T) product; a warp owns 8 bins x 32 frames, the CTA 8 warps
 // along the frames.
 constexpr int kSpecMaxKs = kMaxK / 4;
-constexpr int kSpecWarps = 4;
+constexpr int kSpecWarps = 4, kSpecTiles = 4;  // a warp owns 8 bins x (4 x 8) frames
+template <int KS>  // k-steps of 4 (K <= 4 KS)
 __global__ void __launch_bounds__(32 * kSpecWarps) k_spec_mma(int F, int T, int N, int K, const double* __restrict__ Tf,
                                                              const double* __restrict__ V, double* __restrict__ H) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
   const int n = blockIdx.z, f0 = blockIdx.y * 8;
-  const int tb = (blockIdx.x * kSpecWarps + warp) * 8;
-  if (tb >= T) return;
-  const int ks = (K + 3) / 4;
-  const int f = f0 + g, tl = tb + g;
-  double a[kSpecMaxKs], b[kSpecMaxKs];
+  const int t0 = (blockIdx.x * kSpecWarps + warp) * 8 * kSpecTiles;
+  if (t0 >= T) return;
+  constexpr int ks = KS;
+  const int f = f0 + g;
+  // all operand loads first (many in flight), then the DMMAs
+  double a[KS], b[kSpecTiles][KS];
 #pragma unroll
-  for (int s = 0; s < kSpecMaxKs; ++s) {
+  for (int s = 0; s < KS; ++s) {
     const int k = 4 * s + q;
     const bool ok = s < ks && k < K;
     a[s] = (ok && f < F) ? __ldg(Tf + ((size_t)f * N + n) * K + k) : 0.0;
-    b[s] = (ok && tl < T) ? __ldg(V + ((size_t)n * K + k) * T + tl) : 0.0;
-  }
-  double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-  for (int s = 0; s < kSpecMaxKs; ++s)
-    if (s < ks) dmma(c0, c1, a[s], b[s]);
-  const int t = tb + 2 * q;
-  if (f < F) {
-    double* hp = H + ((size_t)f * N + n) * T;
-    if (t < T) hp[t] = c0;
-    if (t + 1 < T) hp[t + 1] = c1;
+    for (int j = 0; j < kSpecTiles; ++j) {
+      const int tl = t0 + 8 * j + g;
+      b[j][s] = (ok && tl < T) ? __ldg(V + ((size_t)n * K + k) * T + tl) : 0.0;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kSpecTiles; ++j) {
+    double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+    for (int s = 0; s < KS; ++s)
+      if (s < ks) dmma(c0, c1, a[s], b[j][s]);
+    const int t = t0 + 8 * j + 2 * q;
+    if (f < F) {
+      double* hp = H + ((size_t)f * N + n) * T;
+      if (t < T) hp[t] = c0;
+      if (t + 1 < T) hp[t + 1] = c1;
+    }
   }
 }
 
@@ -687,7 +696,7 @@ __global__ void __launch_bounds__(32 * kVupdMWarps) k_vupd_mma(int F, int T, int
 // k_spec_mma), eta' = max(h' Lambda, floor), P = |W^H x|^2, and the V-update
 // weights A'_n = sum_m Lambda z, B'_n = sum_m Lambda / eta' (engine.cpp:231-237).
 template <int MB_, int NB_, int NS_, int MAXMB>
-__global__ void __launch_bounds__(128) k_pdw(const EmArgs a) {
+__global__ void __launch_bounds__(128, 6) k_pdw(const EmArgs a) {
   constexpr bool SB = MB_ > 0 && NB_ > 0;
   __shared__ double Ls[kMaxN * 64];
   __shared__ cd Ws[DFM_MAX_MB * DFM_MAX_MB * 4];

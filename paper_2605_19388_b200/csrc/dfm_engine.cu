@@ -232,8 +232,17 @@ void ensure_cost(dfm_ctx* c, int slots) {
 
 // H = T V on the FP64 tensor cores (DMMA)
 void launch_spec(dfm_ctx* c) {
-  const dim3 grid((c->T + 8 * kSpecWarps - 1) / (8 * kSpecWarps), (c->F + 7) / 8, c->N);
-  k_spec_mma<<<grid, 32 * kSpecWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->V.p, c->H.p);
+  const int tpc = 8 * kSpecWarps * kSpecTiles;  // frames per CTA
+  const dim3 grid((c->T + tpc - 1) / tpc, (c->F + 7) / 8, c->N);
+  auto kern = k_spec_mma<16>;
+  switch ((c->K + 3) / 4) {
+    case 1: kern = k_spec_mma<1>; break;
+    case 2: kern = k_spec_mma<2>; break;
+    case 3: case 4: kern = k_spec_mma<4>; break;
+    case 5: case 6: case 7: case 8: kern = k_spec_mma<8>; break;
+    default: kern = k_spec_mma<16>; break;
+  }
+  kern<<<grid, 32 * kSpecWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->V.p, c->H.p);
   DFM_CK_LAUNCH();
   c->launches++;
 }
