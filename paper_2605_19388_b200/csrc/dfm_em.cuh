@@ -77,6 +77,19 @@ __device__ __forceinline__ void em_stamp(const EmArgs& a, int phase) {
   }
 }
 
+// 1/x for x >= floor > 0: hardware reciprocal estimate + two Newton steps
+// (within 1 ulp of the IEEE quotient the reference computes).
+__device__ __forceinline__ double rcp_pos(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b);
+
 template <int MB_, int NB_, int NS_, int MAXMB>
 __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
   constexpr bool SB = MB_ > 0 && NB_ > 0;
@@ -155,6 +168,13 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
     double* is = zs + M * FTp;       // [M][FTp]
     const int NM = N * M, SL = sp.SL;
     for (int u = tid; u < NM * SL; u += FT) red[2 * u] = red[2 * u + 1] = 0.0;
+    constexpr int kLamJobs = 8;
+    const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3, nwarps = FT >> 5;
+    const int njobs = 2 * ((M + 7) / 8);
+    const bool use_mma = N <= 8 && njobs <= kLamJobs * nwarps;
+    double lj0[kLamJobs], lj1[kLamJobs];
+#pragma unroll
+    for (int jj = 0; jj < kLamJobs; ++jj) lj0[jj] = lj1[jj] = 0.0;
     for (int tl = 0; tl < ntiles; ++tl) {
       const int t = tl * FT + tid;
       const int tn = min(FT, T - tl * FT);
@@ -178,15 +198,37 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
 #pragma unroll
               for (int n = 0; n < kMaxN; ++n)
                 if (n < N) raw += h[n] * Lsm[n * M + m];
-              const double ie = 1.0 / fmax(raw, floor_);
+              const double ie = rcp_pos(fmax(raw, floor_));
               is[m * FTp + tid] = ie;
               zs[m * FTp + tid] = P[mu] * ie * ie;
             }
         }
       }
       __syncthreads();
-      // (n, m) units: each sums its frames of the tile (stride SL), then adds
-      // the tile partial to its running sum (tile order: deterministic)
+      // Lambda numerator / denominator (engine.cpp:139-145) as the products
+      // (N x frames) (frames x M) on the FP64 tensor cores: warp job = (column
+      // tile of 8 mics, num|den), accumulated over k-steps of 4 frames and over
+      // tiles in registers.  Fallback: SIMT (n, m) units.
+      if (use_mma) {
+#pragma unroll
+        for (int jj = 0; jj < kLamJobs; ++jj) {
+          const int job = warp + jj * nwarps;
+          if (job < njobs) {
+            const int j = job >> 1;
+            const double* brow = (job & 1) ? is : zs;
+            const int m = 8 * j + g;
+            double c0 = lj0[jj], c1 = lj1[jj];
+            for (int t0 = 0; t0 < tn; t0 += 4) {
+              const int t = t0 + q;
+              const double av = (g < N && t < tn) ? hs[g * FTp + t] : 0.0;
+              const double bv = (m < M && t < tn) ? brow[m * FTp + t] : 0.0;
+              dmma(c0, c1, av, bv);
+            }
+            lj0[jj] = c0;
+            lj1[jj] = c1;
+          }
+        }
+      } else
       for (int u = tid; u < NM * SL; u += FT) {
         const int item = u % NM, sl = u / NM;
         const int in_ = item / M, im = item - in_ * M;
@@ -201,6 +243,23 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
         }
         red[2 * u] += num;
         red[2 * u + 1] += den;
+      }
+      __syncthreads();
+    }
+    if (use_mma) {
+      __syncthreads();
+      // scatter the DMMA accumulators (C[n][m] at c0 = (g, 2q), c1 = (g, 2q+1)) into red[]
+#pragma unroll
+      for (int jj = 0; jj < kLamJobs; ++jj) {
+        const int job = warp + jj * nwarps;
+        if (job < njobs && g < N) {
+          const int j = job >> 1, w = job & 1;
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int m = 8 * j + 2 * q + i;
+            if (m < M) red[2 * (g * M + m) + w] = i ? lj1[jj] : lj0[jj];
+          }
+        }
       }
       __syncthreads();
     }
@@ -275,7 +334,7 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
 #pragma unroll
               for (int n = 0; n < kMaxN; ++n)
                 if (n < N) raw += h[n] * Lsm[n * M + m];
-              const double ie = 1.0 / fmax(raw, floor_);
+              const double ie = rcp_pos(fmax(raw, floor_));
               cost += P[mu] * ie;
               lacc.mul(fmax(raw, 1e-300));
               if (a.start) is[m * FTp + tid] = ie;
@@ -429,7 +488,7 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
 #pragma unroll
           for (int n = 0; n < kMaxN; ++n)
             if (n < N) raw += h[n] * Lsm[n * M + m];
-          const double ie = 1.0 / fmax(raw, floor_);
+          const double ie = rcp_pos(fmax(raw, floor_));
           const double z = P[mu] * ie * ie;
 #pragma unroll
           for (int n = 0; n < kMaxN; ++n)
@@ -764,7 +823,7 @@ __global__ void __launch_bounds__(128, 6) k_pdw(const EmArgs a) {
 #pragma unroll
         for (int n = 0; n < kMaxN; ++n)
           if (n < N) raw += h[n] * Lf[n * M + m];
-        const double ie = 1.0 / fmax(raw, a.floor_);
+        const double ie = rcp_pos(fmax(raw, a.floor_));
         const double z = P[mu] * ie * ie;
 #pragma unroll
         for (int n = 0; n < kMaxN; ++n)
