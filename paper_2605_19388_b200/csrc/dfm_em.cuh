@@ -159,6 +159,27 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
     }
   };
 
+  // static shapes: every sample of a frame is loaded up front (one batch of
+  // M 16-byte loads in flight), then |W^H x|^2 per block from registers
+  constexpr int MS = SB ? MB_ * NB_ : 1;
+  auto load_frame = [&](const cd* xt, cd* xall) {
+#pragma unroll
+    for (int m = 0; m < MS; ++m) {
+      const double2 v = __ldg(reinterpret_cast<const double2*>(xt + m));
+      xall[m] = cd{v.x, v.y};
+    }
+  };
+  auto power_regs = [&](int b, const cd* xall, double* P) {
+    const cd* wb = Wsm + b * MB_ * MB_;
+#pragma unroll
+    for (int mu = 0; mu < MB_; ++mu) {
+      cd s{0.0, 0.0};
+#pragma unroll
+      for (int q = 0; q < MB_; ++q) s = s + cmulc(wb[mu * MB_ + q], xall[b * MB_ + q]);
+      P[mu] = norm2(s);
+    }
+  };
+
   // ================================================================ pass A
   // finish iteration i-1: Lambda update with eta = max(h Lambda_old, floor)
   if (a.finish == 2) {
@@ -185,10 +206,15 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
         for (int n = 0; n < kMaxN; ++n)
           if (n < N) hs[n * FTp + tid] = h[n];
         const cd* xt = xf + (size_t)t * M;
+        cd xall[MS];
+        if constexpr (SB) load_frame(xt, xall);
 #pragma unroll
         for (int b = 0; b < nb; ++b) {
           double P[MAXMB];
-          power_block(b, xt, P);
+          if constexpr (SB)
+            power_regs(b, xall, P);
+          else
+            power_block(b, xt, P);
           const int off = OFF(b), mb = MBof(b);
 #pragma unroll
           for (int mu = 0; mu < MAXMB; ++mu)
@@ -321,11 +347,21 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
         double h[kMaxN];
         load_h(t, h);
         const cd* xt = xf + (size_t)t * M;
+        cd xall[MS];
+        if constexpr (SB) {
+          load_frame(xt, xall);
+          if (a.start)
+#pragma unroll
+            for (int m = 0; m < MS; ++m) xsm[m * FTp + tid] = xall[m];
+        }
 #pragma unroll
         for (int b = 0; b < nb; ++b) {
           double P[MAXMB];
           const int off = OFF(b), mb = MBof(b);
-          power_block(b, xt, P, a.start ? xsm + off * FTp + tid : nullptr, FTp);
+          if constexpr (SB)
+            power_regs(b, xall, P);
+          else
+            power_block(b, xt, P, a.start ? xsm + off * FTp + tid : nullptr, FTp);
 #pragma unroll
           for (int mu = 0; mu < MAXMB; ++mu)
             if (mu < mb) {
@@ -473,12 +509,18 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
     double h[kMaxN];
     load_h(t, h);
     const cd* xt = xf + (size_t)t * M;
+    cd xall[MS];
+    if constexpr (SB) load_frame(xt, xall);
     double A[kMaxN], B[kMaxN];
 #pragma unroll
     for (int n = 0; n < kMaxN; ++n) A[n] = B[n] = 0.0;
+#pragma unroll
     for (int b = 0; b < nb; ++b) {
       double P[MAXMB];
-      power_block(b, xt, P);
+      if constexpr (SB)
+        power_regs(b, xall, P);
+      else
+        power_block(b, xt, P);
       const int off = OFF(b), mb = MBof(b);
 #pragma unroll
       for (int mu = 0; mu < MAXMB; ++mu)
