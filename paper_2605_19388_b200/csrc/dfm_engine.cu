@@ -112,6 +112,8 @@ struct dfm_ctx {
   int nranks = 1, rank = 0;
   long long launches = 0;
   cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  cudaGraphExec_t step_exec = nullptr;  // one steady-state iteration (cost -> slot 1)
+  bool use_graph = true;
   bool has_obs = false, has_model = false;
   std::vector<cudaEvent_t> iter_ev;
 };
@@ -226,8 +228,12 @@ void set_kernel_attrs(dfm_ctx* c) {
 
 }
 
+void drop_graph(dfm_ctx* c);
 void ensure_cost(dfm_ctx* c, int slots) {
-  if (c->cost_part.n < (size_t)slots * c->F) c->cost_part.alloc((size_t)slots * c->F);
+  if (c->cost_part.n < (size_t)slots * c->F) {
+    drop_graph(c);  // a captured step holds the old cost pointer
+    c->cost_part.alloc((size_t)slots * c->F);
+  }
 }
 
 // H = T V on the FP64 tensor cores (DMMA)
@@ -317,6 +323,47 @@ void launch_rest(dfm_ctx* c, cudaEvent_t* ev) {
   launch_spec(c);
 }
 
+void drop_graph(dfm_ctx* c) {
+  if (c->step_exec) cudaGraphExecDestroy(c->step_exec);
+  c->step_exec = nullptr;
+}
+
+// Captures one steady-state iteration (k_em_bin finish+start writing cost
+// slot 1, then the five follow-up kernels, with the split events) into a CUDA
+// graph; replays cut the per-launch gaps.  Not used when sharded (the NCCL
+// allreduce stays a stream launch).
+bool step_graph(dfm_ctx* c) {
+  if (!c->use_graph || (c->comm && c->nranks > 1)) return false;
+  if (c->step_exec) return true;
+  cudaGraph_t g = nullptr;
+  DFM_CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  const long long l0 = c->launches;
+  DFM_CK(cudaEventRecord(c->ev[0], c->stream));
+  launch_em(c, 2, 1, 1);
+  DFM_CK(cudaEventRecord(c->ev[1], c->stream));
+  launch_rest(c, c->ev);
+  DFM_CK(cudaEventRecord(c->ev[5], c->stream));
+  DFM_CK(cudaStreamEndCapture(c->stream, &g));
+  c->launches = l0;  // capture does not launch
+  DFM_CK(cudaGraphInstantiate(&c->step_exec, g, 0));
+  cudaGraphDestroy(g);
+  return true;
+}
+
+// One steady-state iteration: graph replay, or the same launches on the stream.
+void run_step(dfm_ctx* c, bool events) {
+  if (step_graph(c)) {
+    DFM_CK(cudaGraphLaunch(c->step_exec, c->stream));
+    c->launches += 6;
+    return;
+  }
+  if (events) DFM_CK(cudaEventRecord(c->ev[0], c->stream));
+  launch_em(c, 2, 1, 1);
+  if (events) DFM_CK(cudaEventRecord(c->ev[1], c->stream));
+  launch_rest(c, events ? c->ev : nullptr);
+  if (events) DFM_CK(cudaEventRecord(c->ev[5], c->stream));
+}
+
 }  // namespace
 
 #define DFM_API_BEGIN try {
@@ -393,6 +440,7 @@ dfm_ctx* dfm_create(int F, int T, int nblocks, const int* block_sizes, int N, in
 void dfm_destroy(dfm_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
+  drop_graph(c);
   if (c->comm) nccl().CommDestroy(c->comm);
   for (auto e : c->iter_ev) cudaEventDestroy(e);
   for (auto e : c->ev)
@@ -504,6 +552,7 @@ int dfm_comm_init(dfm_ctx* c, const void* uid, int nranks, int rank) {
   DFM_CK(cudaSetDevice(c->device));
   ncclUniqueId id;
   std::memcpy(&id, uid, sizeof(id));
+  drop_graph(c);
   NCCL_CK(nccl().CommInitRank(&c->comm, nranks, id, rank));
   c->nranks = nranks;
   c->rank = rank;
@@ -534,8 +583,15 @@ int dfm_fit(dfm_ctx* c, int iters, double* cost_trace, double* wall_seconds, dou
   launch_spec(c);
   for (int i = 0; i <= iters; ++i) {
     DFM_CK(cudaEventRecord(c->iter_ev[i], c->stream));
-    launch_em(c, i == 0 ? 1 : 2, i < iters ? 1 : 0, i);
-    if (i < iters) launch_rest(c, nullptr);
+    if (i == 0 || i == iters) {
+      launch_em(c, i == 0 ? 1 : 2, i < iters ? 1 : 0, i);
+      if (i < iters) launch_rest(c, nullptr);
+    } else {
+      run_step(c, false);  // writes cost slot 1
+      if (i != 1)
+        DFM_CK(cudaMemcpyAsync(c->cost_part.p + (size_t)i * c->F, c->cost_part.p + c->F, sizeof(double) * c->F,
+                               cudaMemcpyDeviceToDevice, c->stream));
+    }
   }
   DFM_CK(cudaEventRecord(c->iter_ev[iters + 1], c->stream));
   std::vector<double> part((size_t)(iters + 1) * c->F);
@@ -586,11 +642,7 @@ int dfm_prime(dfm_ctx* c) {
 int dfm_bench_step(dfm_ctx* c) {
   if (!c) return DFM_ERR_ARG;
   DFM_API_BEGIN
-  DFM_CK(cudaEventRecord(c->ev[0], c->stream));
-  launch_em(c, 2, 1, 1);
-  DFM_CK(cudaEventRecord(c->ev[1], c->stream));
-  launch_rest(c, c->ev);
-  DFM_CK(cudaEventRecord(c->ev[5], c->stream));
+  run_step(c, true);
   return DFM_OK;
   DFM_API_END
 }
@@ -633,6 +685,7 @@ int dfm_set_tiling(dfm_ctx* c, int frame_tile, int pd_frames) {
   DFM_API_BEGIN
   DFM_CK(cudaSetDevice(c->device));
   const int oFT = c->req_FT, oTB = c->req_TB;
+  drop_graph(c);
   c->req_FT = frame_tile;
   c->req_TB = pd_frames;
   if (!choose_tiling(c)) {
@@ -650,6 +703,7 @@ int dfm_set_trace(dfm_ctx* c, int on) {
   if (!c) return DFM_ERR_ARG;
   DFM_API_BEGIN
   DFM_CK(cudaSetDevice(c->device));
+  drop_graph(c);
   c->tracing = on != 0;
   if (c->tracing) {
     c->trace.alloc((size_t)c->F * 16);
@@ -674,6 +728,7 @@ int dfm_force_generic(dfm_ctx* c, int on) {
   if (!c) return DFM_ERR_ARG;
   DFM_API_BEGIN
   DFM_CK(cudaSetDevice(c->device));
+  drop_graph(c);
   c->force_generic = on != 0;
   select_kernels(c);
   if (!choose_tiling(c)) return DFM_ERR_UNSUPPORTED;

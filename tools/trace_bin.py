@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--workload", default="config1")
     ap.add_argument("--tiling", default="")
     ap.add_argument("--generic", action="store_true")
+    ap.add_argument("--no-flush", action="store_true")
     args = ap.parse_args()
     c = bench.CONFIGS[args.workload]
     layout = dfm.BlockLayout(c["sizes"])
@@ -46,7 +47,8 @@ def main():
     for _ in range(3):
         dfm._capi.check(lib.dfm_bench_step(eng.ctx))
     n = dfm._capi.check(lib.dfm_set_trace(eng.ctx, 1))
-    dfm._capi.check(lib.dfm_l2_flush(0))
+    if not args.no_flush:
+        dfm._capi.check(lib.dfm_l2_flush(0))
     dfm._capi.check(lib.dfm_bench_step(eng.ctx))
     ms = lib.dfm_bench_last_ms(eng.ctx)
     sp = (ctypes.c_double * 5)()
