@@ -278,15 +278,17 @@ def main():
     eng.set_model(init.nmf, init.w0, init.lambda0)
     ctx = eng.ctx
 
-    def step():
-        dfm._capi.check(lib.dfm_l2_flush(local))  # untimed: outside the step's events
-        dfm._capi.check(lib.dfm_bench_step(ctx))
-        ms = lib.dfm_bench_last_ms(ctx)
+    def step(split=False):
         import ctypes
 
-        sp = (ctypes.c_double * 5)()
-        lib.dfm_bench_last_split(ctx, sp)
-        return ms, list(sp)
+        dfm._capi.check(lib.dfm_l2_flush(local))  # untimed: outside the step's events
+        if split:  # stream launches with per-kernel events (breakdown only)
+            dfm._capi.check(lib.dfm_bench_split_step(ctx))
+            sp = (ctypes.c_double * 5)()
+            dfm._capi.check(lib.dfm_bench_last_split(ctx, sp))
+            return list(sp)
+        dfm._capi.check(lib.dfm_bench_step(ctx))  # one CUDA-graph replay
+        return lib.dfm_bench_last_ms(ctx)
 
     dfm._capi.check(lib.dfm_prime(ctx))
     for _ in range(args.warmup):
@@ -297,15 +299,15 @@ def main():
     torch.cuda.synchronize()
     launches0 = eng.launches()
     sampler = ClockSampler(local).start()
-    t_ms, split = [], []
+    t_ms = []
     for _ in range(args.steps):
-        ms, sp = step()
-        t_ms.append(ms)
-        split.append(sp)
+        t_ms.append(step())
     dfm._capi.check(lib.dfm_sync(ctx))
     torch.cuda.synchronize()
     clocks = sampler.stop()
     launches = eng.launches() - launches0
+    # per-kernel breakdown from separate (untimed-for-value) stream-launched steps
+    split = [step(split=True) for _ in range(min(20, args.steps))]
     total_ms = float(np.sum(t_ms))
     if pg:
         tt = torch.tensor([total_ms], dtype=torch.float64, device="cuda")

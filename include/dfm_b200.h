@@ -111,8 +111,11 @@ int dfm_prime(dfm_ctx* ctx);
 int dfm_bench_step(dfm_ctx* ctx);
 int dfm_sync(dfm_ctx* ctx);
 double dfm_bench_last_ms(dfm_ctx* ctx);
-/* Device time of each kernel of the last dfm_bench_step (ms):
- * {k_em_bin, k_tupd, k_pd, k_vupd (+ allreduce), k_spec}. */
+/* dfm_bench_step replays the iteration as a CUDA graph (one launch).
+ * dfm_bench_split_step runs the same iteration as stream launches with events
+ * between the kernels; dfm_bench_last_split then returns the device time of
+ * each kernel (ms): {k_em_bin, k_tupd, k_spec+k_pdw, k_vupd (+ allreduce), k_spec}. */
+int dfm_bench_split_step(dfm_ctx* ctx);
 int dfm_bench_last_split(dfm_ctx* ctx, double* ms5);
 /* Kernel launches issued by the context so far (for the bench's gpu_launches). */
 long long dfm_launch_count(const dfm_ctx* ctx);

@@ -34,6 +34,7 @@ _SIGS = {
     "dfm_fit": (_i, [_vp, _i, _vp, _vp, _vp]),
     "dfm_prime": (_i, [_vp]),
     "dfm_bench_step": (_i, [_vp]),
+    "dfm_bench_split_step": (_i, [_vp]),
     "dfm_sync": (_i, [_vp]),
     "dfm_bench_last_ms": (_d, [_vp]),
     "dfm_bench_last_split": (_i, [_vp, _dp]),

@@ -97,7 +97,7 @@ struct dfm_ctx {
   Layout L;
   cudaStream_t stream = nullptr;
   DBuf<cd> x, W;
-  DBuf<double> Tf, V, lam, H, Aw, Bw, numden, cost_part, cost_sum;
+  DBuf<double> Tf, V, lam, H, Aw, Bw, numden, cost_part, cost_sum, cost_step;
   DBuf<int> fallbacks;
   int maxmb = 4;
   int kmaxmb = 4;  // MAXMB of the selected instantiations
@@ -253,11 +253,11 @@ void launch_spec(dfm_ctx* c) {
   c->launches++;
 }
 
-void launch_em(dfm_ctx* c, int finish, int start, int slot) {
+void launch_em(dfm_ctx* c, int finish, int start, int slot, double* cost_dst = nullptr) {
   EmArgs a = make_args(c);
   a.finish = finish;
   a.start = start;
-  a.cost_out = c->cost_part.p + (size_t)slot * c->F;
+  a.cost_out = cost_dst ? cost_dst : c->cost_part.p + (size_t)slot * c->F;
   a.trace = c->tracing ? c->trace.p : nullptr;
   c->kem<<<c->F, c->FT, c->smem_em, c->stream>>>(a);
   DFM_CK_LAUNCH();
@@ -335,14 +335,12 @@ void drop_graph(dfm_ctx* c) {
 bool step_graph(dfm_ctx* c) {
   if (!c->use_graph || (c->comm && c->nranks > 1)) return false;
   if (c->step_exec) return true;
+  if (c->cost_step.n < (size_t)c->F) c->cost_step.alloc(c->F);
   cudaGraph_t g = nullptr;
   DFM_CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   const long long l0 = c->launches;
-  DFM_CK(cudaEventRecord(c->ev[0], c->stream));
-  launch_em(c, 2, 1, 1);
-  DFM_CK(cudaEventRecord(c->ev[1], c->stream));
-  launch_rest(c, c->ev);
-  DFM_CK(cudaEventRecord(c->ev[5], c->stream));
+  launch_em(c, 2, 1, 0, c->cost_step.p);
+  launch_rest(c, nullptr);
   DFM_CK(cudaStreamEndCapture(c->stream, &g));
   c->launches = l0;  // capture does not launch
   DFM_CK(cudaGraphInstantiate(&c->step_exec, g, 0));
@@ -350,18 +348,21 @@ bool step_graph(dfm_ctx* c) {
   return true;
 }
 
-// One steady-state iteration: graph replay, or the same launches on the stream.
-void run_step(dfm_ctx* c, bool events) {
-  if (step_graph(c)) {
+// One steady-state iteration whose per-bin cost lands in cost_step: a graph
+// replay, or the same launches on the stream (with the per-kernel split
+// events when `split` is set).
+void run_step(dfm_ctx* c, bool split) {
+  if (!split && step_graph(c)) {
     DFM_CK(cudaGraphLaunch(c->step_exec, c->stream));
     c->launches += 6;
     return;
   }
-  if (events) DFM_CK(cudaEventRecord(c->ev[0], c->stream));
-  launch_em(c, 2, 1, 1);
-  if (events) DFM_CK(cudaEventRecord(c->ev[1], c->stream));
-  launch_rest(c, events ? c->ev : nullptr);
-  if (events) DFM_CK(cudaEventRecord(c->ev[5], c->stream));
+  if (c->cost_step.n < (size_t)c->F) c->cost_step.alloc(c->F);
+  if (split) DFM_CK(cudaEventRecord(c->ev[0], c->stream));
+  launch_em(c, 2, 1, 0, c->cost_step.p);
+  if (split) DFM_CK(cudaEventRecord(c->ev[1], c->stream));
+  launch_rest(c, split ? c->ev : nullptr);
+  if (split) DFM_CK(cudaEventRecord(c->ev[5], c->stream));
 }
 
 }  // namespace
@@ -587,10 +588,9 @@ int dfm_fit(dfm_ctx* c, int iters, double* cost_trace, double* wall_seconds, dou
       launch_em(c, i == 0 ? 1 : 2, i < iters ? 1 : 0, i);
       if (i < iters) launch_rest(c, nullptr);
     } else {
-      run_step(c, false);  // writes cost slot 1
-      if (i != 1)
-        DFM_CK(cudaMemcpyAsync(c->cost_part.p + (size_t)i * c->F, c->cost_part.p + c->F, sizeof(double) * c->F,
-                               cudaMemcpyDeviceToDevice, c->stream));
+      run_step(c, false);  // per-bin cost of iteration i-1 -> cost_step
+      DFM_CK(cudaMemcpyAsync(c->cost_part.p + (size_t)i * c->F, c->cost_step.p, sizeof(double) * c->F,
+                             cudaMemcpyDeviceToDevice, c->stream));
     }
   }
   DFM_CK(cudaEventRecord(c->iter_ev[iters + 1], c->stream));
@@ -640,6 +640,16 @@ int dfm_prime(dfm_ctx* c) {
 }
 
 int dfm_bench_step(dfm_ctx* c) {
+  if (!c) return DFM_ERR_ARG;
+  DFM_API_BEGIN
+  DFM_CK(cudaEventRecord(c->ev[0], c->stream));
+  run_step(c, false);
+  DFM_CK(cudaEventRecord(c->ev[5], c->stream));
+  return DFM_OK;
+  DFM_API_END
+}
+
+int dfm_bench_split_step(dfm_ctx* c) {
   if (!c) return DFM_ERR_ARG;
   DFM_API_BEGIN
   run_step(c, true);

@@ -49,7 +49,7 @@ def main():
     n = dfm._capi.check(lib.dfm_set_trace(eng.ctx, 1))
     if not args.no_flush:
         dfm._capi.check(lib.dfm_l2_flush(0))
-    dfm._capi.check(lib.dfm_bench_step(eng.ctx))
+    dfm._capi.check(lib.dfm_bench_split_step(eng.ctx))
     ms = lib.dfm_bench_last_ms(eng.ctx)
     sp = (ctypes.c_double * 5)()
     lib.dfm_bench_last_split(eng.ctx, sp)
