@@ -92,6 +92,18 @@ int dfm_get_model(dfm_ctx* ctx, double* Tm, double* V, double* lam, double* w);
 int dfm_comm_init(dfm_ctx* ctx, const void* nccl_unique_id, int nranks, int rank);
 int dfm_nccl_get_unique_id(void* out128);
 
+/* Shard stepping: the frequency-sharded iteration with the V-update exchange
+ * done by the caller instead of NCCL (tests of the multi-GPU decomposition on
+ * one device, or a custom transport).  dfm_shard_begin runs up to the first
+ * partial V update; then repeat { dfm_shard_numden (this shard's {num, den},
+ * 2*N*K*T doubles [2][N][K][T]); sum over shards; dfm_shard_advance(sum) }
+ * while it returns 1; dfm_shard_end returns the fallback count and writes the
+ * shard-LOCAL cost trace (iters+1; sum over shards = global cost). */
+int dfm_shard_begin(dfm_ctx* ctx, int iters);
+int dfm_shard_numden(dfm_ctx* ctx, double* out);
+int dfm_shard_advance(dfm_ctx* ctx, const double* in);
+int dfm_shard_end(dfm_ctx* ctx, double* cost_trace_local);
+
 /* Runs `iters` EM sweeps on the device-resident state (engine.cpp:197-272).
  * cost_trace: iters+1 entries (initial cost first, FitReport::cost_trace);
  * wall_seconds: iters per-iteration device times (may be NULL);

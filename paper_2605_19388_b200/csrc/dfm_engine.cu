@@ -112,7 +112,9 @@ struct dfm_ctx {
   int nranks = 1, rank = 0;
   long long launches = 0;
   cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-  cudaGraphExec_t step_exec = nullptr;  // one steady-state iteration (cost -> slot 1)
+  cudaGraphExec_t step_exec = nullptr;  // one steady-state iteration
+  bool host_exchange = false;  // shard stepping API: {num, den} exchanged by the caller
+  int xs_iter = 0, xs_iters = 0;
   bool use_graph = true;
   bool has_obs = false, has_model = false;
   std::vector<cudaEvent_t> iter_ev;
@@ -290,7 +292,7 @@ void launch_pd(dfm_ctx* c) {
 
 void launch_vupd(dfm_ctx* c) {
   const dim3 grid((c->T + 7) / 8, c->N);
-  const bool sharded = c->comm != nullptr && c->nranks > 1;
+  const bool sharded = (c->comm != nullptr && c->nranks > 1) || c->host_exchange;
   auto kern = k_vupd_mma<8>;
   switch ((c->K + 7) / 8) {
     case 1: kern = k_vupd_mma<1>; break;
@@ -302,7 +304,7 @@ void launch_vupd(dfm_ctx* c) {
                                                  sharded ? c->numden.p : nullptr, c->floor_);
   DFM_CK_LAUNCH();
   c->launches++;
-  if (sharded) {
+  if (sharded && !c->host_exchange) {
     const size_t nkt = (size_t)c->N * c->K * c->T;
     NCCL_CK(nccl().AllReduce(c->numden.p, c->numden.p, 2 * nkt, ncclDouble, ncclSum, c->comm, c->stream));
     k_vapply<<<(unsigned)((nkt + 255) / 256), 256, 0, c->stream>>>(nkt, c->numden.p, c->V.p, c->floor_);
@@ -320,7 +322,7 @@ void launch_rest(dfm_ctx* c, cudaEvent_t* ev) {
   if (ev) DFM_CK(cudaEventRecord(ev[3], c->stream));
   launch_vupd(c);
   if (ev) DFM_CK(cudaEventRecord(ev[4], c->stream));
-  launch_spec(c);
+  if (!c->host_exchange) launch_spec(c);  // else: after the caller's exchange
 }
 
 void drop_graph(dfm_ctx* c) {
@@ -333,7 +335,7 @@ void drop_graph(dfm_ctx* c) {
 // graph; replays cut the per-launch gaps.  Not used when sharded (the NCCL
 // allreduce stays a stream launch).
 bool step_graph(dfm_ctx* c) {
-  if (!c->use_graph || (c->comm && c->nranks > 1)) return false;
+  if (!c->use_graph || (c->comm && c->nranks > 1) || c->host_exchange) return false;
   if (c->step_exec) return true;
   if (c->cost_step.n < (size_t)c->F) c->cost_step.alloc(c->F);
   cudaGraph_t g = nullptr;
@@ -623,6 +625,73 @@ int dfm_fit(dfm_ctx* c, int iters, double* cost_trace, double* wall_seconds, dou
     stage_seconds[0] = total_ms * 1e-3;
     stage_seconds[1] = stage_seconds[2] = stage_seconds[3] = 0.0;
   }
+  return fb;
+  DFM_API_END
+}
+
+// ---- shard stepping API (host-side exchange of the V-update {num, den})
+int dfm_shard_begin(dfm_ctx* c, int iters) {
+  if (!c || iters < 1 || !c->has_obs || !c->has_model) return DFM_ERR_ARG;
+  DFM_API_BEGIN
+  DFM_CK(cudaSetDevice(c->device));
+  drop_graph(c);
+  c->host_exchange = true;
+  c->xs_iters = iters;
+  c->xs_iter = 0;
+  ensure_cost(c, iters + 1);
+  DFM_CK(cudaMemsetAsync(c->fallbacks.p, 0, sizeof(int), c->stream));
+  launch_spec(c);
+  launch_em(c, 1, 1, 0);
+  launch_rest(c, nullptr);  // stops after the partial V update
+  return DFM_OK;
+  DFM_API_END
+}
+
+int dfm_shard_numden(dfm_ctx* c, double* out) {
+  if (!c || !out || !c->host_exchange) return DFM_ERR_ARG;
+  DFM_API_BEGIN
+  c->numden.download(out, c->numden.n, c->stream);
+  DFM_CK(cudaStreamSynchronize(c->stream));
+  return DFM_OK;
+  DFM_API_END
+}
+
+int dfm_shard_advance(dfm_ctx* c, const double* in) {
+  if (!c || !in || !c->host_exchange) return DFM_ERR_ARG;
+  DFM_API_BEGIN
+  const size_t nkt = (size_t)c->N * c->K * c->T;
+  c->numden.upload(in, 2 * nkt, c->stream);
+  k_vapply<<<(unsigned)((nkt + 255) / 256), 256, 0, c->stream>>>(nkt, c->numden.p, c->V.p, c->floor_);
+  DFM_CK_LAUNCH();
+  c->launches++;
+  launch_spec(c);
+  const int i = ++c->xs_iter;
+  if (i < c->xs_iters) {
+    launch_em(c, 2, 1, i);
+    launch_rest(c, nullptr);
+    return 1;
+  }
+  launch_em(c, 2, 0, i);
+  return 0;
+  DFM_API_END
+}
+
+int dfm_shard_end(dfm_ctx* c, double* cost_trace_local) {
+  if (!c || !c->host_exchange) return DFM_ERR_ARG;
+  DFM_API_BEGIN
+  const int iters = c->xs_iters;
+  std::vector<double> part((size_t)(iters + 1) * c->F);
+  c->cost_part.download(part.data(), part.size(), c->stream);
+  int fb = 0;
+  c->fallbacks.download(&fb, 1, c->stream);
+  DFM_CK(cudaStreamSynchronize(c->stream));
+  c->host_exchange = false;
+  if (cost_trace_local)
+    for (int i = 0; i <= iters; ++i) {
+      double s = 0.0;
+      for (int f = 0; f < c->F; ++f) s += part[(size_t)i * c->F + f];
+      cost_trace_local[i] = s;
+    }
   return fb;
   DFM_API_END
 }

@@ -278,20 +278,22 @@ def test_eval_callback_chunks_match_single_run(dfm, oracle):
 
 
 @pytest.mark.slow
-def test_config1_trajectory_20_iterations(dfm, oracle):
+def test_config1_full_size_parity(dfm, oracle):
     """BASELINE config 1 at full size (B=3 x M_b=4, N=5, F=513, T=626, K=16):
-    20-iteration cost trajectory within 1e-8 of the oracle."""
+    the north_star bar - cost trajectory within 1e-8 relative over the first 20
+    iterations, cost non-increasing every iteration, and the separated STFTs
+    after 200 iterations within 1e-6 relative L2."""
     import os
 
     oracle.set_threads(os.cpu_count() or 1)
-    F, T, sizes, N, K = 513, 626, [4, 4, 4], 5, 16
+    F, T, sizes, N, K, iters = 513, 626, [4, 4, 4], 5, 16, 200
     layout = dfm.BlockLayout(sizes)
     x = dfm.generate_mixture(1, F, T, 12, N, K, 2605)
     init = dfm.random_init(F, T, layout, N, K, 19388)
-    fit = dfm.fit_distributed(x, layout, init, 20, True)
-    ref = oracle.run_engine(x, sizes, _init_dict(init), 20)
+    fit = dfm.fit_distributed(x, layout, init, iters, True)
+    ref = oracle.run_engine(x, sizes, _init_dict(init), iters)
     c, r = fit.report.cost_trace, ref["cost_trace"]
-    assert np.max(np.abs(c - r) / np.abs(r)) < TRAJ_RTOL
+    assert np.max(np.abs(c[:21] - r[:21]) / np.abs(r[:21])) < TRAJ_RTOL
     assert np.all(c[1:] <= c[:-1] + 1e-9 * np.abs(c[:-1]))
     img = dfm.wiener_block(x, fit.models, fit.spatial).images
     ref_img = oracle.wiener_block(x, sizes, ref)
@@ -319,3 +321,38 @@ def test_static_shape_kernels_match_generic_and_oracle(dfm, oracle, sizes, N, K)
         assert np.max(np.abs(cost - ref["cost_trace"]) / np.abs(ref["cost_trace"])) < TRAJ_RTOL
         assert _rel(nmf.V, ref["V"]) < 1e-7 and _rel(lam, ref["lam"]) < 1e-7
     assert np.max(np.abs(costs[0] - costs[1]) / np.abs(costs[1])) < TRAJ_RTOL
+
+
+@pytest.mark.parametrize("nshards", [2, 3])
+def test_frequency_sharded_engine_matches_single_gpu(dfm, oracle, nshards):
+    """SURVEY §8e on one device: bin-shard contexts run the real kernels in
+    lockstep and exchange the V-update {num, den} on the host (the GPU ranks
+    use ncclAllReduce).  The global trajectory and fitted model must match the
+    unsharded engine and the oracle."""
+    from paper_2605_19388_b200.sharding import fit_sharded_host, shard_bins
+
+    F, T, sizes, N, K, iters = 17, 48, [4, 4, 4], 5, 16, 12
+    layout = dfm.BlockLayout(sizes)
+    x = dfm.generate_mixture(1, F, T, layout.total, N, K, 21)
+    init = dfm.random_init(F, T, layout, N, K, 22)
+    engines = []
+    for r in range(nshards):
+        f0, f1 = shard_bins(F, nshards, r)
+        e = dfm.Engine(F, T, layout, N, K, f_begin=f0, f_end=f1)
+        e.set_obs(x[f0:f1])
+        e.set_model(init.nmf, init.w0, init.lambda0)
+        engines.append(e)
+    cost, fb = fit_sharded_host(engines, iters)
+    ref = oracle.run_engine(x, sizes, _init_dict(init), iters)
+    assert np.max(np.abs(cost - ref["cost_trace"]) / np.abs(ref["cost_trace"])) < TRAJ_RTOL
+    # V is identical on every shard; T / Lambda / W of each shard's bins match the oracle
+    Vs = [e.get_model()[0].V for e in engines]
+    for v in Vs[1:]:
+        assert np.array_equal(v, Vs[0])
+    assert _rel(Vs[0], ref["V"]) < 1e-7
+    for r, e in enumerate(engines):
+        f0, f1 = shard_bins(F, nshards, r)
+        nmf, wb, lam = e.get_model()
+        assert _rel(nmf.T[:, f0:f1], ref["T"][:, f0:f1]) < 1e-7
+        assert _rel(lam[f0:f1], ref["lam"][f0:f1]) < 1e-7
+        e.close()
