@@ -211,7 +211,8 @@ def run_reference(args, c, world, rank):
     return {
         "metric": "dFastMNMF EM TF-bin*iter/s (BASELINE config 1)", "value": value, "unit": "TF-bin*iter/s",
         "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.workload, **{k: c[k] for k in ("F", "T", "sizes", "N", "K")}},
         "cpu_baseline": {"value": value, "unit": "TF-bin*iter/s", "cores": threads, "kind": "port",

@@ -356,3 +356,20 @@ def test_frequency_sharded_engine_matches_single_gpu(dfm, oracle, nshards):
         assert _rel(nmf.T[:, f0:f1], ref["T"][:, f0:f1]) < 1e-7
         assert _rel(lam[f0:f1], ref["lam"][f0:f1]) < 1e-7
         e.close()
+
+
+def test_binding_mirror_fit_is_monotone(dfm):
+    # proj/python/tests/test_smoke.py:40-48 through the _fastmnmf mirror
+    from paper_2605_19388_b200 import _fastmnmf
+
+    rng = np.random.default_rng(3)
+    x = (rng.standard_normal((16, 48, 4)) + 1j * rng.standard_normal((16, 48, 4))) / np.sqrt(2)
+    report = _fastmnmf.fit_distributed(x, partition=[2, 2], n_sources=2, k_bases=4, iterations=15, seed=5)
+    trace = np.asarray(report["cost_trace"])
+    assert trace.shape == (16,)
+    assert np.all(np.diff(trace) <= 1e-9 * np.abs(trace[:-1]))
+    assert set(report) == {"cost_trace", "wall_seconds", "iterations", "stages"}
+    full = _fastmnmf.fit_full(x, n_sources=2, k_bases=4, iterations=5, seed=1)
+    assert len(full["cost_trace"]) == 6
+    with pytest.raises(ValueError):
+        _fastmnmf.fit_full(np.zeros((3, 4)), n_sources=2)
