@@ -351,6 +351,18 @@ def main():
             pg.destroy_process_group()
         return
 
+    # Wiener separation (wiener.cpp:50-69) on the fitted model: HBM-bound,
+    # reads X once and writes N images (16 F T M (1 + N) bytes)
+    import ctypes as _ct
+
+    w_ms = []
+    for _ in range(5):
+        dfm._capi.check(lib.dfm_l2_flush(local))
+        v = _ct.c_double()
+        dfm._capi.check(lib.dfm_bench_wiener(ctx, _ct.byref(v)))
+        w_ms.append(v.value)
+    w_ms = float(np.median(w_ms[1:]))
+    w_bytes = 16.0 * (f1 - f0) * T * M * (1 + N)
     pk = peaks()
     split_avg = np.mean(np.array(split), axis=0)
     names = ["k_em_bin", "k_tupd", "k_pd", "k_vupd", "k_spec"]
@@ -387,6 +399,8 @@ def main():
                           "peak_source": "measured in this run (DFMA microbenchmark, dfm_probe_fp64_tflops)"},
         "iteration_roofline": {"alg_bytes_per_iter": alg_bytes(c), "hbm_frac": alg_bytes(c) / (ms_step * 1e-3) / 1e9 / pk["hbm_gbs"]},
         "kernel_split_ms": {n: float(v) for n, v in zip(names, split_avg)},
+        "wiener": {"ms": w_ms, "alg_bytes": w_bytes, "achieved_gbs": w_bytes / (w_ms * 1e-3) / 1e9,
+                   "frac_hbm": w_bytes / (w_ms * 1e-3) / 1e9 / pk["hbm_gbs"]},
         "dominant_kernel": names[dom],
         "e2e": {"value": e2e_value, "unit": "TF-bin*iter/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h),

@@ -148,6 +148,8 @@ int dfm_get_tiling(const dfm_ctx* ctx, int* bins_per_cta, int* cluster_size, int
  * current model (wiener_block, wiener.cpp:50-69, shared spectrograms).
  * images: [N][F_local][T][M] complex128. */
 int dfm_wiener(dfm_ctx* ctx, double* images);
+/* Device time (ms) of the Wiener separation into a device-resident buffer. */
+int dfm_bench_wiener(dfm_ctx* ctx, double* ms);
 
 /* ------------------------------------------------- stateless per-update API
  * Each call uploads its inputs, runs the step kernels once and downloads the

@@ -49,6 +49,7 @@ _SIGS = {
     "dfm_set_trace": (_i, [_vp, _i]),
     "dfm_get_trace": (_i, [_vp, _vp, _i]),
     "dfm_wiener": (_i, [_vp, _vp]),
+    "dfm_bench_wiener": (_i, [_vp, _dp]),
     "dfm_step_spectrogram": (_i, [_i, _i, _i, _i, _vp, _vp, _vp]),
     "dfm_step_eta": (_i, [_i, _i, _i, _i, _vp, _vp, _d, _vp]),
     "dfm_step_decorrelate": (_i, [_i, _i, _i, _vp, _i, _i, _vp, _vp, _vp]),

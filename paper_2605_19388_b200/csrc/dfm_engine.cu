@@ -826,6 +826,29 @@ int dfm_get_tiling(const dfm_ctx* c, int* frame_tile, int* pd_frames, int* ctas,
   return DFM_OK;
 }
 
+// Device-timed Wiener separation into a context-owned image buffer (bench).
+int dfm_bench_wiener(dfm_ctx* c, double* ms_out) {
+  if (!c) return DFM_ERR_ARG;
+  DFM_API_BEGIN
+  DFM_CK(cudaSetDevice(c->device));
+  const int F = c->F, T = c->T, N = c->N, K = c->K, M = c->M;
+  static thread_local DBuf<cd>* img = nullptr;
+  const size_t need = (size_t)N * F * T * M;
+  if (!img) img = new DBuf<cd>();
+  if (img->n < need) img->alloc(need);
+  ModelView mv{c->Tf.p, K, (long long)N * K, 1, c->V.p, (long long)K * T, T, 1,
+               c->lam.p, (long long)N * M, M, 1};
+  DFM_CK(cudaEventRecord(c->ev[0], c->stream));
+  launch_wiener(c->L, F, T, N, K, c->x.p, mv, c->W.p, c->L.wsz, c->floor_, img->p, c->stream, &c->launches);
+  DFM_CK(cudaEventRecord(c->ev[5], c->stream));
+  DFM_CK(cudaEventSynchronize(c->ev[5]));
+  float ms = 0.f;
+  DFM_CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[5]));
+  if (ms_out) *ms_out = ms;
+  return DFM_OK;
+  DFM_API_END
+}
+
 int dfm_wiener(dfm_ctx* c, double* images) {
   if (!c || !images) return DFM_ERR_ARG;
   DFM_API_BEGIN
