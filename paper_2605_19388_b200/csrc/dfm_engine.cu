@@ -98,6 +98,7 @@ struct dfm_ctx {
   cudaStream_t stream = nullptr;
   DBuf<cd> x, W;
   DBuf<double> Tf, V, lam, H, Aw, Bw, numden, cost_part, cost_sum, cost_step;
+  DBuf<cd> Ginv;  // (W^H)^-1 per (bin, block) for the Wiener filter
   DBuf<int> fallbacks;
   int maxmb = 4;
   int kmaxmb = 4;  // MAXMB of the selected instantiations
@@ -836,10 +837,13 @@ int dfm_bench_wiener(dfm_ctx* c, double* ms_out) {
   const size_t need = (size_t)N * F * T * M;
   if (!img) img = new DBuf<cd>();
   if (img->n < need) img->alloc(need);
-  ModelView mv{c->Tf.p, K, (long long)N * K, 1, c->V.p, (long long)K * T, T, 1,
+  ModelView mv{c->H.p, c->Tf.p, K, (long long)N * K, 1, c->V.p, (long long)K * T, T, 1,
                c->lam.p, (long long)N * M, M, 1};
+  if (c->Ginv.n < (size_t)F * c->L.wsz) c->Ginv.alloc((size_t)F * c->L.wsz);
   DFM_CK(cudaEventRecord(c->ev[0], c->stream));
-  launch_wiener(c->L, F, T, N, K, c->x.p, mv, c->W.p, c->L.wsz, c->floor_, img->p, c->stream, &c->launches);
+  launch_spec(c);  // H = T V of the current model
+  launch_wiener(c->L, F, T, N, K, c->x.p, mv, c->W.p, c->L.wsz, c->floor_, img->p, c->stream, &c->launches,
+                c->Ginv.p);
   DFM_CK(cudaEventRecord(c->ev[5], c->stream));
   DFM_CK(cudaEventSynchronize(c->ev[5]));
   float ms = 0.f;
@@ -855,9 +859,12 @@ int dfm_wiener(dfm_ctx* c, double* images) {
   DFM_CK(cudaSetDevice(c->device));
   const int F = c->F, T = c->T, N = c->N, K = c->K, M = c->M;
   DBuf<cd> img((size_t)N * F * T * M);
-  ModelView mv{c->Tf.p, K, (long long)N * K, 1, c->V.p, (long long)K * T, T, 1,
+  ModelView mv{c->H.p, c->Tf.p, K, (long long)N * K, 1, c->V.p, (long long)K * T, T, 1,
                c->lam.p, (long long)N * M, M, 1};
-  launch_wiener(c->L, F, T, N, K, c->x.p, mv, c->W.p, c->L.wsz, c->floor_, img.p, c->stream, &c->launches);
+  if (c->Ginv.n < (size_t)F * c->L.wsz) c->Ginv.alloc((size_t)F * c->L.wsz);
+  launch_spec(c);  // H = T V of the current model
+  launch_wiener(c->L, F, T, N, K, c->x.p, mv, c->W.p, c->L.wsz, c->floor_, img.p, c->stream, &c->launches,
+                c->Ginv.p);
   img.download((cd*)images, img.n, c->stream);
   DFM_CK(cudaStreamSynchronize(c->stream));
   return DFM_OK;

@@ -61,6 +61,7 @@ struct DBuf {
 // Strided views used by the Wiener kernel so one kernel serves both the
 // Eigen-ordered step buffers and the engine's device layouts.
 struct ModelView {
+  const double* H;  // optional precomputed spectrogram [F][N][T] (else T V per frame)
   const double* Tm;
   long long sTn, sTf, sTk;  // T(n, f, k)
   const double* V;
@@ -79,8 +80,10 @@ struct Layout {
 bool make_layout(int nb, const int* sizes, Layout& L);
 
 // Wiener separation over bins [0, F) with W stored as wb(f) = W + f*wstride + woff[b].
+// G: optional caller-owned scratch of F * wsz complex values for (W^H)^-1
+// (allocated per call when null); the call does not synchronise.
 void launch_wiener(const Layout& L, int F, int T, int N, int K, const cd* x, const ModelView& mv,
                    const cd* W, long long wstride, double floor_, cd* images, cudaStream_t s,
-                   long long* launches);
+                   long long* launches, cd* G = nullptr);
 
 }  // namespace dfm

@@ -322,9 +322,14 @@ __global__ void __launch_bounds__(128) k_wiener(int F, int T, int N, int K, Layo
 #pragma unroll
   for (int n = 0; n < MAXN; ++n) {
     double s = 0.0;
-    if (n < N)
-      for (int k = 0; k < K; ++k)
-        s += mv.Tm[n * mv.sTn + f * mv.sTf + k * mv.sTk] * mv.V[n * mv.sVn + k * mv.sVk + j * mv.sVt];
+    if (n < N) {
+      if (mv.H) {
+        s = __ldg(mv.H + ((size_t)f * N + n) * T + j);
+      } else {
+        for (int k = 0; k < K; ++k)
+          s += mv.Tm[n * mv.sTn + f * mv.sTf + k * mv.sTk] * mv.V[n * mv.sVn + k * mv.sVk + j * mv.sVt];
+      }
+    }
     h[n] = s;
   }
   const cd* xj = x + ((size_t)f * T + j) * L.M;
@@ -366,22 +371,27 @@ static inline unsigned nblk(long long n, int b) { return (unsigned)((n + b - 1) 
 
 void launch_wiener(const Layout& L, int F, int T, int N, int K, const cd* x, const ModelView& mv,
                    const cd* W, long long wstride, double floor_, cd* images, cudaStream_t s,
-                   long long* launches) {
-  DBuf<cd> G((size_t)F * L.wsz);
-  k_wh_inverse<<<nblk((long long)F * L.nb, 128), 128, 0, s>>>(F, L, W, wstride, G.p);
+                   long long* launches, cd* Gbuf) {
+  DBuf<cd> Gown;
+  cd* G = Gbuf;
+  if (!G) {
+    Gown.alloc((size_t)F * L.wsz);
+    G = Gown.p;
+  }
+  k_wh_inverse<<<nblk((long long)F * L.nb, 128), 128, 0, s>>>(F, L, W, wstride, G);
   DFM_CK_LAUNCH();
   const unsigned grid = nblk((long long)F * T, 128);
   if (N <= 8)
-    k_wiener<8><<<grid, 128, 0, s>>>(F, T, N, K, L, x, mv, W, wstride, G.p, floor_, images);
+    k_wiener<8><<<grid, 128, 0, s>>>(F, T, N, K, L, x, mv, W, wstride, G, floor_, images);
   else if (N <= 32)
-    k_wiener<32><<<grid, 128, 0, s>>>(F, T, N, K, L, x, mv, W, wstride, G.p, floor_, images);
+    k_wiener<32><<<grid, 128, 0, s>>>(F, T, N, K, L, x, mv, W, wstride, G, floor_, images);
   else {
     set_error("wiener: more than 32 sources is unsupported");
     throw CudaError{DFM_ERR_UNSUPPORTED};
   }
   DFM_CK_LAUNCH();
   if (launches) *launches += 2;
-  DFM_CK(cudaStreamSynchronize(s));
+  if (!Gbuf) DFM_CK(cudaStreamSynchronize(s));  // Gown is freed on return
 }
 
 // ------------------------------------------------------------ probes
@@ -702,7 +712,7 @@ int dfm_step_wiener(int F, int T, int nblocks, const int* block_sizes, int N, in
     dw.upload(wbin.data(), wbin.size());
     DFM_CK(cudaDeviceSynchronize());
   }
-  ModelView mv{dT.p, (long long)K * F, 1, F, dV.p, (long long)T * K, 1, K, dl.p, (long long)M * N, 1, N};
+  ModelView mv{nullptr, dT.p, (long long)K * F, 1, F, dV.p, (long long)T * K, 1, K, dl.p, (long long)M * N, 1, N};
   launch_wiener(L, F, T, N, K, dx.p, mv, dw.p, L.wsz, floor_, dimg.p, 0, nullptr);
   dimg.download((cd*)images, dimg.n);
   DFM_CK(cudaDeviceSynchronize());
