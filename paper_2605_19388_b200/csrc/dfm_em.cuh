@@ -886,3 +886,125 @@ __global__ void __launch_bounds__(128, 6) k_pdw(const EmArgs a) {
 }
 
 }  // namespace dfm
+
+namespace dfm {
+// Wiener separation for the engine context (wiener.cpp:11-34 per block):
+// c_n = (W_b^H)^-1 (g_n .* (W_b^H x^b)), g_n,m = h_n Lambda(n, m) / max(h Lambda, floor).
+// CTA = (128 frames, bin); W, (W^H)^-1 and Lambda of the bin in shared memory,
+// h from H; every per-frame value in registers; each source's image tile is
+// staged in shared memory and written with coalesced 16-byte stores.
+constexpr int kWienFT = 128;
+template <int MB_, int NB_, int NS_, int MAXMB>
+__global__ void __launch_bounds__(kWienFT) k_wiener_ctx(const EmArgs a, const cd* __restrict__ G,
+                                                        cd* __restrict__ images) {
+  constexpr bool SB = MB_ > 0 && NB_ > 0;
+  extern __shared__ __align__(16) unsigned char swn[];
+  const int M = SB ? MB_ * NB_ : a.M;
+  const int nb = SB ? NB_ : a.nb;
+  const int N = NS_ > 0 ? NS_ : a.N;
+  const int T = a.T;
+  const int wsz = SB ? MB_ * MB_ * NB_ : a.wsz;
+  auto MBof = [&](int b) { return SB ? MB_ : a.mb[b]; };
+  auto OFF = [&](int b) { return SB ? b * MB_ : a.off[b]; };
+  auto WOFF = [&](int b) { return SB ? b * MB_ * MB_ : a.woff[b]; };
+  cd* Ws = (cd*)swn;             // [wsz]
+  cd* Gs = Ws + wsz;             // [wsz]
+  cd* stage = Gs + wsz;          // [FT][M]
+  double* Ls = (double*)(stage + (size_t)kWienFT * M);  // [N][M]
+  const int f = blockIdx.y, t0 = blockIdx.x * kWienFT, tid = threadIdx.x;
+  const int tn = min(kWienFT, T - t0);
+  for (int e = tid; e < wsz; e += kWienFT) {
+    Ws[e] = a.W[(size_t)f * wsz + e];
+    Gs[e] = G[(size_t)f * wsz + e];
+  }
+  for (int e = tid; e < N * M; e += kWienFT) Ls[e] = a.lam[(size_t)f * N * M + e];
+  __syncthreads();
+  const int t = t0 + tid;
+  const bool act = tid < tn;
+  double h[kMaxN];
+  constexpr int MX = SB ? MB_ * NB_ : 1;
+  cd y[MX];
+  double eta[MX];
+  if (act) {
+#pragma unroll
+    for (int n = 0; n < kMaxN; ++n) h[n] = n < N ? __ldg(a.H + ((size_t)f * N + n) * T + t) : 0.0;
+    if constexpr (SB) {
+      const cd* xt = a.x + ((size_t)f * T + t) * M;
+      cd xv[MX];
+#pragma unroll
+      for (int m = 0; m < MX; ++m) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(xt + m));
+        xv[m] = cd{v.x, v.y};
+      }
+#pragma unroll
+      for (int b = 0; b < NB_; ++b)
+#pragma unroll
+        for (int mu = 0; mu < MB_; ++mu) {
+          cd s{0.0, 0.0};
+#pragma unroll
+          for (int q = 0; q < MB_; ++q) s = s + cmulc(Ws[b * MB_ * MB_ + mu * MB_ + q], xv[b * MB_ + q]);
+          y[b * MB_ + mu] = s;
+          double e = 0.0;
+#pragma unroll
+          for (int n = 0; n < kMaxN; ++n)
+            if (n < N) e += h[n] * Ls[n * M + b * MB_ + mu];
+          eta[b * MB_ + mu] = fmax(e, a.floor_);
+        }
+    }
+  }
+  for (int n = 0; n < N; ++n) {
+    if (act) {
+      if constexpr (SB) {
+#pragma unroll
+        for (int b = 0; b < NB_; ++b) {
+          cd sc[MB_];
+#pragma unroll
+          for (int mu = 0; mu < MB_; ++mu) {
+            const double gain = (h[n] * Ls[n * M + b * MB_ + mu]) / eta[b * MB_ + mu];
+            sc[mu] = y[b * MB_ + mu] * gain;
+          }
+          const cd* gb = Gs + b * MB_ * MB_;
+#pragma unroll
+          for (int r = 0; r < MB_; ++r) {
+            cd s{0.0, 0.0};
+#pragma unroll
+            for (int c = 0; c < MB_; ++c) s = s + gb[c * MB_ + r] * sc[c];
+            stage[tid * M + b * MB_ + r] = s;
+          }
+        }
+      } else {
+        // generic layouts: per block, recompute y and eta (no register arrays)
+        const cd* xt = a.x + ((size_t)f * T + t) * M;
+        for (int b = 0; b < nb; ++b) {
+          const int mb = MBof(b), off = OFF(b);
+          const cd* wb = Ws + WOFF(b);
+          const cd* gb = Gs + WOFF(b);
+          for (int r = 0; r < mb; ++r) {
+            cd s{0.0, 0.0};
+            for (int c = 0; c < mb; ++c) {
+              cd yc{0.0, 0.0};
+              for (int q = 0; q < mb; ++q) {
+                const double2 v = __ldg(reinterpret_cast<const double2*>(xt + off + q));
+                yc = yc + cmulc(wb[c * mb + q], cd{v.x, v.y});
+              }
+              double e = 0.0;
+              for (int nn = 0; nn < N; ++nn) e += h[nn] * Ls[nn * M + off + c];
+              const double gain = (h[n] * Ls[n * M + off + c]) / fmax(e, a.floor_);
+              s = s + gb[c * mb + r] * (yc * gain);
+            }
+            stage[tid * M + off + r] = s;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // coalesced copy of the tile (tn frames x M, contiguous in images)
+    cd* dst = images + (((size_t)n * a.F + f) * T + t0) * M;
+    for (int e = tid; e < tn * M; e += kWienFT) {
+      const cd v = stage[e];
+      *reinterpret_cast<double2*>(dst + e) = make_double2(v.re, v.im);
+    }
+    __syncthreads();
+  }
+}
+}  // namespace dfm

@@ -104,6 +104,7 @@ struct dfm_ctx {
   int kmaxmb = 4;  // MAXMB of the selected instantiations
   void (*kem)(EmArgs) = nullptr;
   void (*kpdw)(EmArgs) = nullptr;
+  void (*kwien)(EmArgs, const cd*, cd*) = nullptr;
   bool force_generic = false;
   int FT = 128, TB = 128, smem_em = 0;
   int req_FT = 0, req_TB = 0;
@@ -175,20 +176,20 @@ void select_kernels(dfm_ctx* c) {
   c->kem = nullptr;
   if (uniform && !c->force_generic) {
     if (mb == 4 && nb == 3 && N == 5 && K == 16) {
-      c->kem = k_em_bin<4, 3, 5, 4>; c->kpdw = k_pdw<4, 3, 5, 4>; c->kmaxmb = 4;
+      c->kem = k_em_bin<4, 3, 5, 4>; c->kpdw = k_pdw<4, 3, 5, 4>; c->kwien = k_wiener_ctx<4, 3, 5, 4>; c->kmaxmb = 4;
     } else if (mb == 2 && nb == 2 && N == 3 && K == 4) {
-      c->kem = k_em_bin<2, 2, 3, 2>; c->kpdw = k_pdw<2, 2, 3, 2>; c->kmaxmb = 2;
+      c->kem = k_em_bin<2, 2, 3, 2>; c->kpdw = k_pdw<2, 2, 3, 2>; c->kwien = k_wiener_ctx<2, 2, 3, 2>; c->kmaxmb = 2;
     } else if (mb == 4 && nb == 8 && N == 8 && K == 32) {
-      c->kem = k_em_bin<4, 8, 8, 4>; c->kpdw = k_pdw<4, 8, 8, 4>; c->kmaxmb = 4;
+      c->kem = k_em_bin<4, 8, 8, 4>; c->kpdw = k_pdw<4, 8, 8, 4>; c->kwien = k_wiener_ctx<4, 8, 8, 4>; c->kmaxmb = 4;
     } else if (mb == 12 && nb == 1 && N == 5 && K == 16) {
-      c->kem = k_em_bin<12, 1, 5, 12>; c->kpdw = k_pdw<12, 1, 5, 12>; c->kmaxmb = 12;
+      c->kem = k_em_bin<12, 1, 5, 12>; c->kpdw = k_pdw<12, 1, 5, 12>; c->kwien = k_wiener_ctx<12, 1, 5, 12>; c->kmaxmb = 12;
     }
   }
   if (!c->kem) {
     if (c->maxmb <= 4) {
-      c->kem = k_em_bin<0, 0, 0, 4>; c->kpdw = k_pdw<0, 0, 0, 4>; c->kmaxmb = 4;
+      c->kem = k_em_bin<0, 0, 0, 4>; c->kpdw = k_pdw<0, 0, 0, 4>; c->kwien = k_wiener_ctx<0, 0, 0, 4>; c->kmaxmb = 4;
     } else {
-      c->kem = k_em_bin<0, 0, 0, DFM_MAX_MB>; c->kpdw = k_pdw<0, 0, 0, DFM_MAX_MB>; c->kmaxmb = DFM_MAX_MB;
+      c->kem = k_em_bin<0, 0, 0, DFM_MAX_MB>; c->kpdw = k_pdw<0, 0, 0, DFM_MAX_MB>; c->kwien = k_wiener_ctx<0, 0, 0, DFM_MAX_MB>; c->kmaxmb = DFM_MAX_MB;
     }
   }
 }
@@ -366,6 +367,21 @@ void run_step(dfm_ctx* c, bool split) {
   if (split) DFM_CK(cudaEventRecord(c->ev[1], c->stream));
   launch_rest(c, split ? c->ev : nullptr);
   if (split) DFM_CK(cudaEventRecord(c->ev[5], c->stream));
+}
+
+// Wiener separation of the context's bins into the device buffer `img`
+// [N][F][T][M]: (W^H)^-1 per (bin, block), H = T V, then k_wiener_ctx.
+void launch_wiener_ctx(dfm_ctx* c, cd* img) {
+  if (c->Ginv.n < (size_t)c->F * c->L.wsz) c->Ginv.alloc((size_t)c->F * c->L.wsz);
+  launch_wh_inverse(c->F, c->L, c->W.p, c->L.wsz, c->Ginv.p, c->stream);
+  launch_spec(c);
+  const size_t smem = (size_t)(2 * c->L.wsz + kWienFT * c->M) * sizeof(cd) + (size_t)c->N * c->M * 8;
+  DFM_CK(cudaFuncSetAttribute(c->kwien, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const EmArgs a = make_args(c);
+  const dim3 grid((c->T + kWienFT - 1) / kWienFT, c->F);
+  c->kwien<<<grid, kWienFT, smem, c->stream>>>(a, c->Ginv.p, img);
+  DFM_CK_LAUNCH();
+  c->launches += 3;
 }
 
 }  // namespace
@@ -837,13 +853,8 @@ int dfm_bench_wiener(dfm_ctx* c, double* ms_out) {
   const size_t need = (size_t)N * F * T * M;
   if (!img) img = new DBuf<cd>();
   if (img->n < need) img->alloc(need);
-  ModelView mv{c->H.p, c->Tf.p, K, (long long)N * K, 1, c->V.p, (long long)K * T, T, 1,
-               c->lam.p, (long long)N * M, M, 1};
-  if (c->Ginv.n < (size_t)F * c->L.wsz) c->Ginv.alloc((size_t)F * c->L.wsz);
   DFM_CK(cudaEventRecord(c->ev[0], c->stream));
-  launch_spec(c);  // H = T V of the current model
-  launch_wiener(c->L, F, T, N, K, c->x.p, mv, c->W.p, c->L.wsz, c->floor_, img->p, c->stream, &c->launches,
-                c->Ginv.p);
+  launch_wiener_ctx(c, img->p);
   DFM_CK(cudaEventRecord(c->ev[5], c->stream));
   DFM_CK(cudaEventSynchronize(c->ev[5]));
   float ms = 0.f;
@@ -859,12 +870,7 @@ int dfm_wiener(dfm_ctx* c, double* images) {
   DFM_CK(cudaSetDevice(c->device));
   const int F = c->F, T = c->T, N = c->N, K = c->K, M = c->M;
   DBuf<cd> img((size_t)N * F * T * M);
-  ModelView mv{c->H.p, c->Tf.p, K, (long long)N * K, 1, c->V.p, (long long)K * T, T, 1,
-               c->lam.p, (long long)N * M, M, 1};
-  if (c->Ginv.n < (size_t)F * c->L.wsz) c->Ginv.alloc((size_t)F * c->L.wsz);
-  launch_spec(c);  // H = T V of the current model
-  launch_wiener(c->L, F, T, N, K, c->x.p, mv, c->W.p, c->L.wsz, c->floor_, img.p, c->stream, &c->launches,
-                c->Ginv.p);
+  launch_wiener_ctx(c, img.p);
   img.download((cd*)images, img.n, c->stream);
   DFM_CK(cudaStreamSynchronize(c->stream));
   return DFM_OK;

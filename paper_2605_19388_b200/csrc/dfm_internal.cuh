@@ -86,4 +86,7 @@ void launch_wiener(const Layout& L, int F, int T, int N, int K, const cd* x, con
                    const cd* W, long long wstride, double floor_, cd* images, cudaStream_t s,
                    long long* launches, cd* G = nullptr);
 
+// (W_b^H)^-1 per (bin, block) into G [F][wsz] (wiener.cpp:25).
+void launch_wh_inverse(int F, const Layout& L, const cd* W, long long wstride, cd* G, cudaStream_t s);
+
 }  // namespace dfm

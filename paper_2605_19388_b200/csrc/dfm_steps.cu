@@ -394,6 +394,11 @@ void launch_wiener(const Layout& L, int F, int T, int N, int K, const cd* x, con
   if (!Gbuf) DFM_CK(cudaStreamSynchronize(s));  // Gown is freed on return
 }
 
+void launch_wh_inverse(int F, const Layout& L, const cd* W, long long wstride, cd* G, cudaStream_t s) {
+  k_wh_inverse<<<nblk((long long)F * L.nb, 128), 128, 0, s>>>(F, L, W, wstride, G);
+  DFM_CK_LAUNCH();
+}
+
 // ------------------------------------------------------------ probes
 __global__ void k_fp64_probe(double* out, int iters) {
   double a0 = threadIdx.x * 1e-9, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,
