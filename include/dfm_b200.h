@@ -138,6 +138,9 @@ int dfm_set_tiling(dfm_ctx* ctx, int bins_per_cta, int cluster_size);
  * per-bin kernel (16 slots per CTA).  dfm_set_trace returns the buffer length. */
 int dfm_set_trace(dfm_ctx* ctx, int on);
 int dfm_get_trace(dfm_ctx* ctx, unsigned long long* out, int n);
+/* Timing experiments only (results become wrong): bit0 skips the Lambda
+ * frame reduction, bit1 the Q accumulation of the per-bin kernel. */
+int dfm_debug_bits(dfm_ctx* ctx, int bits);
 /* Use the generic (runtime-shape) bin kernel even when a compile-time-shape
  * instantiation matches the layout (A/B testing of the two code paths). */
 int dfm_force_generic(dfm_ctx* ctx, int on);

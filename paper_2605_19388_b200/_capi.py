@@ -46,6 +46,7 @@ _SIGS = {
     "dfm_set_tiling": (_i, [_vp, _i, _i]),
     "dfm_get_tiling": (_i, [_vp, _ip, _ip, _ip, _ip, _ip]),
     "dfm_force_generic": (_i, [_vp, _i]),
+    "dfm_debug_bits": (_i, [_vp, _i]),
     "dfm_set_trace": (_i, [_vp, _i]),
     "dfm_get_trace": (_i, [_vp, _vp, _i]),
     "dfm_wiener": (_i, [_vp, _vp]),

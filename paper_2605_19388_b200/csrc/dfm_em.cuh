@@ -34,6 +34,8 @@ struct EmArgs {
   int finish;  // 1 = cost only (first launch), 2 = Lambda update + cost
   int start;   // 1 = Q, IP, T-update weights
   unsigned long long* trace;  // optional [bin][16] phase stamps
+  int dbg;                    // timing experiments only: bit0 no Lambda reduction, bit1 no Q accumulation,
+                              // bit2 no per-frame arithmetic in passes A/B
 };
 
 struct EmPlan {
@@ -235,7 +237,8 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
       // (N x frames) (frames x M) on the FP64 tensor cores: warp job = (column
       // tile of 8 mics, num|den), accumulated over k-steps of 4 frames and over
       // tiles in registers.  Fallback: SIMT (n, m) units.
-      if (use_mma) {
+      if (a.dbg & 1) {
+      } else if (use_mma) {
 #pragma unroll
         for (int jj = 0; jj < kLamJobs; ++jj) {
           const int job = warp + jj * nwarps;
@@ -243,15 +246,20 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
             const int j = job >> 1;
             const double* brow = (job & 1) ? is : zs;
             const int m = 8 * j + g;
-            double c0 = lj0[jj], c1 = lj1[jj];
-            for (int t0 = 0; t0 < tn; t0 += 4) {
-              const int t = t0 + q;
+            // two independent accumulator chains (even / odd k-steps), added at
+            // the end of the tile in a fixed order
+            double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
+            for (int t0 = 0; t0 < tn; t0 += 8) {
+              const int t = t0 + q, u = t0 + 4 + q;
               const double av = (g < N && t < tn) ? hs[g * FTp + t] : 0.0;
               const double bv = (m < M && t < tn) ? brow[m * FTp + t] : 0.0;
+              const double au = (g < N && u < tn) ? hs[g * FTp + u] : 0.0;
+              const double bu = (m < M && u < tn) ? brow[m * FTp + u] : 0.0;
               dmma(c0, c1, av, bv);
+              dmma(d0, d1, au, bu);
             }
-            lj0[jj] = c0;
-            lj1[jj] = c1;
+            lj0[jj] += c0 + d0;
+            lj1[jj] += c1 + d1;
           }
         }
       } else
@@ -381,7 +389,7 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
       if (a.start) {
         __syncthreads();
         // (block, entry r<=c) units accumulate all mu of their block
-        for (int u = tid; u < nitems * SQ; u += FT) {
+        for (int u = tid; u < ((a.dbg & 2) ? 0 : nitems * SQ); u += FT) {
           const int qitem = u % nitems, qs = u / nitems;
           int rem = qitem, qb_ = 0, qr, qc;
           if constexpr (SB) {
@@ -637,13 +645,16 @@ __global__ void __launch_bounds__(32 * kTupdWarps) k_tupd_mma(int F, int T, int 
   const int steps = (T + 3) / 4;
   const int per = (steps + kTupdWarps - 1) / kTupdWarps;
   const int s0 = warp * per, s1 = min(steps, s0 + per);
+  constexpr int U = 4;  // k-steps per batch, each with its own accumulator chain
   double num[KT][2], den[KT][2];
+  double cn[U][KT][2], cd_[U][KT][2];
 #pragma unroll
-  for (int j = 0; j < KT; ++j) num[j][0] = num[j][1] = den[j][0] = den[j][1] = 0.0;
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int j = 0; j < KT; ++j) cn[u][j][0] = cn[u][j][1] = cd_[u][j][0] = cd_[u][j][1] = 0.0;
   const int f = f0 + g;
   const double* ar = Aw + ((size_t)n * F + (f < F ? f : 0)) * T;
   const double* br = Bw + ((size_t)n * F + (f < F ? f : 0)) * T;
-  constexpr int U = 4;  // k-steps whose operands are loaded before their DMMAs
   for (int sb = s0; sb < s1; sb += U) {
     double av[U], bv[U], vb[U][KT];
 #pragma unroll
@@ -663,10 +674,17 @@ __global__ void __launch_bounds__(32 * kTupdWarps) k_tupd_mma(int F, int T, int 
 #pragma unroll
       for (int j = 0; j < KT; ++j)
         if (j < kt) {
-          dmma(num[j][0], num[j][1], av[u], vb[u][j]);
-          dmma(den[j][0], den[j][1], bv[u], vb[u][j]);
+          dmma(cn[u][j][0], cn[u][j][1], av[u], vb[u][j]);
+          dmma(cd_[u][j][0], cd_[u][j][1], bv[u], vb[u][j]);
         }
   }
+#pragma unroll
+  for (int j = 0; j < KT; ++j)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      num[j][i] = (cn[0][j][i] + cn[1][j][i]) + (cn[2][j][i] + cn[3][j][i]);
+      den[j][i] = (cd_[0][j][i] + cd_[1][j][i]) + (cd_[2][j][i] + cd_[3][j][i]);
+    }
   // fixed-order tree over the warps: w += w + h for h = W/2, W/4, ..., 1
 #pragma unroll
   for (int h = kTupdWarps / 2; h >= 1; h >>= 1) {
@@ -723,11 +741,14 @@ __global__ void __launch_bounds__(32 * kVupdMWarps) k_vupd_mma(int F, int T, int
   const int steps = (F + 3) / 4;
   const int per = (steps + kVupdMWarps - 1) / kVupdMWarps;
   const int s0 = warp * per, s1 = min(steps, s0 + per);
+  constexpr int U = 4;  // k-steps per batch, each with its own accumulator chain
   double num[KT][2], den[KT][2];
+  double cn[U][KT][2], cd_[U][KT][2];
 #pragma unroll
-  for (int j = 0; j < KT; ++j) num[j][0] = num[j][1] = den[j][0] = den[j][1] = 0.0;
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int j = 0; j < KT; ++j) cn[u][j][0] = cn[u][j][1] = cd_[u][j][0] = cd_[u][j][1] = 0.0;
   const int tb = t0 + g;
-  constexpr int U = 4;
   for (int sb = s0; sb < s1; sb += U) {
     double av[U], bv[U], ta[U][KT];
 #pragma unroll
@@ -747,10 +768,17 @@ __global__ void __launch_bounds__(32 * kVupdMWarps) k_vupd_mma(int F, int T, int
 #pragma unroll
       for (int j = 0; j < KT; ++j)
         if (j < kt) {
-          dmma(num[j][0], num[j][1], ta[u][j], av[u]);
-          dmma(den[j][0], den[j][1], ta[u][j], bv[u]);
+          dmma(cn[u][j][0], cn[u][j][1], ta[u][j], av[u]);
+          dmma(cd_[u][j][0], cd_[u][j][1], ta[u][j], bv[u]);
         }
   }
+#pragma unroll
+  for (int j = 0; j < KT; ++j)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      num[j][i] = (cn[0][j][i] + cn[1][j][i]) + (cn[2][j][i] + cn[3][j][i]);
+      den[j][i] = (cd_[0][j][i] + cd_[1][j][i]) + (cd_[2][j][i] + cd_[3][j][i]);
+    }
   // fixed-order tree over the warps: w += w + h for h = W/2, W/4, ..., 1
 #pragma unroll
   for (int h = kVupdMWarps / 2; h >= 1; h >>= 1) {

@@ -115,6 +115,7 @@ struct dfm_ctx {
   long long launches = 0;
   cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   cudaGraphExec_t step_exec = nullptr;  // one steady-state iteration
+  int dbg = 0;
   bool host_exchange = false;  // shard stepping API: {num, den} exchanged by the caller
   int xs_iter = 0, xs_iters = 0;
   bool use_graph = true;
@@ -263,6 +264,7 @@ void launch_em(dfm_ctx* c, int finish, int start, int slot, double* cost_dst = n
   a.start = start;
   a.cost_out = cost_dst ? cost_dst : c->cost_part.p + (size_t)slot * c->F;
   a.trace = c->tracing ? c->trace.p : nullptr;
+  a.dbg = c->dbg;
   c->kem<<<c->F, c->FT, c->smem_em, c->stream>>>(a);
   DFM_CK_LAUNCH();
   c->launches++;
@@ -818,6 +820,13 @@ int dfm_get_trace(dfm_ctx* c, unsigned long long* out, int n) {
   DFM_CK(cudaStreamSynchronize(c->stream));
   return (int)m;
   DFM_API_END
+}
+
+int dfm_debug_bits(dfm_ctx* c, int bits) {
+  if (!c) return DFM_ERR_ARG;
+  drop_graph(c);
+  c->dbg = bits;
+  return DFM_OK;
 }
 
 int dfm_force_generic(dfm_ctx* c, int on) {

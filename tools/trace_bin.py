@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--tiling", default="")
     ap.add_argument("--generic", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--dbg", type=int, default=0, help="timing experiments (results invalid)")
     args = ap.parse_args()
     c = bench.CONFIGS[args.workload]
     layout = dfm.BlockLayout(c["sizes"])
@@ -41,6 +42,8 @@ def main():
     if args.tiling:
         ft, tb = (int(v) for v in args.tiling.split(","))
         eng.set_tiling(ft, tb)
+    if args.dbg:
+        dfm._capi.check(lib.dfm_debug_bits(eng.ctx, args.dbg))
     eng.set_obs(x)
     eng.set_model(init.nmf, init.w0, init.lambda0)
     dfm._capi.check(lib.dfm_prime(eng.ctx))
