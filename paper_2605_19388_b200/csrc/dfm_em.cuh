@@ -29,13 +29,13 @@ struct EmArgs {
   cd* W;             // [F][wsz]
   double* Aw;        // [N][F][T] T-update weights (A)
   double* Bw;        // [N][F][T] T-update weights (B)
+  double* P;         // [F][M][T] decorrelated power |W^H x|^2 of the current W
   double* cost_out;  // [F] per-bin cost of this launch's slot
   int* fallbacks;
   int finish;  // 1 = cost only (first launch), 2 = Lambda update + cost
   int start;   // 1 = Q, IP, T-update weights
   unsigned long long* trace;  // optional [bin][16] phase stamps
   int dbg;                    // timing experiments only: bit0 no Lambda reduction, bit1 no Q accumulation,
-                              // bit2 no per-frame arithmetic in passes A/B
 };
 
 struct EmPlan {
@@ -117,6 +117,7 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
   const double floor_ = a.floor_;
   const int ntiles = (T + FT - 1) / FT;
   const cd* xf = a.x + (size_t)f * T * M;
+  double* Pf = a.P + (size_t)f * M * T;
   const double* Hf = a.H + (size_t)f * N * T;
   em_stamp(a, 0);
 
@@ -182,6 +183,12 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
     }
   };
 
+  // the frame's decorrelated power (written by pass C / k_power), one batch of loads
+  auto load_power = [&](int t, double* pv) {
+#pragma unroll
+    for (int m = 0; m < MS; ++m) pv[m] = Pf[(size_t)m * T + t];
+  };
+
   // ================================================================ pass A
   // finish iteration i-1: Lambda update with eta = max(h Lambda_old, floor)
   if (a.finish == 2) {
@@ -191,7 +198,9 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
     double* is = zs + M * FTp;       // [M][FTp]
     const int NM = N * M, SL = sp.SL;
     for (int u = tid; u < NM * SL; u += FT) red[2 * u] = red[2 * u + 1] = 0.0;
-    constexpr int kLamJobs = 8;
+    // DMMA jobs per warp: (mic tile of 8, num|den) pairs over the CTA's warps
+    // (static shapes: enough for >= 2 warps; else the SIMT reduction)
+    constexpr int kLamJobs = SB ? ((MB_ * NB_ + 7) / 8 * 2 + 1) / 2 : 8;
     const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3, nwarps = FT >> 5;
     const int njobs = 2 * ((M + 7) / 8);
     const bool use_mma = N <= 8 && njobs <= kLamJobs * nwarps;
@@ -207,29 +216,18 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
 #pragma unroll
         for (int n = 0; n < kMaxN; ++n)
           if (n < N) hs[n * FTp + tid] = h[n];
-        const cd* xt = xf + (size_t)t * M;
-        cd xall[MS];
-        if constexpr (SB) load_frame(xt, xall);
+        double pv[MS];
+        if constexpr (SB) load_power(t, pv);
 #pragma unroll
-        for (int b = 0; b < nb; ++b) {
-          double P[MAXMB];
-          if constexpr (SB)
-            power_regs(b, xall, P);
-          else
-            power_block(b, xt, P);
-          const int off = OFF(b), mb = MBof(b);
+        for (int m = 0; m < (SB ? MS : M); ++m) {
+          double raw = 0.0;
 #pragma unroll
-          for (int mu = 0; mu < MAXMB; ++mu)
-            if (mu < mb) {
-              const int m = off + mu;
-              double raw = 0.0;
-#pragma unroll
-              for (int n = 0; n < kMaxN; ++n)
-                if (n < N) raw += h[n] * Lsm[n * M + m];
-              const double ie = rcp_pos(fmax(raw, floor_));
-              is[m * FTp + tid] = ie;
-              zs[m * FTp + tid] = P[mu] * ie * ie;
-            }
+          for (int n = 0; n < kMaxN; ++n)
+            if (n < N) raw += h[n] * Lsm[n * M + m];
+          const double ie = rcp_pos(fmax(raw, floor_));
+          const double p = SB ? pv[SB ? m : 0] : Pf[(size_t)m * T + t];
+          is[m * FTp + tid] = ie;
+          zs[m * FTp + tid] = p * ie * ie;
         }
       }
       __syncthreads();
@@ -355,34 +353,32 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
         double h[kMaxN];
         load_h(t, h);
         const cd* xt = xf + (size_t)t * M;
-        cd xall[MS];
-        if constexpr (SB) {
-          load_frame(xt, xall);
-          if (a.start)
+        if (a.start) {  // the frame's samples for the Q tile
+          if constexpr (SB) {
+            cd xall[MS];
+            load_frame(xt, xall);
 #pragma unroll
             for (int m = 0; m < MS; ++m) xsm[m * FTp + tid] = xall[m];
-        }
-#pragma unroll
-        for (int b = 0; b < nb; ++b) {
-          double P[MAXMB];
-          const int off = OFF(b), mb = MBof(b);
-          if constexpr (SB)
-            power_regs(b, xall, P);
-          else
-            power_block(b, xt, P, a.start ? xsm + off * FTp + tid : nullptr, FTp);
-#pragma unroll
-          for (int mu = 0; mu < MAXMB; ++mu)
-            if (mu < mb) {
-              const int m = off + mu;
-              double raw = 0.0;
-#pragma unroll
-              for (int n = 0; n < kMaxN; ++n)
-                if (n < N) raw += h[n] * Lsm[n * M + m];
-              const double ie = rcp_pos(fmax(raw, floor_));
-              cost += P[mu] * ie;
-              lacc.mul(fmax(raw, 1e-300));
-              if (a.start) is[m * FTp + tid] = ie;
+          } else {
+            for (int m = 0; m < M; ++m) {
+              const double2 v = __ldg(reinterpret_cast<const double2*>(xt + m));
+              xsm[m * FTp + tid] = cd{v.x, v.y};
             }
+          }
+        }
+        double pv[MS];
+        if constexpr (SB) load_power(t, pv);
+#pragma unroll
+        for (int m = 0; m < (SB ? MS : M); ++m) {
+          double raw = 0.0;
+#pragma unroll
+          for (int n = 0; n < kMaxN; ++n)
+            if (n < N) raw += h[n] * Lsm[n * M + m];
+          const double ie = rcp_pos(fmax(raw, floor_));
+          const double p = SB ? pv[SB ? m : 0] : Pf[(size_t)m * T + t];
+          cost += p * ie;
+          lacc.mul(fmax(raw, 1e-300));
+          if (a.start) is[m * FTp + tid] = ie;
         }
         lacc.renorm();
       }
@@ -540,6 +536,7 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
             if (n < N) raw += h[n] * Lsm[n * M + m];
           const double ie = rcp_pos(fmax(raw, floor_));
           const double z = P[mu] * ie * ie;
+          Pf[(size_t)m * T + t] = P[mu];
 #pragma unroll
           for (int n = 0; n < kMaxN; ++n)
             if (n < N) {
@@ -822,86 +819,51 @@ __global__ void __launch_bounds__(32 * kVupdMWarps) k_vupd_mma(int F, int T, int
 }
 
 // Pass D as an elementwise kernel over (bin, frame): h' from H (= T_new V by
-// k_spec_mma), eta' = max(h' Lambda, floor), P = |W^H x|^2, and the V-update
-// weights A'_n = sum_m Lambda z, B'_n = sum_m Lambda / eta' (engine.cpp:231-237).
+// k_spec_mma), eta' = max(h' Lambda, floor), P = |W^H x|^2 as stored by pass C,
+// and the V-update weights A'_n = sum_m Lambda z, B'_n = sum_m Lambda / eta'
+// (engine.cpp:231-237).
 template <int MB_, int NB_, int NS_, int MAXMB>
 __global__ void __launch_bounds__(128, 6) k_pdw(const EmArgs a) {
   constexpr bool SB = MB_ > 0 && NB_ > 0;
   __shared__ double Ls[kMaxN * 64];
-  __shared__ cd Ws[DFM_MAX_MB * DFM_MAX_MB * 4];
   const int M = SB ? MB_ * NB_ : a.M;
-  const int nb = SB ? NB_ : a.nb;
   const int N = NS_ > 0 ? NS_ : a.N;
   const int T = a.T;
-  const int wsz = SB ? MB_ * MB_ * NB_ : a.wsz;
-  auto MBof = [&](int b) { return SB ? MB_ : a.mb[b]; };
-  auto OFF = [&](int b) { return SB ? b * MB_ : a.off[b]; };
-  auto WOFF = [&](int b) { return SB ? b * MB_ * MB_ : a.woff[b]; };
   const int f = blockIdx.y, t = blockIdx.x * blockDim.x + threadIdx.x;
   const double* Lg = a.lam + (size_t)f * N * M;
-  const cd* Wg = a.W + (size_t)f * wsz;
-  const bool smemL = N * M <= kMaxN * 64, smemW = wsz <= DFM_MAX_MB * DFM_MAX_MB * 4;
+  const bool smemL = N * M <= kMaxN * 64;
   if (smemL)
     for (int e = threadIdx.x; e < N * M; e += blockDim.x) Ls[e] = Lg[e];
-  if (smemW)
-    for (int e = threadIdx.x; e < wsz; e += blockDim.x) Ws[e] = Wg[e];
   __syncthreads();
   if (t >= T) return;
   const double* Lf = smemL ? Ls : Lg;
-  const cd* Wf = smemW ? Ws : Wg;
   double h[kMaxN];
 #pragma unroll
   for (int n = 0; n < kMaxN; ++n) h[n] = n < N ? __ldg(a.H + ((size_t)f * N + n) * T + t) : 0.0;
-  const cd* xt = a.x + ((size_t)f * T + t) * M;
+  const double* Pt = a.P + (size_t)f * M * T + t;
+  double pv[SB ? MB_ * NB_ : 1];
+  if constexpr (SB) {
+#pragma unroll
+    for (int m = 0; m < MB_ * NB_; ++m) pv[m] = __ldg(Pt + (size_t)m * T);
+  }
   double A[kMaxN], B[kMaxN];
 #pragma unroll
   for (int n = 0; n < kMaxN; ++n) A[n] = B[n] = 0.0;
 #pragma unroll
-  for (int b = 0; b < nb; ++b) {
-    const int mb = MBof(b), off = OFF(b);
-    const cd* wb = Wf + WOFF(b);
-    double P[MAXMB];
-    if constexpr (SB) {
-      cd xv[MB_];
+  for (int m = 0; m < (SB ? MB_ * NB_ : M); ++m) {
+    double raw = 0.0;
 #pragma unroll
-      for (int qq = 0; qq < MB_; ++qq) {
-        const double2 v = __ldg(reinterpret_cast<const double2*>(xt + off + qq));
-        xv[qq] = cd{v.x, v.y};
-      }
+    for (int n = 0; n < kMaxN; ++n)
+      if (n < N) raw += h[n] * Lf[n * M + m];
+    const double ie = rcp_pos(fmax(raw, a.floor_));
+    const double p = SB ? pv[SB ? m : 0] : __ldg(Pt + (size_t)m * T);
+    const double z = p * ie * ie;
 #pragma unroll
-      for (int mu = 0; mu < MB_; ++mu) {
-        cd s{0.0, 0.0};
-#pragma unroll
-        for (int qq = 0; qq < MB_; ++qq) s = s + cmulc(wb[mu * MB_ + qq], xv[qq]);
-        P[mu] = norm2(s);
-      }
-    } else {
-      for (int mu = 0; mu < mb; ++mu) {
-        cd s{0.0, 0.0};
-        for (int qq = 0; qq < mb; ++qq) {
-          const double2 v = __ldg(reinterpret_cast<const double2*>(xt + off + qq));
-          s = s + cmulc(wb[mu * mb + qq], cd{v.x, v.y});
-        }
-        P[mu] = norm2(s);
-      }
-    }
-#pragma unroll
-    for (int mu = 0; mu < MAXMB; ++mu)
-      if (mu < mb) {
-        const int m = off + mu;
-        double raw = 0.0;
-#pragma unroll
-        for (int n = 0; n < kMaxN; ++n)
-          if (n < N) raw += h[n] * Lf[n * M + m];
-        const double ie = rcp_pos(fmax(raw, a.floor_));
-        const double z = P[mu] * ie * ie;
-#pragma unroll
-        for (int n = 0; n < kMaxN; ++n)
-          if (n < N) {
-            const double l = Lf[n * M + m];
-            A[n] += z * l;
-            B[n] += ie * l;
-          }
+    for (int n = 0; n < kMaxN; ++n)
+      if (n < N) {
+        const double l = Lf[n * M + m];
+        A[n] += z * l;
+        B[n] += ie * l;
       }
   }
 #pragma unroll
@@ -916,6 +878,41 @@ __global__ void __launch_bounds__(128, 6) k_pdw(const EmArgs a) {
 }  // namespace dfm
 
 namespace dfm {
+// Decorrelation P = |W^H x|^2 (engine.cpp:60-69) of the current demixers into
+// P [F][M][T]; run before the first k_em_bin of a fit (pass C keeps P current
+// afterwards).  CTA = (128 frames, bin), W of the bin in shared memory.
+template <int MB_, int NB_, int NS_, int MAXMB>
+__global__ void __launch_bounds__(128) k_power(const EmArgs a) {
+  constexpr bool SB = MB_ > 0 && NB_ > 0;
+  __shared__ cd Ws[DFM_MAX_MB * DFM_MAX_MB * 4];
+  const int M = SB ? MB_ * NB_ : a.M;
+  const int nb = SB ? NB_ : a.nb;
+  const int T = a.T;
+  const int wsz = SB ? MB_ * MB_ * NB_ : a.wsz;
+  const int f = blockIdx.y, t = blockIdx.x * blockDim.x + threadIdx.x;
+  const cd* Wg = a.W + (size_t)f * wsz;
+  const bool smemW = wsz <= DFM_MAX_MB * DFM_MAX_MB * 4;
+  if (smemW)
+    for (int e = threadIdx.x; e < wsz; e += blockDim.x) Ws[e] = Wg[e];
+  __syncthreads();
+  if (t >= T) return;
+  const cd* Wf = smemW ? Ws : Wg;
+  const cd* xt = a.x + ((size_t)f * T + t) * M;
+  double* Pt = a.P + (size_t)f * M * T + t;
+  for (int b = 0; b < nb; ++b) {
+    const int mb = SB ? MB_ : a.mb[b], off = SB ? b * MB_ : a.off[b];
+    const cd* wb = Wf + (SB ? b * MB_ * MB_ : a.woff[b]);
+    for (int mu = 0; mu < mb; ++mu) {
+      cd s{0.0, 0.0};
+      for (int qq = 0; qq < mb; ++qq) {
+        const double2 v = __ldg(reinterpret_cast<const double2*>(xt + off + qq));
+        s = s + cmulc(wb[mu * mb + qq], cd{v.x, v.y});
+      }
+      Pt[(size_t)(off + mu) * T] = norm2(s);
+    }
+  }
+}
+
 // Wiener separation for the engine context (wiener.cpp:11-34 per block):
 // c_n = (W_b^H)^-1 (g_n .* (W_b^H x^b)), g_n,m = h_n Lambda(n, m) / max(h Lambda, floor).
 // CTA = (128 frames, bin); W, (W^H)^-1 and Lambda of the bin in shared memory,

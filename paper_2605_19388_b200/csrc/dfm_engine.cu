@@ -97,13 +97,14 @@ struct dfm_ctx {
   Layout L;
   cudaStream_t stream = nullptr;
   DBuf<cd> x, W;
-  DBuf<double> Tf, V, lam, H, Aw, Bw, numden, cost_part, cost_sum, cost_step;
+  DBuf<double> Tf, V, lam, H, Aw, Bw, P, numden, cost_part, cost_sum, cost_step;
   DBuf<cd> Ginv;  // (W^H)^-1 per (bin, block) for the Wiener filter
   DBuf<int> fallbacks;
   int maxmb = 4;
   int kmaxmb = 4;  // MAXMB of the selected instantiations
   void (*kem)(EmArgs) = nullptr;
   void (*kpdw)(EmArgs) = nullptr;
+  void (*kpow)(EmArgs) = nullptr;
   void (*kwien)(EmArgs, const cd*, cd*) = nullptr;
   bool force_generic = false;
   int FT = 128, TB = 128, smem_em = 0;
@@ -155,6 +156,7 @@ EmArgs make_args(dfm_ctx* c) {
   a.W = c->W.p;
   a.Aw = c->Aw.p;
   a.Bw = c->Bw.p;
+  a.P = c->P.p;
   a.fallbacks = c->fallbacks.p;
   return a;
 }
@@ -177,20 +179,20 @@ void select_kernels(dfm_ctx* c) {
   c->kem = nullptr;
   if (uniform && !c->force_generic) {
     if (mb == 4 && nb == 3 && N == 5 && K == 16) {
-      c->kem = k_em_bin<4, 3, 5, 4>; c->kpdw = k_pdw<4, 3, 5, 4>; c->kwien = k_wiener_ctx<4, 3, 5, 4>; c->kmaxmb = 4;
+      c->kem = k_em_bin<4, 3, 5, 4>; c->kpdw = k_pdw<4, 3, 5, 4>; c->kpow = k_power<4, 3, 5, 4>; c->kwien = k_wiener_ctx<4, 3, 5, 4>; c->kmaxmb = 4;
     } else if (mb == 2 && nb == 2 && N == 3 && K == 4) {
-      c->kem = k_em_bin<2, 2, 3, 2>; c->kpdw = k_pdw<2, 2, 3, 2>; c->kwien = k_wiener_ctx<2, 2, 3, 2>; c->kmaxmb = 2;
+      c->kem = k_em_bin<2, 2, 3, 2>; c->kpdw = k_pdw<2, 2, 3, 2>; c->kpow = k_power<2, 2, 3, 2>; c->kwien = k_wiener_ctx<2, 2, 3, 2>; c->kmaxmb = 2;
     } else if (mb == 4 && nb == 8 && N == 8 && K == 32) {
-      c->kem = k_em_bin<4, 8, 8, 4>; c->kpdw = k_pdw<4, 8, 8, 4>; c->kwien = k_wiener_ctx<4, 8, 8, 4>; c->kmaxmb = 4;
+      c->kem = k_em_bin<4, 8, 8, 4>; c->kpdw = k_pdw<4, 8, 8, 4>; c->kpow = k_power<4, 8, 8, 4>; c->kwien = k_wiener_ctx<4, 8, 8, 4>; c->kmaxmb = 4;
     } else if (mb == 12 && nb == 1 && N == 5 && K == 16) {
-      c->kem = k_em_bin<12, 1, 5, 12>; c->kpdw = k_pdw<12, 1, 5, 12>; c->kwien = k_wiener_ctx<12, 1, 5, 12>; c->kmaxmb = 12;
+      c->kem = k_em_bin<12, 1, 5, 12>; c->kpdw = k_pdw<12, 1, 5, 12>; c->kpow = k_power<12, 1, 5, 12>; c->kwien = k_wiener_ctx<12, 1, 5, 12>; c->kmaxmb = 12;
     }
   }
   if (!c->kem) {
     if (c->maxmb <= 4) {
-      c->kem = k_em_bin<0, 0, 0, 4>; c->kpdw = k_pdw<0, 0, 0, 4>; c->kwien = k_wiener_ctx<0, 0, 0, 4>; c->kmaxmb = 4;
+      c->kem = k_em_bin<0, 0, 0, 4>; c->kpdw = k_pdw<0, 0, 0, 4>; c->kpow = k_power<0, 0, 0, 4>; c->kwien = k_wiener_ctx<0, 0, 0, 4>; c->kmaxmb = 4;
     } else {
-      c->kem = k_em_bin<0, 0, 0, DFM_MAX_MB>; c->kpdw = k_pdw<0, 0, 0, DFM_MAX_MB>; c->kwien = k_wiener_ctx<0, 0, 0, DFM_MAX_MB>; c->kmaxmb = DFM_MAX_MB;
+      c->kem = k_em_bin<0, 0, 0, DFM_MAX_MB>; c->kpdw = k_pdw<0, 0, 0, DFM_MAX_MB>; c->kpow = k_power<0, 0, 0, DFM_MAX_MB>; c->kwien = k_wiener_ctx<0, 0, 0, DFM_MAX_MB>; c->kmaxmb = DFM_MAX_MB;
     }
   }
 }
@@ -260,6 +262,12 @@ void launch_spec(dfm_ctx* c) {
 
 void launch_em(dfm_ctx* c, int finish, int start, int slot, double* cost_dst = nullptr) {
   EmArgs a = make_args(c);
+  if (finish == 1) {  // first launch of a fit: P of the initial demixers
+    const dim3 grid((c->T + 127) / 128, c->F);
+    c->kpow<<<grid, 128, 0, c->stream>>>(a);
+    DFM_CK_LAUNCH();
+    c->launches++;
+  }
   a.finish = finish;
   a.start = start;
   a.cost_out = cost_dst ? cost_dst : c->cost_part.p + (size_t)slot * c->F;
@@ -446,6 +454,7 @@ dfm_ctx* dfm_create(int F, int T, int nblocks, const int* block_sizes, int N, in
     c->H.alloc((size_t)c->F * N * T);
     c->Aw.alloc((size_t)N * c->F * T);
     c->Bw.alloc((size_t)N * c->F * T);
+    c->P.alloc((size_t)c->F * c->M * T);
     c->numden.alloc(2 * (size_t)N * K * T);
     c->fallbacks.alloc(1);
     DFM_CK(cudaMemset(c->fallbacks.p, 0, sizeof(int)));
