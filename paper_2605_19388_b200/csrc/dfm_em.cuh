@@ -184,6 +184,9 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
   };
 
   // the frame's decorrelated power (written by pass C / k_power), one batch of loads
+  // P of the next tile is prefetched into registers when the frame is small
+  constexpr bool PF = SB && MS <= 16;
+  constexpr int MP = PF ? MS : 1;
   auto load_power = [&](int t, double* pv) {
 #pragma unroll
     for (int m = 0; m < MS; ++m) pv[m] = Pf[(size_t)m * T + t];
@@ -207,17 +210,33 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
     double lj0[kLamJobs], lj1[kLamJobs];
 #pragma unroll
     for (int jj = 0; jj < kLamJobs; ++jj) lj0[jj] = lj1[jj] = 0.0;
+    // software pipeline: the next tile's h and P are in flight while this
+    // tile is computed and reduced
+    double hn[kMaxN], pn[MP];
+    if (tid < T) {
+      load_h(tid, hn);
+      if constexpr (PF) load_power(tid, pn);
+    }
     for (int tl = 0; tl < ntiles; ++tl) {
       const int t = tl * FT + tid;
       const int tn = min(FT, T - tl * FT);
+      double h[kMaxN], pv[MS];
+#pragma unroll
+      for (int n = 0; n < kMaxN; ++n) h[n] = hn[n];
+      if constexpr (PF) {
+#pragma unroll
+        for (int m = 0; m < MS; ++m) pv[m] = pn[m];
+      }
+      if (t + FT < T) {
+        load_h(t + FT, hn);
+        if constexpr (PF) load_power(t + FT, pn);
+      }
+      if constexpr (SB && !PF)
+        if (tid < tn) load_power(t, pv);
       if (tid < tn) {
-        double h[kMaxN];
-        load_h(t, h);
 #pragma unroll
         for (int n = 0; n < kMaxN; ++n)
           if (n < N) hs[n * FTp + tid] = h[n];
-        double pv[MS];
-        if constexpr (SB) load_power(t, pv);
 #pragma unroll
         for (int m = 0; m < (SB ? MS : M); ++m) {
           double raw = 0.0;
@@ -346,28 +365,42 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
     const int FTp = FT + 1;
     cd* xsm = (cd*)tile;                              // [M][FTp]
     double* is = tile + 2 * (size_t)M * FTp;          // [M][FTp]
+    double hn[kMaxN], pn[MP];
+    if (tid < T) {
+      load_h(tid, hn);
+      if constexpr (PF) load_power(tid, pn);
+    }
     for (int tl = 0; tl < ntiles; ++tl) {
       const int t = tl * FT + tid;
       const int tn = min(FT, T - tl * FT);
-      if (tid < tn) {
-        double h[kMaxN];
-        load_h(t, h);
-        const cd* xt = xf + (size_t)t * M;
-        if (a.start) {  // the frame's samples for the Q tile
-          if constexpr (SB) {
-            cd xall[MS];
-            load_frame(xt, xall);
+      const cd* xt = xf + (size_t)t * M;
+      // the frame's samples for the Q tile: asynchronous copies that land
+      // while the per-frame terms below are computed
+      if (a.start && tid < tn) {
+        if constexpr (SB) {
 #pragma unroll
-            for (int m = 0; m < MS; ++m) xsm[m * FTp + tid] = xall[m];
-          } else {
-            for (int m = 0; m < M; ++m) {
-              const double2 v = __ldg(reinterpret_cast<const double2*>(xt + m));
-              xsm[m * FTp + tid] = cd{v.x, v.y};
-            }
+          for (int m = 0; m < MS; ++m) cp_async16(xsm + m * FTp + tid, xt + m);
+        } else {
+          for (int m = 0; m < M; ++m) {
+            const double2 v = __ldg(reinterpret_cast<const double2*>(xt + m));
+            xsm[m * FTp + tid] = cd{v.x, v.y};
           }
         }
-        double pv[MS];
-        if constexpr (SB) load_power(t, pv);
+      }
+      double h[kMaxN], pv[MS];
+#pragma unroll
+      for (int n = 0; n < kMaxN; ++n) h[n] = hn[n];
+      if constexpr (PF) {
+#pragma unroll
+        for (int m = 0; m < MS; ++m) pv[m] = pn[m];
+      }
+      if (t + FT < T) {
+        load_h(t + FT, hn);
+        if constexpr (PF) load_power(t + FT, pn);
+      }
+      if constexpr (SB && !PF)
+        if (tid < tn) load_power(t, pv);
+      if (tid < tn) {
 #pragma unroll
         for (int m = 0; m < (SB ? MS : M); ++m) {
           double raw = 0.0;
@@ -383,6 +416,7 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
         lacc.renorm();
       }
       if (a.start) {
+        if constexpr (SB) cp_async_wait_all();
         __syncthreads();
         // (block, entry r<=c) units accumulate all mu of their block
         for (int u = tid; u < ((a.dbg & 2) ? 0 : nitems * SQ); u += FT) {
@@ -435,6 +469,16 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
     a.cost_out[f] = c - (double)T * d;
   }
   if (!a.start) return;
+  // pass C's first frame: copies in flight during the Q reduction and the IP
+  // sweep (thread-private slots of the free frame tile)
+  const int FTpc = FT + 1;
+  cd* xst = (cd*)tile;  // [M][FTpc]
+  if constexpr (SB) {
+    __syncthreads();  // the Q tile reads of pass B are done
+    if (tid < T)
+#pragma unroll
+      for (int m = 0; m < MS; ++m) cp_async16(xst + m * FTpc + tid, xf + (size_t)tid * M + m);
+  }
   for (int idx = tid; idx < nitems * MAXMB; idx += FT) {
     const int it = idx / MAXMB, mu = idx - it * MAXMB;
     int rem = it, b = 0;
@@ -514,7 +558,14 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
     load_h(t, h);
     const cd* xt = xf + (size_t)t * M;
     cd xall[MS];
-    if constexpr (SB) load_frame(xt, xall);
+    if constexpr (SB) {
+      cp_async_wait_all();
+#pragma unroll
+      for (int m = 0; m < MS; ++m) xall[m] = xst[m * FTpc + tid];
+      if (t + FT < T)  // the thread's next frame
+#pragma unroll
+        for (int m = 0; m < MS; ++m) cp_async16(xst + m * FTpc + tid, xt + (size_t)FT * M + m);
+    }
     double A[kMaxN], B[kMaxN];
 #pragma unroll
     for (int n = 0; n < kMaxN; ++n) A[n] = B[n] = 0.0;
