@@ -636,7 +636,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 // (F x K) x (K x T) product; a warp owns 8 bins x 32 frames, the CTA 8 warps
 // along the frames.
 constexpr int kSpecMaxKs = kMaxK / 4;
-constexpr int kSpecWarps = 4, kSpecTiles = 4;  // a warp owns 8 bins x (4 x 8) frames
+constexpr int kSpecWarps = 4, kSpecTiles = 8;  // a warp owns 8 bins x (8 x 8) frames
 template <int KS>  // k-steps of 4 (K <= 4 KS)
 __global__ void __launch_bounds__(32 * kSpecWarps) k_spec_mma(int F, int T, int N, int K, const double* __restrict__ Tf,
                                                              const double* __restrict__ V, double* __restrict__ H) {
@@ -669,8 +669,12 @@ __global__ void __launch_bounds__(32 * kSpecWarps) k_spec_mma(int F, int T, int 
     const int t = t0 + 8 * j + 2 * q;
     if (f < F) {
       double* hp = H + ((size_t)f * N + n) * T;
-      if (t < T) hp[t] = c0;
-      if (t + 1 < T) hp[t + 1] = c1;
+      if (!(T & 1) && t + 1 < T) {  // even rows: 16-byte aligned pairs
+        *reinterpret_cast<double2*>(hp + t) = make_double2(c0, c1);
+      } else {
+        if (t < T) hp[t] = c0;
+        if (t + 1 < T) hp[t + 1] = c1;
+      }
     }
   }
 }
@@ -681,7 +685,7 @@ __global__ void __launch_bounds__(32 * kSpecWarps) k_spec_mma(int F, int T, int 
 constexpr int kTupdWarps = 8;
 constexpr int kMaxKt = kMaxK / 8;
 template <int KT>
-__global__ void __launch_bounds__(32 * kTupdWarps) k_tupd_mma(int F, int T, int N, int K, double* __restrict__ Tf,
+__global__ void __launch_bounds__(32 * kTupdWarps, KT <= 2 ? 3 : 2) k_tupd_mma(int F, int T, int N, int K, double* __restrict__ Tf,
                                                              const double* __restrict__ V,
                                                              const double* __restrict__ Aw,
                                                              const double* __restrict__ Bw, double floor_) {
@@ -693,13 +697,10 @@ __global__ void __launch_bounds__(32 * kTupdWarps) k_tupd_mma(int F, int T, int 
   const int steps = (T + 3) / 4;
   const int per = (steps + kTupdWarps - 1) / kTupdWarps;
   const int s0 = warp * per, s1 = min(steps, s0 + per);
-  constexpr int U = 4;  // k-steps per batch, each with its own accumulator chain
+  constexpr int U = 4;  // k-steps whose operands are loaded before their DMMAs
   double num[KT][2], den[KT][2];
-  double cn[U][KT][2], cd_[U][KT][2];
 #pragma unroll
-  for (int u = 0; u < U; ++u)
-#pragma unroll
-    for (int j = 0; j < KT; ++j) cn[u][j][0] = cn[u][j][1] = cd_[u][j][0] = cd_[u][j][1] = 0.0;
+  for (int j = 0; j < KT; ++j) num[j][0] = num[j][1] = den[j][0] = den[j][1] = 0.0;
   const int f = f0 + g;
   const double* ar = Aw + ((size_t)n * F + (f < F ? f : 0)) * T;
   const double* br = Bw + ((size_t)n * F + (f < F ? f : 0)) * T;
@@ -722,17 +723,10 @@ __global__ void __launch_bounds__(32 * kTupdWarps) k_tupd_mma(int F, int T, int 
 #pragma unroll
       for (int j = 0; j < KT; ++j)
         if (j < kt) {
-          dmma(cn[u][j][0], cn[u][j][1], av[u], vb[u][j]);
-          dmma(cd_[u][j][0], cd_[u][j][1], bv[u], vb[u][j]);
+          dmma(num[j][0], num[j][1], av[u], vb[u][j]);
+          dmma(den[j][0], den[j][1], bv[u], vb[u][j]);
         }
   }
-#pragma unroll
-  for (int j = 0; j < KT; ++j)
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      num[j][i] = (cn[0][j][i] + cn[1][j][i]) + (cn[2][j][i] + cn[3][j][i]);
-      den[j][i] = (cd_[0][j][i] + cd_[1][j][i]) + (cd_[2][j][i] + cd_[3][j][i]);
-    }
   // fixed-order tree over the warps: w += w + h for h = W/2, W/4, ..., 1
 #pragma unroll
   for (int h = kTupdWarps / 2; h >= 1; h >>= 1) {
@@ -775,7 +769,7 @@ __global__ void __launch_bounds__(32 * kTupdWarps) k_tupd_mma(int F, int T, int 
 // in warp order; apply in place or write {num, den} for the allreduce.
 constexpr int kVupdMWarps = 8;
 template <int KT>
-__global__ void __launch_bounds__(32 * kVupdMWarps) k_vupd_mma(int F, int T, int N, int K,
+__global__ void __launch_bounds__(32 * kVupdMWarps, KT <= 2 ? 3 : 2) k_vupd_mma(int F, int T, int N, int K,
                                                               const double* __restrict__ Tf,
                                                               const double* __restrict__ Aw,
                                                               const double* __restrict__ Bw,
@@ -789,13 +783,10 @@ __global__ void __launch_bounds__(32 * kVupdMWarps) k_vupd_mma(int F, int T, int
   const int steps = (F + 3) / 4;
   const int per = (steps + kVupdMWarps - 1) / kVupdMWarps;
   const int s0 = warp * per, s1 = min(steps, s0 + per);
-  constexpr int U = 4;  // k-steps per batch, each with its own accumulator chain
+  constexpr int U = 4;  // k-steps whose operands are loaded before their DMMAs
   double num[KT][2], den[KT][2];
-  double cn[U][KT][2], cd_[U][KT][2];
 #pragma unroll
-  for (int u = 0; u < U; ++u)
-#pragma unroll
-    for (int j = 0; j < KT; ++j) cn[u][j][0] = cn[u][j][1] = cd_[u][j][0] = cd_[u][j][1] = 0.0;
+  for (int j = 0; j < KT; ++j) num[j][0] = num[j][1] = den[j][0] = den[j][1] = 0.0;
   const int tb = t0 + g;
   for (int sb = s0; sb < s1; sb += U) {
     double av[U], bv[U], ta[U][KT];
@@ -816,17 +807,10 @@ __global__ void __launch_bounds__(32 * kVupdMWarps) k_vupd_mma(int F, int T, int
 #pragma unroll
       for (int j = 0; j < KT; ++j)
         if (j < kt) {
-          dmma(cn[u][j][0], cn[u][j][1], ta[u][j], av[u]);
-          dmma(cd_[u][j][0], cd_[u][j][1], ta[u][j], bv[u]);
+          dmma(num[j][0], num[j][1], ta[u][j], av[u]);
+          dmma(den[j][0], den[j][1], ta[u][j], bv[u]);
         }
   }
-#pragma unroll
-  for (int j = 0; j < KT; ++j)
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      num[j][i] = (cn[0][j][i] + cn[1][j][i]) + (cn[2][j][i] + cn[3][j][i]);
-      den[j][i] = (cd_[0][j][i] + cd_[1][j][i]) + (cd_[2][j][i] + cd_[3][j][i]);
-    }
   // fixed-order tree over the warps: w += w + h for h = W/2, W/4, ..., 1
 #pragma unroll
   for (int h = kVupdMWarps / 2; h >= 1; h >>= 1) {
