@@ -162,26 +162,7 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
     }
   };
 
-  // static shapes: every sample of a frame is loaded up front (one batch of
-  // M 16-byte loads in flight), then |W^H x|^2 per block from registers
   constexpr int MS = SB ? MB_ * NB_ : 1;
-  auto load_frame = [&](const cd* xt, cd* xall) {
-#pragma unroll
-    for (int m = 0; m < MS; ++m) {
-      const double2 v = __ldg(reinterpret_cast<const double2*>(xt + m));
-      xall[m] = cd{v.x, v.y};
-    }
-  };
-  auto power_regs = [&](int b, const cd* xall, double* P) {
-    const cd* wb = Wsm + b * MB_ * MB_;
-#pragma unroll
-    for (int mu = 0; mu < MB_; ++mu) {
-      cd s{0.0, 0.0};
-#pragma unroll
-      for (int q = 0; q < MB_; ++q) s = s + cmulc(wb[mu * MB_ + q], xall[b * MB_ + q]);
-      P[mu] = norm2(s);
-    }
-  };
 
   // the frame's decorrelated power (written by pass C / k_power), one batch of loads
   // P of the next tile is prefetched into registers when the frame is small
@@ -511,6 +492,7 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
         w.ok[mu] = chol_thread<MB_>(Qsum + a.qofs[b] + mu * E, w.L[mu], w.dinv[mu]) ? 1 : 0;
       }
       __syncthreads();
+      em_stamp(a, 6);
       const int l = tid & 3;
       const unsigned qmask = 0xFu << (tid & 28);
       for (int b = tid >> 2; b < nb; b += FT >> 2) {
@@ -518,6 +500,7 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
         cd* wb = Wsm + b * MB_ * MB_;
         const cd* qb = Qsum + a.qofs[b];
         const bool ok = ip_sweep_quad<MB_>(wb, w, qb, floor_, l, qmask);
+        if (!ok && l == 0 && a.trace) atomicAdd(a.trace + blockIdx.x * 16 + 7, 1ull);
         if (!ok && l == 0) {
           // exact path (engine.cpp:47-49: LU, residual test, pinv) from W_old
 #pragma unroll
@@ -557,25 +540,28 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
     double h[kMaxN];
     load_h(t, h);
     const cd* xt = xf + (size_t)t * M;
-    cd xall[MS];
-    if constexpr (SB) {
-      cp_async_wait_all();
-#pragma unroll
-      for (int m = 0; m < MS; ++m) xall[m] = xst[m * FTpc + tid];
-      if (t + FT < T)  // the thread's next frame
-#pragma unroll
-        for (int m = 0; m < MS; ++m) cp_async16(xst + m * FTpc + tid, xt + (size_t)FT * M + m);
-    }
+    if constexpr (SB) cp_async_wait_all();
     double A[kMaxN], B[kMaxN];
 #pragma unroll
     for (int n = 0; n < kMaxN; ++n) A[n] = B[n] = 0.0;
 #pragma unroll
     for (int b = 0; b < nb; ++b) {
       double P[MAXMB];
-      if constexpr (SB)
-        power_regs(b, xall, P);
-      else
+      if constexpr (SB) {  // the block's samples from the thread's slot
+        const cd* wb = Wsm + b * MB_ * MB_;
+        cd xv[MB_];
+#pragma unroll
+        for (int q = 0; q < MB_; ++q) xv[q] = xst[(b * MB_ + q) * FTpc + tid];
+#pragma unroll
+        for (int mu = 0; mu < MB_; ++mu) {
+          cd s{0.0, 0.0};
+#pragma unroll
+          for (int q = 0; q < MB_; ++q) s = s + cmulc(wb[mu * MB_ + q], xv[q]);
+          P[mu] = norm2(s);
+        }
+      } else {
         power_block(b, xt, P);
+      }
       const int off = OFF(b), mb = MBof(b);
 #pragma unroll
       for (int mu = 0; mu < MAXMB; ++mu)
@@ -596,6 +582,12 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
               B[n] += ie * l;
             }
         }
+    }
+    if constexpr (SB) {
+      if (t + FT < T) {  // the thread's next frame, after its slot has been read
+#pragma unroll
+        for (int m = 0; m < MS; ++m) cp_async16(xst + m * FTpc + tid, xt + (size_t)FT * M + m);
+      }
     }
 #pragma unroll
     for (int n = 0; n < kMaxN; ++n)

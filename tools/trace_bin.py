@@ -71,6 +71,12 @@ def main():
            "phases_us_mean": {p: round(float(d[:, i].mean()), 3) for i, p in enumerate(PHASES)},
            "phases_us_max": {p: round(float(d[:, i].max()), 3) for i, p in enumerate(PHASES)}}
     starts = np.sort(tr[:, 0]) / 1e3
+    chol = (buf.reshape(-1, 16)[:, 6].astype(np.int64) - t0 - tr[:, 3]) / 1e3
+    if (buf.reshape(-1, 16)[:, 6] > 0).all():
+        out["ip_cholesky_us_mean"] = round(float(chol.mean()), 3)
+    slow = buf.reshape(-1, 16)[:, 7]
+    out["ip_slow_path_blocks"] = int(slow.sum())
+    out["ip_slow_path_bins"] = int((slow > 0).sum())
     out["start_percentiles_us"] = [round(float(np.percentile(starts, q)), 1) for q in (0, 10, 25, 50, 75, 90, 100)]
     print(json.dumps(out, indent=1))
 
