@@ -2,7 +2,7 @@
 """Benchmark of the B200-native distributed-FastMNMF EM iteration.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                  [--workload config1|config0|config2|config3] [--e2e-iters I]
+                  [--workload config1|config0|config2|config3|config4] [--e2e-iters I]
 
 A *step* is one steady-state EM iteration of BASELINE.json's config 1
 (B=3 subarrays x M_b=4 mics, N=5 sources, F=513 bins, T=626 frames, K=16):
@@ -15,6 +15,12 @@ barrier + synchronize on both sides, max over ranks.
 
 N > 1 (torchrun): frequency bins sharded over the ranks, one NCCL allreduce of
 the V-update numerator/denominator per iteration (strong scaling).
+
+--workload config4: 64 independent config-1 mixtures (seeds SEED_X + j,
+SEED_INIT + j), mixtures sharded over the ranks with no communication; a step
+is one EM iteration of every local mixture (one context per mixture, each on
+its own stream, kernels of different mixtures overlapping).  The 64 contexts'
+working sets (8.4 GB) exceed L2, so no flush is needed between steps.
 
 --impl reference: the reference's CPU algorithm (oracle/ restatement; the
 reference itself needs Eigen, absent here) on all host cores, rank 0 only.
@@ -39,6 +45,8 @@ CONFIGS = {
     "config1": dict(kind=1, F=513, T=626, sizes=[4, 4, 4], N=5, K=16, iters=200),
     "config2": dict(kind=1, F=513, T=626, sizes=[12], N=5, K=16, iters=200),
     "config3": dict(kind=1, F=1025, T=2000, sizes=[4] * 8, N=8, K=32, iters=100),
+    # 64 independent config-1 mixtures, each from its own seed, sharded over GPUs
+    "config4": dict(kind=1, F=513, T=626, sizes=[4, 4, 4], N=5, K=16, iters=100, batch=64),
 }
 SEED_X, SEED_INIT = 2605, 19388
 PAPER_CPU_TFBIN = 266.5e3  # BASELINE.md derived paper figure (other config/hardware), context only
@@ -209,8 +217,8 @@ def run_reference(args, c, world, rank):
     sample = (f"oracle/ C restatement of engine.cpp (reference needs Eigen3, unbuildable here) on the first "
               f"{Fs} of {F} bins x {T} frames per step, OpenMP over bins")
     return {
-        "metric": "dFastMNMF EM TF-bin*iter/s (BASELINE config 1)", "value": value, "unit": "TF-bin*iter/s",
-        "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "metric": f"dFastMNMF EM TF-bin*iter/s (BASELINE {args.workload})", "value": value,
+        "unit": "TF-bin*iter/s", "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -220,6 +228,120 @@ def run_reference(args, c, world, rank):
         "e2e": {"value": value, "unit": "TF-bin*iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "iter_per_s_full_config": value / (F * T),
     }
+
+
+def run_batch(args, c, world, rank, local):
+    """config 4: independent mixtures, one context each, no communication."""
+    import ctypes
+
+    import torch
+
+    import paper_2605_19388_b200 as dfm
+
+    lib = dfm._capi.load()
+    layout = dfm.BlockLayout(c["sizes"])
+    F, T, N, K, M = c["F"], c["T"], c["N"], c["K"], layout.total
+    nb = args.batch or c["batch"]
+    mine = list(range(rank, nb, world))
+    engines, xs, inits = [], [], []
+    for j in mine:
+        x = dfm.generate_mixture(c["kind"], F, T, M, N, K, SEED_X + j)
+        init = dfm.random_init(F, T, layout, N, K, SEED_INIT + j)
+        e = dfm.Engine(F, T, layout, N, K, device=local)
+        e.set_obs(x)
+        e.set_model(init.nmf, init.w0, init.lambda0)
+        dfm._capi.check(lib.dfm_prime(e.ctx))
+        engines.append(e)
+        xs.append(torch.from_numpy(x).pin_memory().numpy())
+        inits.append(init)
+    arr = (ctypes.c_void_p * len(engines))(*[e.ctx for e in engines])
+
+    def step():
+        v = ctypes.c_double()
+        dfm._capi.check(lib.dfm_bench_step_many(arr, len(engines), ctypes.byref(v)))
+        return v.value
+
+    pg = torch.distributed if world > 1 else None
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    launches0 = sum(e.launches() for e in engines)
+    sampler = ClockSampler(local).start()
+    t_ms = [step() for _ in range(args.steps)]
+    clocks = sampler.stop()
+    launches = sum(e.launches() for e in engines) - launches0
+    total_ms = float(np.sum(t_ms))
+    if pg:
+        tt = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        pg.all_reduce(tt, op=pg.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_step = total_ms / args.steps
+    value = nb * F * T * args.steps / (total_ms * 1e-3)
+    # e2e: every local mixture's pinned host X + init in, e2e_iters EM sweeps
+    # of the batch (dfm_fit_many), cost traces and fitted models out
+    e2e_times = []
+    for _ in range(2):
+        if pg:
+            pg.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for e, x, init in zip(engines, xs, inits):
+            e.set_obs(x)
+            e.set_model(init.nmf, init.w0, init.lambda0)
+        dfm.fit_many(engines, args.e2e_iters)
+        for e in engines:
+            e.get_model()
+        dt = time.perf_counter() - t0
+        if pg:
+            tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            pg.all_reduce(tt, op=pg.ReduceOp.MAX)
+            dt = float(tt.item())
+        e2e_times.append(dt)
+    e2e_dt = min(e2e_times)
+    mbytes = (inits[0].nmf.T.nbytes + inits[0].nmf.V.nbytes + inits[0].lambda0.nbytes
+              + sum(w.nbytes for w in inits[0].w0))
+    h2d = len(engines) * (xs[0].nbytes + mbytes)
+    d2h = len(engines) * (mbytes + 8 * (args.e2e_iters + 1))
+    if rank != 0:
+        for e in engines:
+            e.close()
+        return None
+    pk = peaks()
+    fp64_peak = float(lib.dfm_probe_fp64_tflops(local))
+    fl = nb * alg_flops(c) / (ms_step * 1e-3) / 1e12
+    ab = nb * alg_bytes(c)
+    line = {
+        "metric": f"dFastMNMF EM TF-bin*iter/s (BASELINE {args.workload})",
+        "value": value, "unit": "TF-bin*iter/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded STFT-domain mixtures, BASELINE config generator, one seed per mixture)",
+        "config": {"workload": args.workload, "mixtures": nb, "F": F, "T": T, "sizes": c["sizes"], "N": N, "K": K,
+                   "l2": f"working set of {len(engines)} contexts (~131 MB each) exceeds L2 (no flush)",
+                   "parallelism": f"mixtures sharded x{world}" if world > 1 else "1 GPU, one stream per mixture"},
+        "iter_per_s": 1e3 / ms_step,
+        "roofline": {"bound": "hbm", "achieved": ab / (ms_step * 1e-3) / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": ab / (ms_step * 1e-3) / 1e9 / pk["hbm_gbs"], "traffic": None,
+                     "kernel": "whole iteration (all mixtures)", "alg_bytes_per_step": ab,
+                     "peak_source": pk["source"]},
+        "roofline_fp64": {"bound": "fp64", "achieved": fl, "peak": fp64_peak, "unit": "TFLOP/s",
+                          "frac": fl / fp64_peak if fp64_peak > 0 else None,
+                          "peak_source": "measured in this run (DFMA microbenchmark, dfm_probe_fp64_tflops)"},
+        "e2e": {"value": nb * F * T * args.e2e_iters / e2e_dt, "unit": "TF-bin*iter/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "step": f"set_obs/set_model of every mixture (pinned host X + init H2D), fit_many({args.e2e_iters}), "
+                        "get_model of every mixture; best of 2", "seconds_per_step": e2e_dt},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+    }
+    if not args.no_cpu_baseline:
+        init_d = dict(T=inits[0].nmf.T, V=inits[0].nmf.V, lam=inits[0].lambda0, w=inits[0].w0)
+        line["cpu_baseline"] = cpu_baseline(c, xs[0], init_d, threads=1)
+    for e in engines:
+        e.close()
+    return line
 
 
 def main():
@@ -232,6 +354,7 @@ def main():
     ap.add_argument("--e2e-iters", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tiling", default="", help="FT,TB override: frame tile of the per-bin kernel and of k_pd")
+    ap.add_argument("--batch", type=int, default=0, help="config4: number of mixtures (default 64)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     c = CONFIGS[args.workload]
@@ -252,6 +375,13 @@ def main():
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         pg = dist
+    if "batch" in c:
+        line = run_batch(args, c, world, rank, local)
+        if line is not None:
+            print(json.dumps(line), flush=True)
+        if pg:
+            pg.destroy_process_group()
+        return
     import paper_2605_19388_b200 as dfm
 
     lib = dfm._capi.load()
@@ -381,7 +511,7 @@ def main():
         except Exception:
             traffic = None
     line = {
-        "metric": "dFastMNMF EM TF-bin*iter/s (BASELINE config 1)",
+        "metric": f"dFastMNMF EM TF-bin*iter/s (BASELINE {args.workload})",
         "value": value, "unit": "TF-bin*iter/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded STFT-domain mixture, BASELINE config generator)",

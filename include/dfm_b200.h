@@ -114,6 +114,17 @@ int dfm_shard_end(dfm_ctx* ctx, double* cost_trace_local);
 int dfm_fit(dfm_ctx* ctx, int iters, double* cost_trace, double* wall_seconds,
             double* stage_seconds);
 
+/* Batch of independent mixtures (BASELINE config 4): runs dfm_fit on every
+ * context (same device, each its own stream) with their launches
+ * interleaved iteration by iteration, so the kernels of different mixtures
+ * overlap on the GPU.  No reference counterpart: the reference fits one
+ * mixture per call (fastmnmf.cpp:118-126); this is n such calls.
+ * cost_traces: n * (iters+1) entries, mixture-major (may be NULL);
+ * elapsed_seconds: device time of the whole batch (may be NULL).
+ * Returns the total number of IP pinv fallbacks or an error code. */
+int dfm_fit_many(dfm_ctx* const* ctxs, int n, int iters, double* cost_traces,
+                 double* elapsed_seconds);
+
 /* Benchmark hooks: one steady-state EM iteration (per-bin kernel in
  * "finish previous + start next" mode, T update, V weights, V update,
  * spectrogram), enqueued on the context stream; dfm_prime runs the first
@@ -123,6 +134,11 @@ int dfm_prime(dfm_ctx* ctx);
 int dfm_bench_step(dfm_ctx* ctx);
 int dfm_sync(dfm_ctx* ctx);
 double dfm_bench_last_ms(dfm_ctx* ctx);
+/* Bench hook for a batch of independent mixtures (config 4): one
+ * steady-state iteration of every context (each its own stream, primed),
+ * joined; *ms_out = device time of the batch.  Synchronous. */
+int dfm_bench_step_many(dfm_ctx* const* ctxs, int n, double* ms_out);
+
 /* dfm_bench_step replays the iteration as a CUDA graph (one launch).
  * dfm_bench_split_step runs the same iteration as stream launches with events
  * between the kernels; dfm_bench_last_split then returns the device time of

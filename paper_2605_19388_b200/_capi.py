@@ -32,6 +32,8 @@ _SIGS = {
     "dfm_comm_init": (_i, [_vp, _vp, _i, _i]),
     "dfm_nccl_get_unique_id": (_i, [_vp]),
     "dfm_fit": (_i, [_vp, _i, _vp, _vp, _vp]),
+    "dfm_fit_many": (_i, [_vp, _i, _i, _vp, _vp]),
+    "dfm_bench_step_many": (_i, [_vp, _i, _vp]),
     "dfm_shard_begin": (_i, [_vp, _i]),
     "dfm_shard_numden": (_i, [_vp, _vp]),
     "dfm_shard_advance": (_i, [_vp, _vp]),

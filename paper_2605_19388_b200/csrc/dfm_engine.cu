@@ -591,17 +591,25 @@ int dfm_comm_init(dfm_ctx* c, const void* uid, int nranks, int rank) {
   DFM_API_END
 }
 
-int dfm_fit(dfm_ctx* c, int iters, double* cost_trace, double* wall_seconds, double* stage_seconds) {
-  if (!c) return DFM_ERR_ARG;
+}  // extern "C"
+
+namespace {
+// dfm_fit in three pieces so several contexts can interleave their launches
+// (dfm_fit_many): fit_begin queues the spectrogram, fit_launch(i) queues
+// launch i (finish iteration i-1, start iteration i), fit_end collects.
+bool fit_check(dfm_ctx* c, int iters) {
   if (iters < 0) {
     set_error("run_engine: negative iteration count");
-    return DFM_ERR_ARG;
+    return false;
   }
   if (!c->has_obs || !c->has_model) {
     set_error("dfm_fit: observations and model must be set first");
-    return DFM_ERR_ARG;
+    return false;
   }
-  DFM_API_BEGIN
+  return true;
+}
+
+void fit_begin(dfm_ctx* c, int iters) {
   DFM_CK(cudaSetDevice(c->device));
   ensure_cost(c, iters + 1);
   DFM_CK(cudaMemsetAsync(c->fallbacks.p, 0, sizeof(int), c->stream));
@@ -610,20 +618,24 @@ int dfm_fit(dfm_ctx* c, int iters, double* cost_trace, double* wall_seconds, dou
     DFM_CK(cudaEventCreate(&e));
     c->iter_ev.push_back(e);
   }
-  // launch i (0..iters): finish iteration i-1 (cost-only for i = 0), start iteration i
   launch_spec(c);
-  for (int i = 0; i <= iters; ++i) {
-    DFM_CK(cudaEventRecord(c->iter_ev[i], c->stream));
-    if (i == 0 || i == iters) {
-      launch_em(c, i == 0 ? 1 : 2, i < iters ? 1 : 0, i);
-      if (i < iters) launch_rest(c, nullptr);
-    } else {
-      run_step(c, false);  // per-bin cost of iteration i-1 -> cost_step
-      DFM_CK(cudaMemcpyAsync(c->cost_part.p + (size_t)i * c->F, c->cost_step.p, sizeof(double) * c->F,
-                             cudaMemcpyDeviceToDevice, c->stream));
-    }
+}
+
+void fit_launch(dfm_ctx* c, int i, int iters) {
+  DFM_CK(cudaEventRecord(c->iter_ev[i], c->stream));
+  if (i == 0 || i == iters) {
+    launch_em(c, i == 0 ? 1 : 2, i < iters ? 1 : 0, i);
+    if (i < iters) launch_rest(c, nullptr);
+  } else {
+    run_step(c, false);  // per-bin cost of iteration i-1 -> cost_step
+    DFM_CK(cudaMemcpyAsync(c->cost_part.p + (size_t)i * c->F, c->cost_step.p, sizeof(double) * c->F,
+                           cudaMemcpyDeviceToDevice, c->stream));
   }
-  DFM_CK(cudaEventRecord(c->iter_ev[iters + 1], c->stream));
+  if (i == iters) DFM_CK(cudaEventRecord(c->iter_ev[iters + 1], c->stream));
+}
+
+int fit_end(dfm_ctx* c, int iters, double* cost_trace, double* wall_seconds, double* stage_seconds) {
+  DFM_CK(cudaSetDevice(c->device));
   std::vector<double> part((size_t)(iters + 1) * c->F);
   c->cost_part.download(part.data(), part.size(), c->stream);
   int fb = 0;
@@ -653,6 +665,60 @@ int dfm_fit(dfm_ctx* c, int iters, double* cost_trace, double* wall_seconds, dou
     stage_seconds[0] = total_ms * 1e-3;
     stage_seconds[1] = stage_seconds[2] = stage_seconds[3] = 0.0;
   }
+  return fb;
+}
+}  // namespace
+
+extern "C" {
+
+int dfm_fit(dfm_ctx* c, int iters, double* cost_trace, double* wall_seconds, double* stage_seconds) {
+  if (!c) return DFM_ERR_ARG;
+  if (!fit_check(c, iters)) return DFM_ERR_ARG;
+  DFM_API_BEGIN
+  fit_begin(c, iters);
+  for (int i = 0; i <= iters; ++i) fit_launch(c, i, iters);
+  return fit_end(c, iters, cost_trace, wall_seconds, stage_seconds);
+  DFM_API_END
+}
+
+int dfm_fit_many(dfm_ctx* const* ctxs, int n, int iters, double* cost_traces, double* elapsed_seconds) {
+  if (!ctxs || n < 1) return DFM_ERR_ARG;
+  for (int j = 0; j < n; ++j)
+    if (!ctxs[j] || ctxs[j]->device != ctxs[0]->device) {
+      set_error("dfm_fit_many: contexts must be valid and on one device");
+      return DFM_ERR_ARG;
+    }
+  for (int j = 0; j < n; ++j)
+    if (!fit_check(ctxs[j], iters)) return DFM_ERR_ARG;
+  DFM_API_BEGIN
+  DFM_CK(cudaSetDevice(ctxs[0]->device));
+  cudaEvent_t e0, e1;
+  DFM_CK(cudaEventCreate(&e0));
+  DFM_CK(cudaEventCreate(&e1));
+  // every context's stream starts after e0 and e1 follows every stream, so the
+  // elapsed time covers the whole batch
+  DFM_CK(cudaEventRecord(e0, ctxs[0]->stream));
+  for (int j = 1; j < n; ++j) DFM_CK(cudaStreamWaitEvent(ctxs[j]->stream, e0, 0));
+  for (int j = 0; j < n; ++j) fit_begin(ctxs[j], iters);
+  for (int i = 0; i <= iters; ++i)
+    for (int j = 0; j < n; ++j) fit_launch(ctxs[j], i, iters);
+  for (int j = 1; j < n; ++j) {
+    DFM_CK(cudaEventRecord(ctxs[j]->ev[5], ctxs[j]->stream));
+    DFM_CK(cudaStreamWaitEvent(ctxs[0]->stream, ctxs[j]->ev[5], 0));
+  }
+  DFM_CK(cudaEventRecord(e1, ctxs[0]->stream));
+  int fb = 0;
+  for (int j = 0; j < n; ++j) {
+    const int r = fit_end(ctxs[j], iters, cost_traces ? cost_traces + (size_t)j * (iters + 1) : nullptr, nullptr,
+                          nullptr);
+    fb += r;
+  }
+  float ms = 0.f;
+  DFM_CK(cudaEventSynchronize(e1));
+  DFM_CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (elapsed_seconds) *elapsed_seconds = ms * 1e-3;
   return fb;
   DFM_API_END
 }
@@ -742,6 +808,33 @@ int dfm_bench_step(dfm_ctx* c) {
   DFM_CK(cudaEventRecord(c->ev[0], c->stream));
   run_step(c, false);
   DFM_CK(cudaEventRecord(c->ev[5], c->stream));
+  return DFM_OK;
+  DFM_API_END
+}
+
+int dfm_bench_step_many(dfm_ctx* const* ctxs, int n, double* ms_out) {
+  if (!ctxs || n < 1) return DFM_ERR_ARG;
+  for (int j = 0; j < n; ++j)
+    if (!ctxs[j] || ctxs[j]->device != ctxs[0]->device) return DFM_ERR_ARG;
+  DFM_API_BEGIN
+  DFM_CK(cudaSetDevice(ctxs[0]->device));
+  cudaEvent_t e0, e1;
+  DFM_CK(cudaEventCreate(&e0));
+  DFM_CK(cudaEventCreate(&e1));
+  DFM_CK(cudaEventRecord(e0, ctxs[0]->stream));
+  for (int j = 1; j < n; ++j) DFM_CK(cudaStreamWaitEvent(ctxs[j]->stream, e0, 0));
+  for (int j = 0; j < n; ++j) run_step(ctxs[j], false);
+  for (int j = 1; j < n; ++j) {
+    DFM_CK(cudaEventRecord(ctxs[j]->ev[5], ctxs[j]->stream));
+    DFM_CK(cudaStreamWaitEvent(ctxs[0]->stream, ctxs[j]->ev[5], 0));
+  }
+  DFM_CK(cudaEventRecord(e1, ctxs[0]->stream));
+  DFM_CK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  DFM_CK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (ms_out) *ms_out = ms;
   return DFM_OK;
   DFM_API_END
 }

@@ -508,6 +508,24 @@ class Engine:
         return int(self.lib.dfm_launch_count(self.ctx))
 
 
+def fit_many(engines: Sequence["Engine"], iters: int):
+    """Fits independent mixtures together (BASELINE config 4): every engine
+    (one mixture each, same device, observations and model already set) runs
+    `iters` EM sweeps with their launches interleaved so their kernels overlap.
+    Returns (cost_traces (n, iters+1), device seconds of the batch, fallbacks)."""
+    engines = list(engines)
+    if not engines:
+        raise ValueError("fit_many: no engines")
+    if iters < 0:
+        raise ValueError("run_engine: negative iteration count")
+    arr = (C.c_void_p * len(engines))(*[e.ctx for e in engines])
+    cost = np.zeros((len(engines), iters + 1))
+    secs = C.c_double(0.0)
+    lib = engines[0].lib
+    fb = check(lib.dfm_fit_many(arr, len(engines), iters, _ptr(cost), C.byref(secs)), "fit_many")
+    return cost, secs.value, fb
+
+
 def _run_engine(x, layout: BlockLayout, init: InitBundle, iters: int, options: FitOptions):
     """detail::run_engine (engine.cpp:167-272) on the device."""
     x = _obs(x)

@@ -373,3 +373,37 @@ def test_binding_mirror_fit_is_monotone(dfm):
     assert len(full["cost_trace"]) == 6
     with pytest.raises(ValueError):
         _fastmnmf.fit_full(np.zeros((3, 4)), n_sources=2)
+
+
+def test_fit_many_matches_individual_fits(dfm, oracle):
+    # BASELINE config 4 path: independent mixtures fitted together (one
+    # context and stream each, launches interleaved) give bitwise the results
+    # of fitting each alone, and each trace matches the oracle
+    F, T, N, K, sizes = 257, 200, 3, 4, [2, 2]
+    engines, inits, xs = [], [], []
+    for j in range(3):
+        x = dfm.generate_mixture(0, F, T, 4, N, K, 700 + j)
+        layout = dfm.BlockLayout(sizes)
+        init = dfm.random_init(F, T, layout, N, K, 900 + j)
+        e = dfm.Engine(F, T, layout, N, K)
+        e.set_obs(x)
+        e.set_model(init.nmf, init.w0, init.lambda0)
+        engines.append(e)
+        inits.append(init)
+        xs.append(x)
+    costs, secs, fb = dfm.fit_many(engines, 12)
+    assert costs.shape == (3, 13) and secs > 0 and fb >= 0
+    for j, (e, x, init) in enumerate(zip(engines, xs, inits)):
+        nmf, w, lam = e.get_model()
+        e2 = dfm.Engine(F, T, dfm.BlockLayout(sizes), N, K)
+        e2.set_obs(x)
+        e2.set_model(init.nmf, init.w0, init.lambda0)
+        c2, _, _, _ = e2.fit(12)
+        assert np.array_equal(costs[j], c2)
+        nmf2, w2, lam2 = e2.get_model()
+        assert np.array_equal(nmf.T, nmf2.T) and np.array_equal(nmf.V, nmf2.V) and np.array_equal(lam, lam2)
+        r = oracle.run_engine(x, sizes, _init_dict(init), 12)
+        assert _rel(costs[j], r["cost_trace"]) < TRAJ_RTOL
+        assert np.all(np.diff(costs[j]) <= 1e-9 * np.abs(costs[j][:-1]))
+        e.close()
+        e2.close()
