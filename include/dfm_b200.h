@@ -41,7 +41,7 @@
  *   DFM_ERR_SHAPE     -> ShapeMismatch / std::invalid_argument
  *   DFM_ERR_SINGULAR  -> SingularDemixer (cost functions only; inside a fit a
  *                        singular demixer records a +inf cost, engine.hpp:41-43)
- *   DFM_ERR_CUDA, DFM_ERR_NCCL -> std::runtime_error
+ *   DFM_ERR_CUDA, DFM_ERR_NCCL, DFM_ERR_IO -> std::runtime_error
  */
 #ifndef DFM_B200_H
 #define DFM_B200_H
@@ -54,12 +54,19 @@ extern "C" {
 #endif
 
 #define DFM_OK 0
+#ifndef DFM_MAX_BLOCKS
+#define DFM_MAX_BLOCKS 32 /* subarrays per layout */
+#endif
+#ifndef DFM_MAX_MB
+#define DFM_MAX_MB 16 /* largest subarray (block) size */
+#endif
 #define DFM_ERR_SHAPE -1
 #define DFM_ERR_ARG -2
 #define DFM_ERR_SINGULAR -3
 #define DFM_ERR_CUDA -4
 #define DFM_ERR_NCCL -5
 #define DFM_ERR_UNSUPPORTED -6
+#define DFM_ERR_IO -7 /* file / container errors -> std::runtime_error */
 
 typedef struct dfm_ctx dfm_ctx;
 
@@ -223,6 +230,32 @@ int dfm_generate_mixture(int kind, int F, int T, int M, int N, int K, uint64_t s
  * flush helper (writes a buffer larger than L2 on the current device). */
 double dfm_probe_fp64_tflops(int device);
 int dfm_l2_flush(int device);
+
+/* ---- FMNM v2 model container (io.hpp:26-34 / io.cpp:49-135) ----------
+ * save_model / load_model for dumped initialisations and fitted models.
+ * Payload buffers use the reference's order, which is also the dfm_set_model
+ * layout: T: n_models x N x (F x K col-major); V: n_models x N x (K x T
+ * col-major); lam: F x (N x M col-major); w: per block, per bin, M_b x M_b
+ * complex col-major (interleaved re/im).  Errors are DFM_ERR_IO with the
+ * reference's messages ("load_model: bad magic in <path>", "load_model:
+ * unsupported container version", "load_model: truncated file <path>", ...). */
+#define DFM_FMNM_VERSION 2u
+typedef struct dfm_fmnm_header {
+  uint32_t version, num_bins, num_frames, channels, n_sources, k_bases, n_blocks;
+  uint32_t sizes[DFM_MAX_BLOCKS];
+  uint32_t shared; /* share_spectrograms (1 model) or independent (1 per block) */
+  double floor;
+  uint64_t seed;
+  double sample_rate;
+  uint32_t window_len, hop_len, iterations, n_models;
+} dfm_fmnm_header;
+
+/* Element counts (doubles) of the four payload buffers; returns the total. */
+size_t dfm_fmnm_sizes(const dfm_fmnm_header* h, size_t* n_t, size_t* n_v, size_t* n_lam, size_t* n_w);
+int dfm_fmnm_write(const char* path, const dfm_fmnm_header* h, const double* T, const double* V,
+                   const double* lam, const double* w);
+int dfm_fmnm_read_header(const char* path, dfm_fmnm_header* h);
+int dfm_fmnm_read(const char* path, dfm_fmnm_header* h, double* T, double* V, double* lam, double* w);
 
 #ifdef __cplusplus
 }

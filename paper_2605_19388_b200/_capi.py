@@ -18,6 +18,20 @@ _vp = C.c_void_p
 _i = C.c_int
 _d = C.c_double
 _u64 = C.c_uint64
+_sz = C.c_size_t
+_cp = C.c_char_p
+
+DFM_MAX_BLOCKS = 32
+
+
+class FmnmHeader(C.Structure):
+    """dfm_fmnm_header (include/dfm_b200.h): the FMNM v2 container header."""
+    _fields_ = [("version", C.c_uint32), ("num_bins", C.c_uint32), ("num_frames", C.c_uint32),
+                ("channels", C.c_uint32), ("n_sources", C.c_uint32), ("k_bases", C.c_uint32),
+                ("n_blocks", C.c_uint32), ("sizes", C.c_uint32 * DFM_MAX_BLOCKS), ("shared", C.c_uint32),
+                ("floor", C.c_double), ("seed", C.c_uint64), ("sample_rate", C.c_double),
+                ("window_len", C.c_uint32), ("hop_len", C.c_uint32), ("iterations", C.c_uint32),
+                ("n_models", C.c_uint32)]
 
 # name: (restype, argtypes)
 _SIGS = {
@@ -33,6 +47,10 @@ _SIGS = {
     "dfm_nccl_get_unique_id": (_i, [_vp]),
     "dfm_fit": (_i, [_vp, _i, _vp, _vp, _vp]),
     "dfm_fit_many": (_i, [_vp, _i, _i, _vp, _vp]),
+    "dfm_fmnm_sizes": (_sz, [_vp, _vp, _vp, _vp, _vp]),
+    "dfm_fmnm_write": (_i, [_cp, _vp, _vp, _vp, _vp, _vp]),
+    "dfm_fmnm_read_header": (_i, [_cp, _vp]),
+    "dfm_fmnm_read": (_i, [_cp, _vp, _vp, _vp, _vp, _vp]),
     "dfm_bench_step_many": (_i, [_vp, _i, _vp]),
     "dfm_shard_begin": (_i, [_vp, _i]),
     "dfm_shard_numden": (_i, [_vp, _vp]),
@@ -80,6 +98,7 @@ DFM_ERR_SINGULAR = -3
 DFM_ERR_CUDA = -4
 DFM_ERR_NCCL = -5
 DFM_ERR_UNSUPPORTED = -6
+DFM_ERR_IO = -7
 
 
 class ShapeMismatchError(ValueError):
@@ -134,6 +153,8 @@ def check(rc: int, what: str = "") -> int:
         raise SingularDemixerError(msg)
     if rc == DFM_ERR_UNSUPPORTED:
         raise NotImplementedError(msg)
+    if rc == DFM_ERR_IO:  # std::runtime_error in the reference (io.cpp)
+        raise RuntimeError(last_error())
     raise DeviceError(msg)
 
 

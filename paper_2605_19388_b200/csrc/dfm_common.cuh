@@ -11,7 +11,9 @@
 #ifndef DFM_MAX_MB
 #define DFM_MAX_MB 16  // largest subarray (block) size the kernels accept
 #endif
+#ifndef DFM_MAX_BLOCKS
 #define DFM_MAX_BLOCKS 32
+#endif
 
 namespace dfm {
 
