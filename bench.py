@@ -493,6 +493,20 @@ def main():
         w_ms.append(v.value)
     w_ms = float(np.median(w_ms[1:]))
     w_bytes = 16.0 * (f1 - f0) * T * M * (1 + N)
+    # STFT / inverse STFT of this workload's shape (stft.cpp:74-141, the
+    # steps either side of the path): window 2 (F - 1), hop window / 4,
+    # T frames, M channels, signal resident on the device
+    sa, sb = _ct.c_double(), _ct.c_double()
+    n_win = 2 * (F - 1)
+    hop = n_win // 4
+    sig_len = (T - 1) * hop + n_win
+    dfm._capi.check(lib.dfm_bench_stft(sig_len, M, n_win, hop, 5, _ct.byref(sa), _ct.byref(sb), local))
+    x_bytes = 16.0 * F * T * M
+    stft = {"window": n_win, "hop": hop, "frames": T, "channels": M, "forward_ms": sa.value,
+            "inverse_ms": sb.value,
+            "alg_bytes_forward": 8.0 * sig_len * M + x_bytes, "alg_bytes_inverse": x_bytes + 8.0 * sig_len * M,
+            "forward_gbs": (8.0 * sig_len * M + x_bytes) / (sa.value * 1e-3) / 1e9,
+            "inverse_gbs": (x_bytes + 8.0 * sig_len * M) / (sb.value * 1e-3) / 1e9}
     pk = peaks()
     split_avg = np.mean(np.array(split), axis=0)
     names = ["k_em_bin", "k_tupd", "k_pd", "k_vupd", "k_spec"]
@@ -532,6 +546,7 @@ def main():
         "wiener": {"ms": w_ms, "alg_bytes": w_bytes, "achieved_gbs": w_bytes / (w_ms * 1e-3) / 1e9,
                    "frac_hbm": w_bytes / (w_ms * 1e-3) / 1e9 / pk["hbm_gbs"]},
         "dominant_kernel": names[dom],
+        "stft": stft,
         "e2e": {"value": e2e_value, "unit": "TF-bin*iter/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h),
                 "step": f"Engine.set_obs/set_model (pinned host X + init H2D), Engine.fit({args.e2e_iters}) "

@@ -67,6 +67,7 @@ extern "C" {
 #define DFM_ERR_NCCL -5
 #define DFM_ERR_UNSUPPORTED -6
 #define DFM_ERR_IO -7 /* file / container errors -> std::runtime_error */
+#define DFM_ERR_TOO_SHORT -8 /* SignalTooShort (types.hpp:27), an invalid_argument */
 
 typedef struct dfm_ctx dfm_ctx;
 
@@ -256,6 +257,25 @@ int dfm_fmnm_write(const char* path, const dfm_fmnm_header* h, const double* T, 
                    const double* lam, const double* w);
 int dfm_fmnm_read_header(const char* path, dfm_fmnm_header* h);
 int dfm_fmnm_read(const char* path, dfm_fmnm_header* h, double* T, double* V, double* lam, double* w);
+
+/* ---- STFT / inverse STFT (stft.hpp:27-40, stft.cpp:74-141) ------------
+ * Hann-window one-sided STFT and weighted overlap-add inverse on the device.
+ * signal / out: samples x channels, Eigen col-major ([channels][len]);
+ * X: ObsTensor layout, complex128 [F][T][M] (interleaved), F = window/2+1,
+ * T = dfm_stft_num_frames(len, window, hop).  Power-of-two windows use a
+ * radix-2 FFT, others the reference's direct DFT; windows up to 8192.
+ * Errors: window_len >= hop_len >= 1 (DFM_ERR_ARG), non-finite samples
+ * (DFM_ERR_ARG), DFM_ERR_TOO_SHORT when no full frame fits, and a bin count
+ * that does not match the window (DFM_ERR_SHAPE, inverse). */
+int dfm_stft_num_frames(int signal_len, int window_len, int hop_len);
+int dfm_stft_forward(const double* signal, int len, int channels, int window_len, int hop_len, double* out,
+                     int device);
+int dfm_stft_inverse(const double* x, int num_bins, int num_frames, int channels, int window_len, int hop_len,
+                     int out_len, double* out, int device);
+/* Bench hook: device time of one forward and one inverse transform of a
+ * resident signal (mean over reps). */
+int dfm_bench_stft(int len, int channels, int window_len, int hop_len, int reps, double* fwd_ms, double* inv_ms,
+                   int device);
 
 #ifdef __cplusplus
 }

@@ -48,6 +48,10 @@ _SIGS = {
     "dfm_fit": (_i, [_vp, _i, _vp, _vp, _vp]),
     "dfm_fit_many": (_i, [_vp, _i, _i, _vp, _vp]),
     "dfm_fmnm_sizes": (_sz, [_vp, _vp, _vp, _vp, _vp]),
+    "dfm_stft_num_frames": (_i, [_i, _i, _i]),
+    "dfm_stft_forward": (_i, [_vp, _i, _i, _i, _i, _vp, _i]),
+    "dfm_stft_inverse": (_i, [_vp, _i, _i, _i, _i, _i, _i, _vp, _i]),
+    "dfm_bench_stft": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _i]),
     "dfm_fmnm_write": (_i, [_cp, _vp, _vp, _vp, _vp, _vp]),
     "dfm_fmnm_read_header": (_i, [_cp, _vp]),
     "dfm_fmnm_read": (_i, [_cp, _vp, _vp, _vp, _vp, _vp]),
@@ -99,6 +103,7 @@ DFM_ERR_CUDA = -4
 DFM_ERR_NCCL = -5
 DFM_ERR_UNSUPPORTED = -6
 DFM_ERR_IO = -7
+DFM_ERR_TOO_SHORT = -8
 
 
 class ShapeMismatchError(ValueError):
@@ -111,6 +116,10 @@ class SingularDemixerError(RuntimeError):
 
 class NotPositiveDefiniteError(RuntimeError):
     """fastmnmf::NotPositiveDefinite (include/fastmnmf/types.hpp:21-23)."""
+
+
+class SignalTooShortError(ValueError):
+    """fastmnmf::SignalTooShort (include/fastmnmf/types.hpp:27-29)."""
 
 
 class DeviceError(RuntimeError):
@@ -153,6 +162,8 @@ def check(rc: int, what: str = "") -> int:
         raise SingularDemixerError(msg)
     if rc == DFM_ERR_UNSUPPORTED:
         raise NotImplementedError(msg)
+    if rc == DFM_ERR_TOO_SHORT:
+        raise SignalTooShortError(last_error())
     if rc == DFM_ERR_IO:  # std::runtime_error in the reference (io.cpp)
         raise RuntimeError(last_error())
     raise DeviceError(msg)

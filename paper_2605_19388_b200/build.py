@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdfm_b200.so")
-SOURCES = ["dfm_steps.cu", "dfm_engine.cu", "dfm_host.cpp", "dfm_io.cpp"]
+SOURCES = ["dfm_steps.cu", "dfm_engine.cu", "dfm_host.cpp", "dfm_io.cpp", "dfm_stft.cu"]
 HEADERS = ["dfm_common.cuh", "dfm_internal.cuh", "dfm_ip.cuh", "dfm_em.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
