@@ -105,6 +105,21 @@ void dfo_wiener_block(int F, int T, int M, const double* x, int nb, const int* s
                       int K, const double* Tm, const double* V, const double* lam,
                       const double* w, double floor_, double* images);
 
+/* ---- initialisation pipeline (dfm_init_oracle.c; init.cpp / hermlin.cpp) */
+int dfo_best_permutation(int L, int N, const double* cand, const double* ref, int* best);
+void dfo_align_frequency_permutations(int F, int T, int N, double* mask, int nbhd, int rounds);
+int dfo_cluster_masks(int F, int T, int M, const double* x, int N, uint64_t seed, int kmeans_iters, double temp,
+                      int nbhd, int rounds, double* mask);
+int dfo_align_subarray_permutations(int L, int F, int T, int N, const double* masks, int* perms);
+void dfo_init_scm(int F, int T, int M, int N, const double* x, int nb, const int* sizes, const double* masks,
+                  double* R);
+void dfo_init_spectrogram(int F, int T, int M, int N, const double* x, int nb, const int* sizes,
+                          const double* masks, const double* R, double* h0);
+void dfo_is_nmf(int F, int T, int N, int K, const double* h0, int max_iters, uint64_t seed, double* Tm,
+                double* V, double* trace, int* iters_out);
+int dfo_gevd(int m, const double* A, const double* B, double* w_out, double* d_out);
+int dfo_init_spatial(int F, int M, int N, int nb, const int* sizes, const double* R, double* w0, double* lambda0);
+
 #ifdef __cplusplus
 }
 #endif
