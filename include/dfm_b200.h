@@ -277,6 +277,34 @@ int dfm_stft_inverse(const double* x, int num_bins, int num_frames, int channels
 int dfm_bench_stft(int len, int channels, int window_len, int hop_len, int reps, double* fwd_ms, double* inv_ms,
                    int device);
 
+/* ---- initialisation pipeline (init.hpp:44-111, init.cpp:76-523) --------
+ * Device k-means soft masks, masked SCMs + ML spectrograms, IS-NMF and GEVD
+ * spatial start; host permutation alignment.  Reference layouts (Eigen
+ * col-major): x [F][T][M] complex; mask / h0 [F] x (T x N) = [F][N][T];
+ * R [N][F] x (M x M) complex; T [N] x (F x K); V [N] x (K x T);
+ * lambda0 [F] x (N x M); w0 [block][F] x (mb x mb) complex.
+ * GEVD eigenvector phases follow a canonical rule (largest-magnitude entry
+ * real positive); the reference's Eigen solver phases are not reproduced. */
+int dfm_cluster_masks(const double* x, int F, int T, int M, int N, uint64_t seed, int kmeans_iters,
+                      double temperature, int neighborhood, int rounds, double* mask, int device);
+int dfm_align_frequency_permutations(double* mask, int F, int T, int N, int neighborhood, int rounds);
+/* masks: L x [F][N][T]; perms: L x N (perms[l][n] = source of mask l matched to n) */
+int dfm_align_subarray_permutations(const double* masks, int L, int F, int T, int N, int* perms);
+/* masks: one per block, nblocks x [F][N][T] */
+int dfm_init_scm_spectrogram(const double* x, int F, int T, int M, int N, int nblocks, const int* sizes,
+                             const double* masks, double* R, double* h0, int device);
+/* trace: N x (max_iters+1) divergences (NaN past each source's stop), may be NULL */
+int dfm_is_nmf(const double* h0, int F, int T, int N, int K, int max_iters, uint64_t seed, double* T_out,
+               double* V_out, double* trace, int* iters_out, int device);
+int dfm_init_spatial(const double* R, int F, int M, int N, int nblocks, const int* sizes, double* w0,
+                     double* lambda0, int device);
+/* init_distributed (nblocks > 1) / init_full (one block): the whole pipeline.
+ * h0_out, mask_out (the first subarray's aligned mask) may be NULL. */
+int dfm_init_pipeline(const double* x, int F, int T, int nblocks, const int* sizes, int N, int K, uint64_t seed,
+                      int nmf_iters, int kmeans_iters, double temperature, int neighborhood, int rounds,
+                      double* T_out, double* V_out, double* lambda0, double* w0, double* h0_out, double* mask_out,
+                      int device);
+
 #ifdef __cplusplus
 }
 #endif

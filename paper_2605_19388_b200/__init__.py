@@ -9,7 +9,7 @@ from .fastmnmf import (  # noqa: F401
     ip_update_block, ip_update_w, kFloor, mm_update_lambda, mm_update_t, mm_update_v, power_of,
     fit_many, random_init, random_observations, slice_init, wiener_block, wiener_full)
 
-from . import container, stft  # noqa: F401,E402
+from . import container, init, stft  # noqa: F401,E402
 from ._capi import SignalTooShortError  # noqa: F401,E402
 
 __all__ = [n for n in dir() if not n.startswith("_")]

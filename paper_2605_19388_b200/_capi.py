@@ -49,6 +49,14 @@ _SIGS = {
     "dfm_fit_many": (_i, [_vp, _i, _i, _vp, _vp]),
     "dfm_fmnm_sizes": (_sz, [_vp, _vp, _vp, _vp, _vp]),
     "dfm_stft_num_frames": (_i, [_i, _i, _i]),
+    "dfm_cluster_masks": (_i, [_vp, _i, _i, _i, _i, _u64, _i, _d, _i, _i, _vp, _i]),
+    "dfm_align_frequency_permutations": (_i, [_vp, _i, _i, _i, _i, _i]),
+    "dfm_align_subarray_permutations": (_i, [_vp, _i, _i, _i, _i, _vp]),
+    "dfm_init_scm_spectrogram": (_i, [_vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _i]),
+    "dfm_is_nmf": (_i, [_vp, _i, _i, _i, _i, _i, _u64, _vp, _vp, _vp, _vp, _i]),
+    "dfm_init_spatial": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _vp, _i]),
+    "dfm_init_pipeline": (_i, [_vp, _i, _i, _i, _vp, _i, _i, _u64, _i, _i, _d, _i, _i, _vp, _vp, _vp, _vp, _vp,
+                               _vp, _i]),
     "dfm_stft_forward": (_i, [_vp, _i, _i, _i, _i, _vp, _i]),
     "dfm_stft_inverse": (_i, [_vp, _i, _i, _i, _i, _i, _i, _vp, _i]),
     "dfm_bench_stft": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _i]),

@@ -600,7 +600,7 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
   em_stamp(a, 5);
 }
 
-__global__ void k_vapply(size_t nkt, const double* __restrict__ numden, double* __restrict__ V,
+static __global__ void k_vapply(size_t nkt, const double* __restrict__ numden, double* __restrict__ V,
                          double floor_) {
   const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   if (i >= nkt) return;
@@ -680,11 +680,13 @@ template <int KT>
 __global__ void __launch_bounds__(32 * kTupdWarps, KT <= 2 ? 3 : 2) k_tupd_mma(int F, int T, int N, int K, double* __restrict__ Tf,
                                                              const double* __restrict__ V,
                                                              const double* __restrict__ Aw,
-                                                             const double* __restrict__ Bw, double floor_) {
+                                                             const double* __restrict__ Bw, double floor_,
+                                                             const int* __restrict__ skip) {
   __shared__ double part[kTupdWarps / 2][2][KT][64];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
   const int n = blockIdx.y, f0 = blockIdx.x * 8;
+  if (skip && skip[n]) return;  // IS-NMF: this source has converged
   constexpr int kt = KT;
   const int steps = (T + 3) / 4;
   const int per = (steps + kTupdWarps - 1) / kTupdWarps;
@@ -766,11 +768,12 @@ __global__ void __launch_bounds__(32 * kVupdMWarps, KT <= 2 ? 3 : 2) k_vupd_mma(
                                                               const double* __restrict__ Aw,
                                                               const double* __restrict__ Bw,
                                                               double* __restrict__ V, double* __restrict__ numden,
-                                                              double floor_) {
+                                                              double floor_, const int* __restrict__ skip) {
   __shared__ double part[kVupdMWarps / 2][2][KT][64];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
   const int n = blockIdx.y, t0 = blockIdx.x * 8;
+  if (skip && skip[n]) return;  // IS-NMF: this source has converged
   constexpr int kt = KT;
   const int steps = (F + 3) / 4;
   const int per = (steps + kVupdMWarps - 1) / kVupdMWarps;

@@ -34,11 +34,6 @@
 
 #include "dfm_internal.cuh"
 
-namespace dfm {
-constexpr int kMaxN = 8;   // sources held in registers
-constexpr int kMaxK = 64;  // NMF bases
-}  // namespace dfm
-
 #include "dfm_ip.cuh"
 #include "dfm_em.cuh"
 
@@ -287,7 +282,8 @@ void launch_tupd(dfm_ctx* c) {
     case 3: case 4: kern = k_tupd_mma<4>; break;
     default: kern = k_tupd_mma<8>; break;
   }
-  kern<<<grid, 32 * kTupdWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->V.p, c->Aw.p, c->Bw.p, c->floor_);
+  kern<<<grid, 32 * kTupdWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->V.p, c->Aw.p, c->Bw.p, c->floor_,
+                                                nullptr);
   DFM_CK_LAUNCH();
   c->launches++;
 }
@@ -313,7 +309,7 @@ void launch_vupd(dfm_ctx* c) {
     default: kern = k_vupd_mma<8>; break;
   }
   kern<<<grid, 32 * kVupdMWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->Aw.p, c->Bw.p, c->V.p,
-                                                 sharded ? c->numden.p : nullptr, c->floor_);
+                                                 sharded ? c->numden.p : nullptr, c->floor_, nullptr);
   DFM_CK_LAUNCH();
   c->launches++;
   if (sharded && !c->host_exchange) {

@@ -12,6 +12,9 @@
 
 namespace dfm {
 
+constexpr int kMaxN = 8;   // sources held in registers by the EM kernels
+constexpr int kMaxK = 64;  // NMF bases
+
 void set_error(const std::string& msg);
 
 struct CudaError {

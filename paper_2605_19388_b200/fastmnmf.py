@@ -180,11 +180,15 @@ class FitOptions:
 
 @dataclass
 class InitBundle:
-    """init.hpp:69-77 (the fields the EM path consumes)."""
+    """init.hpp:69-77: the EM starting point (layout, nmf, w0, lambda0) plus,
+    from the initialisation pipeline (paper_2605_19388_b200.init), the ML
+    spectrograms h0 and the reference subarray's aligned soft mask."""
     layout: BlockLayout
     nmf: NmfModel
     w0: List[np.ndarray]   # [block] (F, mb, mb)
     lambda0: np.ndarray    # (F, N, M)
+    h0: Optional[np.ndarray] = None    # (F, T, N)
+    mask: Optional[np.ndarray] = None  # (F, T, N)
 
 
 @dataclass
