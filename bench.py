@@ -230,6 +230,46 @@ def run_reference(args, c, world, rank):
     }
 
 
+def init_measurement(c, x, local, cpu_sample=True):
+    """The initialisation pipeline (init_distributed, init.cpp:438-472) for
+    this workload: device wall time of one dfm_init_pipeline call (host X in,
+    model out, IS-NMF up to 1000 iterations), and the oracle's CPU time on a
+    bounded sample (all host threads; k-means/alignment/SCM/GEVD in full,
+    IS-NMF timed over 20 iterations and reported per iteration)."""
+    import paper_2605_19388_b200 as dfm
+    from paper_2605_19388_b200 import init as dinit
+
+    layout = dfm.BlockLayout(c["sizes"])
+    cfg = dinit.InitConfig(num_sources=c["N"], k_bases=c["K"], nmf_max_iters=1000)
+    dinit.init_distributed(x[:8], layout, dinit.InitConfig(c["N"], c["K"], 5), 1)  # warm-up (module load)
+    t0 = time.perf_counter()
+    b = dinit.init_distributed(x, layout, cfg, SEED_INIT)
+    dev_s = time.perf_counter() - t0
+    out = {"step": "init_distributed (k-means masks, alignment, SCM/h0, IS-NMF <= 1000 iters, GEVD) through "
+                   "paper_2605_19388_b200.init, host X in / model out",
+           "device_seconds": dev_s, "nmf_max_iters": 1000, "lambda0_min": float(b.lambda0.min())}
+    if cpu_sample:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle
+        import init_oracle
+
+        oracle.build()
+        oracle.set_threads(os.cpu_count() or 1)
+        t0 = time.perf_counter()
+        init_oracle.init_distributed(x, c["sizes"], c["N"], c["K"], SEED_INIT, nmf_iters=0)
+        t_rest = time.perf_counter() - t0
+        h0 = b.h0
+        t0 = time.perf_counter()
+        init_oracle.is_nmf(h0, c["K"], 20, 7)
+        t_nmf = (time.perf_counter() - t0) / 20
+        out["cpu_baseline"] = {"kind": "port", "cores": os.cpu_count() or 1,
+                               "seconds_without_nmf": t_rest, "seconds_per_nmf_iter": t_nmf,
+                               "seconds_extrapolated_1000_iters": t_rest + 1000 * t_nmf,
+                               "sample": "oracle/ init_distributed without IS-NMF in full + 20 IS-NMF iterations "
+                                         "(OpenMP over sources/bins)"}
+    return out
+
+
 def run_batch(args, c, world, rank, local):
     """config 4: independent mixtures, one context each, no communication."""
     import ctypes
@@ -355,6 +395,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tiling", default="", help="FT,TB override: frame tile of the per-bin kernel and of k_pd")
     ap.add_argument("--batch", type=int, default=0, help="config4: number of mixtures (default 64)")
+    ap.add_argument("--no-init", action="store_true", help="skip the initialisation-pipeline measurement")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     c = CONFIGS[args.workload]
@@ -556,6 +597,8 @@ def main():
         "clocks": clocks,
         "paper_cpu_tfbin_iter_per_s_other_config": PAPER_CPU_TFBIN,
     }
+    if world == 1 and not args.no_init:
+        line["init_pipeline"] = init_measurement(c, x, local, cpu_sample=not args.no_cpu_baseline)
     if world == 1 and not args.no_cpu_baseline:
         init_d = dict(T=init.nmf.T, V=init.nmf.V, lam=init.lambda0, w=init.w0)
         line["cpu_baseline"] = cpu_baseline(c, x, init_d, threads=1)
