@@ -949,8 +949,81 @@ __global__ void __launch_bounds__(128) k_power(const EmArgs a) {
 // h from H; every per-frame value in registers; each source's image tile is
 // staged in shared memory and written with coalesced 16-byte stores.
 constexpr int kWienFT = 128;
+
+// (W_b^H)^-1 of one block in registers (compile-time size): the algorithm of
+// k_wh_inverse (partial-pivot LU of W^H, then one solve per column), whose
+// result it reproduces; w and g are col-major MB x MB
+template <int MB>
+__device__ __forceinline__ void wh_inverse_regs(const cd* w, cd* g) {
+  cd lu[MB * MB];
+  int perm[MB];
+#pragma unroll
+  for (int c = 0; c < MB; ++c)
+#pragma unroll
+    for (int r = 0; r < MB; ++r) lu[c * MB + r] = conjg(w[r * MB + c]);
+#pragma unroll
+  for (int k = 0; k < MB; ++k) {
+    int piv = k;
+    double best = hypot(lu[k * MB + k].re, lu[k * MB + k].im);
+#pragma unroll
+    for (int r = k + 1; r < MB; ++r) {
+      const double v = hypot(lu[k * MB + r].re, lu[k * MB + r].im);
+      if (v > best) {
+        best = v;
+        piv = r;
+      }
+    }
+    perm[k] = piv;
+    if (best != 0.0) {
+#pragma unroll
+      for (int r = k + 1; r < MB; ++r)
+        if (piv == r)
+#pragma unroll
+          for (int c = 0; c < MB; ++c) {
+            const cd t = lu[c * MB + k];
+            lu[c * MB + k] = lu[c * MB + r];
+            lu[c * MB + r] = t;
+          }
+      const cd d = lu[k * MB + k];
+#pragma unroll
+      for (int r = k + 1; r < MB; ++r) lu[k * MB + r] = cdiv(lu[k * MB + r], d);
+    }
+#pragma unroll
+    for (int c = k + 1; c < MB; ++c)
+#pragma unroll
+      for (int r = k + 1; r < MB; ++r) lu[c * MB + r] = lu[c * MB + r] - lu[k * MB + r] * lu[c * MB + k];
+  }
+#pragma unroll
+  for (int col = 0; col < MB; ++col) {
+    cd v[MB];
+#pragma unroll
+    for (int r = 0; r < MB; ++r) v[r] = cd{r == col ? 1.0 : 0.0, 0.0};
+#pragma unroll
+    for (int k = 0; k < MB; ++k)
+#pragma unroll
+      for (int r = k + 1; r < MB; ++r)
+        if (perm[k] == r) {
+          const cd t = v[k];
+          v[k] = v[r];
+          v[r] = t;
+        }
+#pragma unroll
+    for (int r = 1; r < MB; ++r)
+#pragma unroll
+      for (int c = 0; c < r; ++c) v[r] = v[r] - lu[c * MB + r] * v[c];
+#pragma unroll
+    for (int r = MB - 1; r >= 0; --r) {
+#pragma unroll
+      for (int c = r + 1; c < MB; ++c) v[r] = v[r] - lu[c * MB + r] * v[c];
+      v[r] = cdiv(v[r], lu[r * MB + r]);
+    }
+#pragma unroll
+    for (int r = 0; r < MB; ++r) g[col * MB + r] = v[r];
+  }
+}
+
 template <int MB_, int NB_, int NS_, int MAXMB>
-__global__ void __launch_bounds__(kWienFT) k_wiener_ctx(const EmArgs a, const cd* __restrict__ G,
+__global__ void __launch_bounds__(kWienFT, 4) k_wiener_ctx(const EmArgs a, const cd* __restrict__ G,
                                                         cd* __restrict__ images) {
   constexpr bool SB = MB_ > 0 && NB_ > 0;
   extern __shared__ __align__(16) unsigned char swn[];
@@ -962,18 +1035,22 @@ __global__ void __launch_bounds__(kWienFT) k_wiener_ctx(const EmArgs a, const cd
   auto MBof = [&](int b) { return SB ? MB_ : a.mb[b]; };
   auto OFF = [&](int b) { return SB ? b * MB_ : a.off[b]; };
   auto WOFF = [&](int b) { return SB ? b * MB_ * MB_ : a.woff[b]; };
+  const int Mp = M + 1;          // padded stage row: conflict-free 16-byte rows
   cd* Ws = (cd*)swn;             // [wsz]
   cd* Gs = Ws + wsz;             // [wsz]
-  cd* stage = Gs + wsz;          // [FT][M]
-  double* Ls = (double*)(stage + (size_t)kWienFT * M);  // [N][M]
+  cd* stage = Gs + wsz;          // [FT][M + 1]
+  double* Ls = (double*)(stage + (size_t)kWienFT * Mp);  // [N][M]
   const int f = blockIdx.y, t0 = blockIdx.x * kWienFT, tid = threadIdx.x;
   const int tn = min(kWienFT, T - t0);
-  for (int e = tid; e < wsz; e += kWienFT) {
-    Ws[e] = a.W[(size_t)f * wsz + e];
-    Gs[e] = G[(size_t)f * wsz + e];
-  }
+  for (int e = tid; e < wsz; e += kWienFT) Ws[e] = a.W[(size_t)f * wsz + e];
+  if (!SB)
+    for (int e = tid; e < wsz; e += kWienFT) Gs[e] = G[(size_t)f * wsz + e];
   for (int e = tid; e < N * M; e += kWienFT) Ls[e] = a.lam[(size_t)f * N * M + e];
   __syncthreads();
+  if constexpr (SB) {  // (W_b^H)^-1 of this bin's blocks, one thread each (wiener.cpp:25)
+    if (tid < NB_) wh_inverse_regs<MB_>(Ws + tid * MB_ * MB_, Gs + tid * MB_ * MB_);
+    __syncthreads();
+  }
   const int t = t0 + tid;
   const bool act = tid < tn;
   double h[kMaxN];
@@ -1003,10 +1080,13 @@ __global__ void __launch_bounds__(kWienFT) k_wiener_ctx(const EmArgs a, const cd
 #pragma unroll
           for (int n = 0; n < kMaxN; ++n)
             if (n < N) e += h[n] * Ls[n * M + b * MB_ + mu];
-          eta[b * MB_ + mu] = fmax(e, a.floor_);
+          eta[b * MB_ + mu] = rcp_pos(fmax(e, a.floor_));  // 1 / eta
         }
     }
   }
+  // each warp stages and stores its own 32 frames: no CTA-wide barrier per source
+  const int lane = tid & 31, wbase = tid & ~31;
+  const int wn = max(0, min(32, tn - wbase));
   for (int n = 0; n < N; ++n) {
     if (act) {
       if constexpr (SB) {
@@ -1015,7 +1095,7 @@ __global__ void __launch_bounds__(kWienFT) k_wiener_ctx(const EmArgs a, const cd
           cd sc[MB_];
 #pragma unroll
           for (int mu = 0; mu < MB_; ++mu) {
-            const double gain = (h[n] * Ls[n * M + b * MB_ + mu]) / eta[b * MB_ + mu];
+            const double gain = (h[n] * Ls[n * M + b * MB_ + mu]) * eta[b * MB_ + mu];
             sc[mu] = y[b * MB_ + mu] * gain;
           }
           const cd* gb = Gs + b * MB_ * MB_;
@@ -1024,7 +1104,7 @@ __global__ void __launch_bounds__(kWienFT) k_wiener_ctx(const EmArgs a, const cd
             cd s{0.0, 0.0};
 #pragma unroll
             for (int c = 0; c < MB_; ++c) s = s + gb[c * MB_ + r] * sc[c];
-            stage[tid * M + b * MB_ + r] = s;
+            stage[tid * Mp + b * MB_ + r] = s;
           }
         }
       } else {
@@ -1047,19 +1127,21 @@ __global__ void __launch_bounds__(kWienFT) k_wiener_ctx(const EmArgs a, const cd
               const double gain = (h[n] * Ls[n * M + off + c]) / fmax(e, a.floor_);
               s = s + gb[c * mb + r] * (yc * gain);
             }
-            stage[tid * M + off + r] = s;
+            stage[tid * Mp + off + r] = s;
           }
         }
       }
     }
-    __syncthreads();
-    // coalesced copy of the tile (tn frames x M, contiguous in images)
-    cd* dst = images + (((size_t)n * a.F + f) * T + t0) * M;
-    for (int e = tid; e < tn * M; e += kWienFT) {
-      const cd v = stage[e];
+    __syncwarp();
+    // coalesced copy of the warp's rows (wn frames x M, contiguous in images)
+    cd* dst = images + (((size_t)n * a.F + f) * T + t0 + wbase) * M;
+    const cd* src = stage + (size_t)wbase * Mp;
+    for (int e = lane; e < wn * M; e += 32) {
+      const int row = e / M;
+      const cd v = src[e + row];  // row * (M + 1) + col
       *reinterpret_cast<double2*>(dst + e) = make_double2(v.re, v.im);
     }
-    __syncthreads();
+    __syncwarp();
   }
 }
 }  // namespace dfm

@@ -101,6 +101,7 @@ struct dfm_ctx {
   void (*kpdw)(EmArgs) = nullptr;
   void (*kpow)(EmArgs) = nullptr;
   void (*kwien)(EmArgs, const cd*, cd*) = nullptr;
+  bool static_shapes = false;  // compile-time-shape instantiations selected
   bool force_generic = false;
   int FT = 128, TB = 128, smem_em = 0;
   int req_FT = 0, req_TB = 0;
@@ -183,6 +184,7 @@ void select_kernels(dfm_ctx* c) {
       c->kem = k_em_bin<12, 1, 5, 12>; c->kpdw = k_pdw<12, 1, 5, 12>; c->kpow = k_power<12, 1, 5, 12>; c->kwien = k_wiener_ctx<12, 1, 5, 12>; c->kmaxmb = 12;
     }
   }
+  c->static_shapes = c->kem != nullptr;
   if (!c->kem) {
     if (c->maxmb <= 4) {
       c->kem = k_em_bin<0, 0, 0, 4>; c->kpdw = k_pdw<0, 0, 0, 4>; c->kpow = k_power<0, 0, 0, 4>; c->kwien = k_wiener_ctx<0, 0, 0, 4>; c->kmaxmb = 4;
@@ -379,15 +381,16 @@ void run_step(dfm_ctx* c, bool split) {
 // [N][F][T][M]: (W^H)^-1 per (bin, block), H = T V, then k_wiener_ctx.
 void launch_wiener_ctx(dfm_ctx* c, cd* img) {
   if (c->Ginv.n < (size_t)c->F * c->L.wsz) c->Ginv.alloc((size_t)c->F * c->L.wsz);
-  launch_wh_inverse(c->F, c->L, c->W.p, c->L.wsz, c->Ginv.p, c->stream);
+  // the static-shape kernels invert W^H per CTA in registers
+  if (!c->static_shapes) launch_wh_inverse(c->F, c->L, c->W.p, c->L.wsz, c->Ginv.p, c->stream);
   launch_spec(c);
-  const size_t smem = (size_t)(2 * c->L.wsz + kWienFT * c->M) * sizeof(cd) + (size_t)c->N * c->M * 8;
+  const size_t smem = (size_t)(2 * c->L.wsz + kWienFT * (c->M + 1)) * sizeof(cd) + (size_t)c->N * c->M * 8;
   DFM_CK(cudaFuncSetAttribute(c->kwien, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const EmArgs a = make_args(c);
   const dim3 grid((c->T + kWienFT - 1) / kWienFT, c->F);
   c->kwien<<<grid, kWienFT, smem, c->stream>>>(a, c->Ginv.p, img);
   DFM_CK_LAUNCH();
-  c->launches += 3;
+  c->launches += c->static_shapes ? 2 : 3;
 }
 
 }  // namespace
