@@ -550,7 +550,7 @@ def main():
             "inverse_gbs": (x_bytes + 8.0 * sig_len * M) / (sb.value * 1e-3) / 1e9}
     pk = peaks()
     split_avg = np.mean(np.array(split), axis=0)
-    names = ["k_em_bin", "k_tupd", "k_pd", "k_vupd", "k_spec"]
+    names = ["k_em_bin", "k_tupd+h", "k_pdw", "k_vupd+H", "tail"]
     dom = int(np.argmax(split_avg))
     bin_avg = float(split_avg[0])
     ab_bin = alg_bytes_bin_kernel(c) * (f1 - f0) / F

@@ -671,6 +671,80 @@ __global__ void __launch_bounds__(32 * kSpecWarps) k_spec_mma(int F, int T, int 
   }
 }
 
+// H = T V for one source n, fused into the update kernels (same DMMA k-step
+// order as k_spec_mma, so H is bitwise the same).  spec_rows: bins f0..f0+7,
+// every frame (warps stride over 8-frame tiles); spec_cols: frames t0..t0+7,
+// every bin (warps stride over 8-bin tiles).
+template <int KS>
+__device__ __forceinline__ void spec_rows(int F, int T, int N, int K, int n, int f0, const double* __restrict__ Tf,
+                                          const double* __restrict__ V, double* __restrict__ H, int warp, int nwarps,
+                                          int lane) {
+  const int g = lane >> 2, q = lane & 3, f = f0 + g;
+  double a[KS];
+#pragma unroll
+  for (int s = 0; s < KS; ++s) {
+    const int k = 4 * s + q;
+    a[s] = (f < F && k < K) ? Tf[((size_t)f * N + n) * K + k] : 0.0;
+  }
+  for (int tile = warp; tile * 8 < T; tile += nwarps) {
+    const int tl = tile * 8 + g;
+    double b[KS];
+#pragma unroll
+    for (int s = 0; s < KS; ++s) {
+      const int k = 4 * s + q;
+      b[s] = (k < K && tl < T) ? __ldg(V + ((size_t)n * K + k) * T + tl) : 0.0;
+    }
+    double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+    for (int s = 0; s < KS; ++s) dmma(c0, c1, a[s], b[s]);
+    const int t = tile * 8 + 2 * q;
+    if (f < F) {
+      double* hp = H + ((size_t)f * N + n) * T;
+      if (!(T & 1) && t + 1 < T) {
+        *reinterpret_cast<double2*>(hp + t) = make_double2(c0, c1);
+      } else {
+        if (t < T) hp[t] = c0;
+        if (t + 1 < T) hp[t + 1] = c1;
+      }
+    }
+  }
+}
+
+template <int KS>
+__device__ __forceinline__ void spec_cols(int F, int T, int N, int K, int n, int t0, const double* __restrict__ Tf,
+                                          const double* __restrict__ V, double* __restrict__ H, int warp, int nwarps,
+                                          int lane) {
+  const int g = lane >> 2, q = lane & 3, tl = t0 + g;
+  double b[KS];
+#pragma unroll
+  for (int s = 0; s < KS; ++s) {
+    const int k = 4 * s + q;
+    b[s] = (k < K && tl < T) ? V[((size_t)n * K + k) * T + tl] : 0.0;
+  }
+  const int t = t0 + 2 * q;
+  for (int tile = warp; tile * 8 < F; tile += nwarps) {
+    const int f = tile * 8 + g;
+    double a[KS];
+#pragma unroll
+    for (int s = 0; s < KS; ++s) {
+      const int k = 4 * s + q;
+      a[s] = (f < F && k < K) ? __ldg(Tf + ((size_t)f * N + n) * K + k) : 0.0;
+    }
+    double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+    for (int s = 0; s < KS; ++s) dmma(c0, c1, a[s], b[s]);
+    if (f < F) {
+      double* hp = H + ((size_t)f * N + n) * T;
+      if (!(T & 1) && t + 1 < T) {
+        *reinterpret_cast<double2*>(hp + t) = make_double2(c0, c1);
+      } else {
+        if (t < T) hp[t] = c0;
+        if (t + 1 < T) hp[t + 1] = c1;
+      }
+    }
+  }
+}
+
 // T update (engine.cpp:115-123): num[f][k] = sum_t A[n][f][t] V[n][k][t],
 // den likewise with B.  CTA = (8 bins, source); its 4 warps split the frames,
 // partials are added in warp order, then the multiplicative update.
@@ -681,7 +755,7 @@ __global__ void __launch_bounds__(32 * kTupdWarps, KT <= 2 ? 3 : 2) k_tupd_mma(i
                                                              const double* __restrict__ V,
                                                              const double* __restrict__ Aw,
                                                              const double* __restrict__ Bw, double floor_,
-                                                             const int* __restrict__ skip) {
+                                                             const int* __restrict__ skip, double* __restrict__ Hout) {
   __shared__ double part[kTupdWarps / 2][2][KT][64];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
@@ -744,18 +818,22 @@ __global__ void __launch_bounds__(32 * kTupdWarps, KT <= 2 ? 3 : 2) k_tupd_mma(i
     __syncthreads();
   }
   __syncthreads();
-  if (warp != 0 || f >= F) return;
+  if (warp == 0 && f < F) {
 #pragma unroll
-  for (int j = 0; j < KT; ++j)
-    if (j < kt)
+    for (int j = 0; j < KT; ++j)
+      if (j < kt)
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int k = 8 * j + 2 * q + i;
-        if (k >= K) continue;
-        const double nu = num[j][i], de = den[j][i];
-        double* tp = Tf + ((size_t)f * N + n) * K + k;
-        *tp = fmax(*tp * sqrt(nu / fmax(de, floor_)), floor_);
-      }
+        for (int i = 0; i < 2; ++i) {
+          const int k = 8 * j + 2 * q + i;
+          if (k >= K) continue;
+          const double nu = num[j][i], de = den[j][i];
+          double* tp = Tf + ((size_t)f * N + n) * K + k;
+          *tp = fmax(*tp * sqrt(nu / fmax(de, floor_)), floor_);
+        }
+  }
+  if (!Hout) return;
+  __syncthreads();  // the CTA's new T rows are visible
+  spec_rows<2 * KT>(F, T, N, K, n, f0, Tf, V, Hout, warp, kTupdWarps, lane);  // h' = T_new V
 }
 
 // V update (engine.cpp:125-133): num[k][t] = sum_f T[f][n][k] A'[n][f][t].
@@ -768,7 +846,8 @@ __global__ void __launch_bounds__(32 * kVupdMWarps, KT <= 2 ? 3 : 2) k_vupd_mma(
                                                               const double* __restrict__ Aw,
                                                               const double* __restrict__ Bw,
                                                               double* __restrict__ V, double* __restrict__ numden,
-                                                              double floor_, const int* __restrict__ skip) {
+                                                              double floor_, const int* __restrict__ skip,
+                                                              double* __restrict__ Hout) {
   __shared__ double part[kVupdMWarps / 2][2][KT][64];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
@@ -829,23 +908,27 @@ __global__ void __launch_bounds__(32 * kVupdMWarps, KT <= 2 ? 3 : 2) k_vupd_mma(
     __syncthreads();
   }
   __syncthreads();
-  if (warp != 0) return;
+  if (warp == 0) {
 #pragma unroll
-  for (int j = 0; j < KT; ++j)
-    if (j < kt)
+    for (int j = 0; j < KT; ++j)
+      if (j < kt)
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int k = 8 * j + g, t = t0 + 2 * q + i;
-        if (k >= K || t >= T) continue;
-        const double nu = num[j][i], de = den[j][i];
-        const size_t o = ((size_t)n * K + k) * T + t;
-        if (numden) {
-          numden[o] = nu;
-          numden[(size_t)N * K * T + o] = de;
-        } else {
-          V[o] = fmax(V[o] * sqrt(nu / fmax(de, floor_)), floor_);
+        for (int i = 0; i < 2; ++i) {
+          const int k = 8 * j + g, t = t0 + 2 * q + i;
+          if (k >= K || t >= T) continue;
+          const double nu = num[j][i], de = den[j][i];
+          const size_t o = ((size_t)n * K + k) * T + t;
+          if (numden) {
+            numden[o] = nu;
+            numden[(size_t)N * K * T + o] = de;
+          } else {
+            V[o] = fmax(V[o] * sqrt(nu / fmax(de, floor_)), floor_);
+          }
         }
-      }
+  }
+  if (!Hout || numden) return;  // sharded: V is final only after the allreduce
+  __syncthreads();  // the CTA's new V columns are visible
+  spec_cols<2 * KT>(F, T, N, K, n, t0, Tf, V, Hout, warp, kVupdMWarps, lane);  // H = T V_new
 }
 
 // Pass D as an elementwise kernel over (bin, frame): h' from H (= T_new V by

@@ -112,6 +112,7 @@ struct dfm_ctx {
   long long launches = 0;
   cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   cudaGraphExec_t step_exec = nullptr;  // one steady-state iteration
+  long long graph_launches = 0;         // kernels in one replay
   int dbg = 0;
   bool host_exchange = false;  // shard stepping API: {num, den} exchanged by the caller
   int xs_iter = 0, xs_iters = 0;
@@ -284,15 +285,16 @@ void launch_tupd(dfm_ctx* c) {
     case 3: case 4: kern = k_tupd_mma<4>; break;
     default: kern = k_tupd_mma<8>; break;
   }
+  // h' = T_new V fused into the T update
   kern<<<grid, 32 * kTupdWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->V.p, c->Aw.p, c->Bw.p, c->floor_,
-                                                nullptr);
+                                                nullptr, c->H.p);
   DFM_CK_LAUNCH();
   c->launches++;
 }
 
-// pass D: h' = T_new V into H (DMMA), then the elementwise V-update weights
+// pass D: the elementwise V-update weights from h' (= T_new V, written by the
+// fused T update)
 void launch_pd(dfm_ctx* c) {
-  launch_spec(c);
   EmArgs a = make_args(c);
   const dim3 grid((c->T + c->TB - 1) / c->TB, c->F);
   c->kpdw<<<grid, c->TB, 0, c->stream>>>(a);
@@ -311,7 +313,8 @@ void launch_vupd(dfm_ctx* c) {
     default: kern = k_vupd_mma<8>; break;
   }
   kern<<<grid, 32 * kVupdMWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->Aw.p, c->Bw.p, c->V.p,
-                                                 sharded ? c->numden.p : nullptr, c->floor_, nullptr);
+                                                 sharded ? c->numden.p : nullptr, c->floor_, nullptr,
+                                                 sharded ? nullptr : c->H.p);  // H = T V_new fused (one GPU)
   DFM_CK_LAUNCH();
   c->launches++;
   if (sharded && !c->host_exchange) {
@@ -332,7 +335,10 @@ void launch_rest(dfm_ctx* c, cudaEvent_t* ev) {
   if (ev) DFM_CK(cudaEventRecord(ev[3], c->stream));
   launch_vupd(c);
   if (ev) DFM_CK(cudaEventRecord(ev[4], c->stream));
-  if (!c->host_exchange) launch_spec(c);  // else: after the caller's exchange
+  // H for the next k_em_bin: fused into k_vupd on one GPU; after the
+  // allreduce (or the caller's exchange) when sharded
+  const bool sharded = (c->comm != nullptr && c->nranks > 1) || c->host_exchange;
+  if (sharded && !c->host_exchange) launch_spec(c);
 }
 
 void drop_graph(dfm_ctx* c) {
@@ -354,6 +360,7 @@ bool step_graph(dfm_ctx* c) {
   launch_em(c, 2, 1, 0, c->cost_step.p);
   launch_rest(c, nullptr);
   DFM_CK(cudaStreamEndCapture(c->stream, &g));
+  c->graph_launches = c->launches - l0;
   c->launches = l0;  // capture does not launch
   DFM_CK(cudaGraphInstantiate(&c->step_exec, g, 0));
   cudaGraphDestroy(g);
@@ -366,7 +373,7 @@ bool step_graph(dfm_ctx* c) {
 void run_step(dfm_ctx* c, bool split) {
   if (!split && step_graph(c)) {
     DFM_CK(cudaGraphLaunch(c->step_exec, c->stream));
-    c->launches += 6;
+    c->launches += c->graph_launches;
     return;
   }
   if (c->cost_step.n < (size_t)c->F) c->cost_step.alloc(c->F);

@@ -707,7 +707,8 @@ int is_nmf_dev(const double* h0_dev, int F, int T, int N, int K, int max_iters, 
       case 3: case 4: kern = k_tupd_mma<4>; break;
       default: kern = k_tupd_mma<8>; break;
     }
-    kern<<<dim3((F + 7) / 8, N), 32 * kTupdWarps, 0, s>>>(F, T, N, K, Tf.p, V.p, Aw.p, Bw.p, kEpsNmf, done.p);
+    kern<<<dim3((F + 7) / 8, N), 32 * kTupdWarps, 0, s>>>(F, T, N, K, Tf.p, V.p, Aw.p, Bw.p, kEpsNmf, done.p,
+                                                          nullptr);
     DFM_CK_LAUNCH();
   };
   auto vupd = [&]() {
@@ -719,7 +720,7 @@ int is_nmf_dev(const double* h0_dev, int F, int T, int N, int K, int max_iters, 
       default: kern = k_vupd_mma<8>; break;
     }
     kern<<<dim3((T + 7) / 8, N), 32 * kVupdMWarps, 0, s>>>(F, T, N, K, Tf.p, Aw.p, Bw.p, V.p, nullptr, kEpsNmf,
-                                                         done.p);
+                                                         done.p, nullptr);
     DFM_CK_LAUNCH();
   };
   spec();

@@ -64,7 +64,7 @@ def main():
     d = np.diff(tr, axis=1) / 1e3  # us
     life = (tr[:, 5] - tr[:, 0]) / 1e3
     out = {"workload": args.workload, "tiling": eng.tiling(), "step_ms": ms,
-           "kernels_ms": dict(zip(["k_em_bin", "k_tupd", "k_pd", "k_vupd", "k_spec"], [round(v, 4) for v in sp])),
+           "kernels_ms": dict(zip(["k_em_bin", "k_tupd+h", "k_pdw", "k_vupd+H", "tail"], [round(v, 4) for v in sp])),
            "ctas": int(tr.shape[0]),
            "span_us": float(tr[:, 5].max() / 1e3), "cta_life_us_mean": float(life.mean()),
            "cta_life_us_max": float(life.max()),
