@@ -39,7 +39,7 @@ struct EmArgs {
 };
 
 struct EmPlan {
-  size_t lsm, wsm, qsum, ipscr, red, wsum, ldet, tile, total;
+  size_t lsm, lst, wsm, qsum, ipscr, red, wsum, ldet, tile, total;
   int nwarps, SL, SQ, nitems;
 };
 
@@ -55,6 +55,7 @@ __host__ __device__ inline EmPlan plan_em(const EmArgs& a, int FT) {
   p.SQ = FT / a.etot > 1 ? FT / a.etot : 1;
   size_t o = 0;
   p.lsm = o; o += al(N * M * sizeof(double));
+  p.lst = o; o += al(M * (size_t)((N + 1) & ~1) * sizeof(double));  // Lambda^T [m][N rounded to even]
   p.wsm = o; o += al((size_t)a.wsz * sizeof(cd));
   p.qsum = o; o += al((size_t)a.qper * sizeof(cd));
   p.ipscr = o; o += (size_t)a.nb * ipscr_bytes<MAXMB>();
@@ -121,10 +122,33 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
   const double* Hf = a.H + (size_t)f * N * T;
   em_stamp(a, 0);
 
+  // Lambda of the bin, and its transpose [m][NP] for the per-frame products
+  // sum_n h_n Lambda(n, m): one 16-byte load per source pair
+  const int NP = (N + 1) & ~1;
+  double* LsT = (double*)(smem + sp.lst);
+  auto build_lst = [&]() {
+    for (int e = tid; e < M * NP; e += FT) {
+      const int m = e / NP, n = e - m * NP;
+      LsT[e] = n < N ? Lsm[n * M + m] : 0.0;
+    }
+  };
   for (int e = tid; e < N * M; e += FT) Lsm[e] = a.lam[(size_t)f * N * M + e];
+  __syncthreads();
+  build_lst();
   for (int e = tid; e < wsz; e += FT) Wsm[e] = a.W[(size_t)f * wsz + e];
   __syncthreads();
 
+  // Lambda(:, m) into registers (pairs) -- the products keep the sequential n order
+  auto load_lam = [&](int m, double* lv) {
+    const double* lt = LsT + m * NP;
+#pragma unroll
+    for (int n = 0; n < kMaxN; n += 2)
+      if (n < N) {
+        const double2 v = *reinterpret_cast<const double2*>(lt + n);
+        lv[n] = v.x;
+        if (n + 1 < kMaxN) lv[n + 1] = v.y;
+      }
+  };
   auto load_h = [&](int t, double* h) {
 #pragma unroll
     for (int n = 0; n < kMaxN; ++n) h[n] = n < N ? __ldg(Hf + n * T + t) : 0.0;
@@ -220,10 +244,12 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
           if (n < N) hs[n * FTp + tid] = h[n];
 #pragma unroll
         for (int m = 0; m < (SB ? MS : M); ++m) {
+          double lv[kMaxN];
+          load_lam(m, lv);
           double raw = 0.0;
 #pragma unroll
           for (int n = 0; n < kMaxN; ++n)
-            if (n < N) raw += h[n] * Lsm[n * M + m];
+            if (n < N) raw += h[n] * lv[n];
           const double ie = rcp_pos(fmax(raw, floor_));
           const double p = SB ? pv[SB ? m : 0] : Pf[(size_t)m * T + t];
           is[m * FTp + tid] = ie;
@@ -306,6 +332,8 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
       a.lam[(size_t)f * N * M + q] = l;
     }
     __syncthreads();
+    build_lst();
+    __syncthreads();
   }
   em_stamp(a, 1);
 
@@ -384,10 +412,12 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
       if (tid < tn) {
 #pragma unroll
         for (int m = 0; m < (SB ? MS : M); ++m) {
+          double lv[kMaxN];
+          load_lam(m, lv);
           double raw = 0.0;
 #pragma unroll
           for (int n = 0; n < kMaxN; ++n)
-            if (n < N) raw += h[n] * Lsm[n * M + m];
+            if (n < N) raw += h[n] * lv[n];
           const double ie = rcp_pos(fmax(raw, floor_));
           const double p = SB ? pv[SB ? m : 0] : Pf[(size_t)m * T + t];
           cost += p * ie;
@@ -567,19 +597,20 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
       for (int mu = 0; mu < MAXMB; ++mu)
         if (mu < mb) {
           const int m = off + mu;
+          double lv[kMaxN];
+          load_lam(m, lv);
           double raw = 0.0;
 #pragma unroll
           for (int n = 0; n < kMaxN; ++n)
-            if (n < N) raw += h[n] * Lsm[n * M + m];
+            if (n < N) raw += h[n] * lv[n];
           const double ie = rcp_pos(fmax(raw, floor_));
           const double z = P[mu] * ie * ie;
           Pf[(size_t)m * T + t] = P[mu];
 #pragma unroll
           for (int n = 0; n < kMaxN; ++n)
             if (n < N) {
-              const double l = Lsm[n * M + m];
-              A[n] += z * l;
-              B[n] += ie * l;
+              A[n] += z * lv[n];
+              B[n] += ie * lv[n];
             }
         }
     }
@@ -938,18 +969,36 @@ __global__ void __launch_bounds__(32 * kVupdMWarps, KT <= 2 ? 3 : 2) k_vupd_mma(
 template <int MB_, int NB_, int NS_, int MAXMB>
 __global__ void __launch_bounds__(128, 6) k_pdw(const EmArgs a) {
   constexpr bool SB = MB_ > 0 && NB_ > 0;
-  __shared__ double Ls[kMaxN * 64];
+  __shared__ __align__(16) double Ls[kMaxN * 64];  // Lambda^T [m][NP] (one 16-byte load per source pair)
   const int M = SB ? MB_ * NB_ : a.M;
   const int N = NS_ > 0 ? NS_ : a.N;
   const int T = a.T;
+  const int NP = (N + 1) & ~1;
   const int f = blockIdx.y, t = blockIdx.x * blockDim.x + threadIdx.x;
   const double* Lg = a.lam + (size_t)f * N * M;
-  const bool smemL = N * M <= kMaxN * 64;
+  const bool smemL = M * NP <= kMaxN * 64;
   if (smemL)
-    for (int e = threadIdx.x; e < N * M; e += blockDim.x) Ls[e] = Lg[e];
+    for (int e = threadIdx.x; e < M * NP; e += blockDim.x) {
+      const int m = e / NP, n = e - m * NP;
+      Ls[e] = n < N ? Lg[n * M + m] : 0.0;
+    }
   __syncthreads();
   if (t >= T) return;
-  const double* Lf = smemL ? Ls : Lg;
+  auto load_lam = [&](int m, double* lv) {
+    if (smemL) {
+#pragma unroll
+      for (int n = 0; n < kMaxN; n += 2)
+        if (n < N) {
+          const double2 v = *reinterpret_cast<const double2*>(Ls + m * NP + n);
+          lv[n] = v.x;
+          lv[n + 1] = v.y;
+        }
+    } else {
+#pragma unroll
+      for (int n = 0; n < kMaxN; ++n)
+        if (n < N) lv[n] = Lg[n * M + m];
+    }
+  };
   double h[kMaxN];
 #pragma unroll
   for (int n = 0; n < kMaxN; ++n) h[n] = n < N ? __ldg(a.H + ((size_t)f * N + n) * T + t) : 0.0;
@@ -964,19 +1013,20 @@ __global__ void __launch_bounds__(128, 6) k_pdw(const EmArgs a) {
   for (int n = 0; n < kMaxN; ++n) A[n] = B[n] = 0.0;
 #pragma unroll
   for (int m = 0; m < (SB ? MB_ * NB_ : M); ++m) {
+    double lv[kMaxN];
+    load_lam(m, lv);
     double raw = 0.0;
 #pragma unroll
     for (int n = 0; n < kMaxN; ++n)
-      if (n < N) raw += h[n] * Lf[n * M + m];
+      if (n < N) raw += h[n] * lv[n];
     const double ie = rcp_pos(fmax(raw, a.floor_));
     const double p = SB ? pv[SB ? m : 0] : __ldg(Pt + (size_t)m * T);
     const double z = p * ie * ie;
 #pragma unroll
     for (int n = 0; n < kMaxN; ++n)
       if (n < N) {
-        const double l = Lf[n * M + m];
-        A[n] += z * l;
-        B[n] += ie * l;
+        A[n] += z * lv[n];
+        B[n] += ie * lv[n];
       }
   }
 #pragma unroll
