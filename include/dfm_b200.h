@@ -165,6 +165,10 @@ int dfm_get_trace(dfm_ctx* ctx, unsigned long long* out, int n);
 /* Timing experiments only (results become wrong): bit0 skips the Lambda
  * frame reduction, bit1 the Q accumulation of the per-bin kernel. */
 int dfm_debug_bits(dfm_ctx* ctx, int bits);
+/* Tests: run the frequency-sharded path (V-update {num, den} through
+ * ncclAllReduce, then k_vapply; no graph) even on a one-rank communicator. */
+int dfm_force_collective(dfm_ctx* ctx, int on);
+
 /* Use the generic (runtime-shape) bin kernel even when a compile-time-shape
  * instantiation matches the layout (A/B testing of the two code paths). */
 int dfm_force_generic(dfm_ctx* ctx, int on);

@@ -47,6 +47,7 @@ _SIGS = {
     "dfm_nccl_get_unique_id": (_i, [_vp]),
     "dfm_fit": (_i, [_vp, _i, _vp, _vp, _vp]),
     "dfm_fit_many": (_i, [_vp, _i, _i, _vp, _vp]),
+    "dfm_force_collective": (_i, [_vp, _i]),
     "dfm_fmnm_sizes": (_sz, [_vp, _vp, _vp, _vp, _vp]),
     "dfm_stft_num_frames": (_i, [_i, _i, _i]),
     "dfm_cluster_masks": (_i, [_vp, _i, _i, _i, _i, _u64, _i, _d, _i, _i, _vp, _i]),

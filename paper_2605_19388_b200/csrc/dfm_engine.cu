@@ -115,6 +115,7 @@ struct dfm_ctx {
   long long graph_launches = 0;         // kernels in one replay
   int dbg = 0;
   bool host_exchange = false;  // shard stepping API: {num, den} exchanged by the caller
+  bool force_collective = false;  // run the NCCL path even with one rank (tests)
   int xs_iter = 0, xs_iters = 0;
   bool use_graph = true;
   bool has_obs = false, has_model = false;
@@ -233,6 +234,9 @@ void set_kernel_attrs(dfm_ctx* c) {
 
 }
 
+// frequency-sharded over a communicator: V-update {num, den} allreduced
+bool collective(const dfm_ctx* c) { return c->comm != nullptr && (c->nranks > 1 || c->force_collective); }
+
 void drop_graph(dfm_ctx* c);
 void ensure_cost(dfm_ctx* c, int slots) {
   if (c->cost_part.n < (size_t)slots * c->F) {
@@ -304,7 +308,7 @@ void launch_pd(dfm_ctx* c) {
 
 void launch_vupd(dfm_ctx* c) {
   const dim3 grid((c->T + 7) / 8, c->N);
-  const bool sharded = (c->comm != nullptr && c->nranks > 1) || c->host_exchange;
+  const bool sharded = collective(c) || c->host_exchange;
   auto kern = k_vupd_mma<8>;
   switch ((c->K + 7) / 8) {
     case 1: kern = k_vupd_mma<1>; break;
@@ -337,7 +341,7 @@ void launch_rest(dfm_ctx* c, cudaEvent_t* ev) {
   if (ev) DFM_CK(cudaEventRecord(ev[4], c->stream));
   // H for the next k_em_bin: fused into k_vupd on one GPU; after the
   // allreduce (or the caller's exchange) when sharded
-  const bool sharded = (c->comm != nullptr && c->nranks > 1) || c->host_exchange;
+  const bool sharded = collective(c) || c->host_exchange;
   if (sharded && !c->host_exchange) launch_spec(c);
 }
 
@@ -351,7 +355,7 @@ void drop_graph(dfm_ctx* c) {
 // graph; replays cut the per-launch gaps.  Not used when sharded (the NCCL
 // allreduce stays a stream launch).
 bool step_graph(dfm_ctx* c) {
-  if (!c->use_graph || (c->comm && c->nranks > 1) || c->host_exchange) return false;
+  if (!c->use_graph || collective(c) || c->host_exchange) return false;
   if (c->step_exec) return true;
   if (c->cost_step.n < (size_t)c->F) c->cost_step.alloc(c->F);
   cudaGraph_t g = nullptr;
@@ -650,7 +654,7 @@ int fit_end(dfm_ctx* c, int iters, double* cost_trace, double* wall_seconds, dou
   std::vector<double> cost(iters + 1, 0.0);
   for (int i = 0; i <= iters; ++i)
     for (int f = 0; f < c->F; ++f) cost[i] += part[(size_t)i * c->F + f];
-  if (c->comm && c->nranks > 1) {
+  if (collective(c)) {
     if (c->cost_sum.n < (size_t)iters + 1) c->cost_sum.alloc(iters + 1);
     c->cost_sum.upload(cost.data(), iters + 1, c->stream);
     NCCL_CK(nccl().AllReduce(c->cost_sum.p, c->cost_sum.p, iters + 1, ncclDouble, ncclSum, c->comm, c->stream));
@@ -935,6 +939,15 @@ int dfm_debug_bits(dfm_ctx* c, int bits) {
   drop_graph(c);
   c->dbg = bits;
   return DFM_OK;
+}
+
+int dfm_force_collective(dfm_ctx* c, int on) {
+  if (!c) return DFM_ERR_ARG;
+  DFM_API_BEGIN
+  drop_graph(c);
+  c->force_collective = on != 0;
+  return DFM_OK;
+  DFM_API_END
 }
 
 int dfm_force_generic(dfm_ctx* c, int on) {

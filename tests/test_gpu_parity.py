@@ -9,6 +9,8 @@ the device path.  Tolerances follow BASELINE.json's north_star:
 Per-step kernels are compared at 1e-10 (they differ from the oracle only in
 floating-point summation order and FMA contraction).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -407,3 +409,52 @@ def test_fit_many_matches_individual_fits(dfm, oracle):
         assert np.all(np.diff(costs[j]) <= 1e-9 * np.abs(costs[j][:-1]))
         e.close()
         e2.close()
+
+
+def test_nccl_collective_path_matches_single_gpu(dfm, oracle):
+    # the frequency-sharded device path -- V-update {num, den} through
+    # ncclAllReduce, k_vapply, a separate H = T V launch -- on a one-rank
+    # communicator gives bitwise the single-GPU (fused, graph-replayed) fit
+    import ctypes
+
+    F, T, N, K, sizes = 40, 52, 3, 4, [2, 2]
+    x = dfm.generate_mixture(0, F, T, 4, N, K, 81)
+    layout = dfm.BlockLayout(sizes)
+    init = dfm.random_init(F, T, layout, N, K, 82)
+    runs = []
+    for collective in (False, True):
+        e = dfm.Engine(F, T, layout, N, K)
+        if collective:
+            buf = ctypes.create_string_buffer(128)
+            dfm._capi.check(e.lib.dfm_nccl_get_unique_id(buf))
+            e.comm_init(buf.raw, 1, 0)
+            dfm._capi.check(e.lib.dfm_force_collective(e.ctx, 1))
+        e.set_obs(x)
+        e.set_model(init.nmf, init.w0, init.lambda0)
+        cost, _, _, _ = e.fit(15)
+        runs.append((cost, e.get_model()))
+        e.close()
+    (c0, (n0, w0, l0)), (c1, (n1, w1, l1)) = runs
+    assert np.array_equal(c0, c1)
+    assert np.array_equal(n0.T, n1.T) and np.array_equal(n0.V, n1.V) and np.array_equal(l0, l1)
+    assert all(np.array_equal(a, b) for a, b in zip(w0, w1))
+    maps = open("/proc/self/maps").read()
+    assert "libnccl" in maps, "the collective path must have loaded NCCL"
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("workload", ["config2", "config3"])
+def test_full_size_config_parity(dfm, oracle, workload):
+    # BASELINE configs 2 (one 12x12 block) and 3 (8 x 4 mics, N=8, K=32,
+    # F=1025, T=2000) at full size: 3 EM iterations against the oracle
+    import bench
+
+    c = bench.CONFIGS[workload]
+    layout = dfm.BlockLayout(c["sizes"])
+    x = dfm.generate_mixture(c["kind"], c["F"], c["T"], layout.total, c["N"], c["K"], bench.SEED_X)
+    init = dfm.random_init(c["F"], c["T"], layout, c["N"], c["K"], bench.SEED_INIT)
+    fit = dfm.fit_distributed(x, layout, init, 3, True)
+    oracle.set_threads(os.cpu_count() or 1)
+    ref = oracle.run_engine(x, c["sizes"], _init_dict(init), 3)
+    assert _rel(fit.report.cost_trace, ref["cost_trace"]) < TRAJ_RTOL
+    assert np.all(np.diff(fit.report.cost_trace) <= 1e-9 * np.abs(fit.report.cost_trace[:-1]))
