@@ -155,6 +155,13 @@ ENGINE_CASES = [
     (5, 64, [4, 4, 4], 5, 16, 20),
     (4, 30, [12], 5, 16, 20),
     (6, 25, [1, 1, 1], 3, 3, 20),
+    # limits and ragged shapes: N = 8, K = 64, a 16-mic block, one bin /
+    # one frame, odd frame counts that do not fill a tile
+    (3, 17, [16], 8, 64, 10),
+    (2, 5, [3, 5], 8, 32, 10),
+    (1, 4, [2], 2, 3, 5),
+    (11, 257, [4, 4], 6, 20, 10),
+    (5, 130, [8, 8], 4, 9, 10),
 ]
 
 
