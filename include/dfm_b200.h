@@ -155,9 +155,12 @@ int dfm_bench_split_step(dfm_ctx* ctx);
 int dfm_bench_last_split(dfm_ctx* ctx, double* ms5);
 /* Kernel launches issued by the context so far (for the bench's gpu_launches). */
 long long dfm_launch_count(const dfm_ctx* ctx);
-/* Tuning override for the fused bin kernel: bins per CTA group (G) and
- * cluster size (CTAs splitting T).  0 = heuristic. */
-int dfm_set_tiling(dfm_ctx* ctx, int bins_per_cta, int cluster_size);
+/* Tuning override: frame_tile = threads (frames per tile) of the per-bin
+ * kernel k_em_bin (multiple of 32, <= 512); pd_frames = frames per CTA of the
+ * elementwise pass D (multiple of 32, <= 128).  0 = heuristic (the frame tile
+ * minimising waves x tiles: 128 for config 1 on one GPU, 256/512 when a
+ * frequency shard leaves fewer bins than SMs). */
+int dfm_set_tiling(dfm_ctx* ctx, int frame_tile, int pd_frames);
 /* Profiling aid: per-bin %globaltimer stamps at the phase boundaries of the
  * per-bin kernel (16 slots per CTA).  dfm_set_trace returns the buffer length. */
 int dfm_set_trace(dfm_ctx* ctx, int on);

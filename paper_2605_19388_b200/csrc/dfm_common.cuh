@@ -295,4 +295,27 @@ __device__ inline int ip_column_warp(int mb, cd* W, int mu, const QGet& qget, do
   return fb;
 }
 
+
+// 1/x for x >= floor > 0: hardware reciprocal estimate + two Newton steps
+// (within 1 ulp of the IEEE quotient the reference computes).
+__device__ __forceinline__ double rcp_pos(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// 1/sqrt(x) for x > 0 (normal): hardware estimate + two Newton steps
+// r <- r (3 - x r^2) / 2 (within about 1 ulp)
+__device__ __forceinline__ double rsqrt_pos(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double hx = 0.5 * x;
+  r = r * fma(-hx * r, r, 1.5);
+  r = r * fma(-hx * r, r, 1.5);
+  return r;
+}
+
 }  // namespace dfm

@@ -80,21 +80,11 @@ __device__ __forceinline__ void em_stamp(const EmArgs& a, int phase) {
   }
 }
 
-// 1/x for x >= floor > 0: hardware reciprocal estimate + two Newton steps
-// (within 1 ulp of the IEEE quotient the reference computes).
-__device__ __forceinline__ double rcp_pos(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
-}
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b);
 
 template <int MB_, int NB_, int NS_, int MAXMB>
-__global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
+__global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 registers
   constexpr bool SB = MB_ > 0 && NB_ > 0;
   extern __shared__ __align__(16) unsigned char smem[];
   const int f = blockIdx.x;
@@ -212,6 +202,9 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
     const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3, nwarps = FT >> 5;
     const int njobs = 2 * ((M + 7) / 8);
     const bool use_mma = N <= 8 && njobs <= kLamJobs * nwarps;
+    // spare warps split each job's frames into slices (large frame tiles);
+    // slice partials land in red[] slice rows, summed in a fixed order below
+    const int nsl = nwarps >= njobs ? max(1, min(nwarps / njobs, SL)) : 1;
     double lj0[kLamJobs], lj1[kLamJobs];
 #pragma unroll
     for (int jj = 0; jj < kLamJobs; ++jj) lj0[jj] = lj1[jj] = 0.0;
@@ -265,15 +258,17 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
       } else if (use_mma) {
 #pragma unroll
         for (int jj = 0; jj < kLamJobs; ++jj) {
-          const int job = warp + jj * nwarps;
-          if (job < njobs) {
+          const int jg = warp + jj * nwarps, job = jg % njobs, slc = jg / njobs;
+          if (slc < nsl) {
             const int j = job >> 1;
             const double* brow = (job & 1) ? is : zs;
             const int m = 8 * j + g;
+            const int chunk = (((tn + 7) >> 3) + nsl - 1) / nsl * 8;
+            const int s0 = slc * chunk, s1 = min(tn, s0 + chunk);
             // two independent accumulator chains (even / odd k-steps), added at
             // the end of the tile in a fixed order
             double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
-            for (int t0 = 0; t0 < tn; t0 += 8) {
+            for (int t0 = s0; t0 < s1; t0 += 8) {
               const int t = t0 + q, u = t0 + 4 + q;
               const double av = (g < N && t < tn) ? hs[g * FTp + t] : 0.0;
               const double bv = (m < M && t < tn) ? brow[m * FTp + t] : 0.0;
@@ -309,13 +304,13 @@ __global__ void __launch_bounds__(256, 2) k_em_bin(const EmArgs a) {
       // scatter the DMMA accumulators (C[n][m] at c0 = (g, 2q), c1 = (g, 2q+1)) into red[]
 #pragma unroll
       for (int jj = 0; jj < kLamJobs; ++jj) {
-        const int job = warp + jj * nwarps;
-        if (job < njobs && g < N) {
+        const int jg = warp + jj * nwarps, job = jg % njobs, slc = jg / njobs;
+        if (slc < nsl && g < N) {
           const int j = job >> 1, w = job & 1;
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
             const int m = 8 * j + 2 * q + i;
-            if (m < M) red[2 * (g * M + m) + w] = i ? lj1[jj] : lj0[jj];
+            if (m < M) red[2 * (slc * NM + g * M + m) + w] = i ? lj1[jj] : lj0[jj];
           }
         }
       }

@@ -204,7 +204,8 @@ bool choose_tiling(dfm_ctx* c) {
   const EmArgs a = make_args(c);
   double best = 1e30;
   int bestFT = 0;
-  std::vector<int> cands = {256, 128, 64, 32};
+  // 512 threads per bin when the bins are few (frequency shards): one CTA per SM
+  std::vector<int> cands = {512, 256, 128, 64, 32};
   if (c->req_FT) cands = {c->req_FT};
   for (int FT : cands) {
     const size_t sm = em_smem(a, FT, c->kmaxmb);
@@ -889,7 +890,7 @@ int dfm_bench_last_split(dfm_ctx* c, double* ms5) {
 long long dfm_launch_count(const dfm_ctx* c) { return c ? c->launches : -1; }
 
 int dfm_set_tiling(dfm_ctx* c, int frame_tile, int pd_frames) {
-  if (!c || frame_tile < 0 || frame_tile > 256 || (frame_tile & 31) || pd_frames < 0 || pd_frames > 128 ||
+  if (!c || frame_tile < 0 || frame_tile > 512 || (frame_tile & 31) || pd_frames < 0 || pd_frames > 128 ||
       (pd_frames & 31))
     return DFM_ERR_ARG;
   DFM_API_BEGIN

@@ -282,9 +282,9 @@ __device__ bool chol_thread(const cd* qp, cd* L, double* dinv) {
 #pragma unroll
     for (int k = 0; k < c; ++k) d -= norm2(L[Li(c, k)]);
     if (!(d > 0.0) || !isfinite(d)) return false;
-    const double lc = sqrt(d);
-    dinv[c] = 1.0 / lc;
-    L[Li(c, c)] = cd{lc, 0.0};
+    const double il = rsqrt_pos(d);  // 1 / sqrt(d) without the IEEE sqrt + divide chain
+    dinv[c] = il;
+    L[Li(c, c)] = cd{d * il, 0.0};
 #pragma unroll
     for (int r = c + 1; r < MB; ++r) {
       cd s = Q(r, c);
@@ -457,9 +457,10 @@ __device__ bool ip_sweep_quad(cd* W, IpWork<MB>& f, const cd* qb, double floor_,
     r2 += __shfl_xor_sync(mask, r2, 2, 4);
     nq += __shfl_xor_sync(mask, nq, 1, 4);
     nq += __shfl_xor_sync(mask, nq, 2, 4);
-    if (!fin || !(sqrt(r2) <= 1e-6)) return false;
-    const double sc = sqrt(fmax(nq, floor_));
-    const cd un = cdivr(u, sc);
+    // the reference's ||W^H Q u - e_mu|| <= 1e-6, on the squared norm
+    if (!fin || !(r2 <= 1e-12)) return false;
+    const double isc = rsqrt_pos(fmax(nq, floor_));
+    const cd un{u.re * isc, u.im * isc};
     const cd d = act ? un - W[mu * MB + la] : cd{0.0, 0.0};
     cd dv[MB];
 #pragma unroll
@@ -472,7 +473,8 @@ __device__ bool ip_sweep_quad(cd* W, IpWork<MB>& f, const cd* qb, double floor_,
     const cd den{1.0 + zmu.re, zmu.im};
     const double dn = norm2(den);
     if (!(dn > 0.0)) return false;
-    const cd iden{den.re / dn, -den.im / dn};
+    const double idn = rcp_pos(dn);
+    const cd iden{den.re * idn, -den.im * idn};
     cd row[MB];
 #pragma unroll
     for (int c = 0; c < MB; ++c) row[c] = f.Winv[c * MB + mu] * iden;

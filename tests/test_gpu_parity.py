@@ -184,7 +184,7 @@ def test_engine_trajectory_matches_oracle(dfm, oracle, F, T, sizes, N, K, iters)
         assert _rel(a, b) < 1e-7
 
 
-@pytest.mark.parametrize("FT,TB", [(32, 32), (64, 64), (128, 128), (256, 32), (96, 64)])
+@pytest.mark.parametrize("FT,TB", [(32, 32), (64, 64), (128, 128), (256, 32), (96, 64), (512, 128)])
 def test_engine_tilings_agree(dfm, oracle, FT, TB):
     F, T, sizes, N, K, iters = 11, 70, [4, 4, 4], 5, 8, 10
     layout = dfm.BlockLayout(sizes)

@@ -29,13 +29,18 @@ def main():
     ap.add_argument("--generic", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--dbg", type=int, default=0, help="timing experiments (results invalid)")
+    ap.add_argument("--shards", type=int, default=1, help="trace the first of S frequency shards")
     args = ap.parse_args()
     c = bench.CONFIGS[args.workload]
     layout = dfm.BlockLayout(c["sizes"])
     F, T, N, K = c["F"], c["T"], c["N"], c["K"]
     x = dfm.generate_mixture(c["kind"], F, T, layout.total, N, K, bench.SEED_X)
     init = dfm.random_init(F, T, layout, N, K, bench.SEED_INIT)
-    eng = dfm.Engine(F, T, layout, N, K)
+    from paper_2605_19388_b200.sharding import shard_bins
+
+    f0, f1 = shard_bins(F, args.shards, 0)
+    x = np.ascontiguousarray(x[f0:f1])
+    eng = dfm.Engine(F, T, layout, N, K, f_begin=f0, f_end=f1)
     lib = eng.lib
     if args.generic:
         dfm._capi.check(lib.dfm_force_generic(eng.ctx, 1))
