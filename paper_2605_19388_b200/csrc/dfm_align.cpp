@@ -23,33 +23,44 @@ void set_error(const std::string& msg);
 
 namespace {
 
-// init.cpp:14-22
-double pearson(const double* u, const double* v, size_t L) {
-  double mu = 0.0, mv = 0.0;
-  for (size_t j = 0; j < L; ++j) {
-    mu += u[j];
-    mv += v[j];
+// Pearson correlation (init.cpp:14-22) in two steps: every column is centred
+// once (mean, then u - mean and its sum of squares, in the reference's
+// sequential order); the N^2 correlations then reuse the centred columns, so
+// each equals the reference's pearson(u, v) with a third of the work.
+struct Centred {
+  std::vector<double> d, ss;
+  Centred(const double* m, size_t L, int N) : d((size_t)N * L), ss(N) {
+    for (int c = 0; c < N; ++c) {
+      const double* u = m + c * L;
+      double mu = 0.0;
+      for (size_t j = 0; j < L; ++j) mu += u[j];
+      mu /= (double)L;
+      double s2 = 0.0;
+      for (size_t j = 0; j < L; ++j) {
+        const double a = u[j] - mu;
+        d[c * L + j] = a;
+        s2 += a * a;
+      }
+      ss[c] = s2;
+    }
   }
-  mu /= (double)L;
-  mv /= (double)L;
-  double su = 0.0, sv = 0.0, d = 0.0;
-  for (size_t j = 0; j < L; ++j) {
-    const double a = u[j] - mu, b = v[j] - mv;
-    su += a * a;
-    sv += b * b;
-    d += a * b;
-  }
-  const double den = std::sqrt(su) * std::sqrt(sv);
-  return den <= 0 ? 0.0 : d / den;
-}
+};
 
 // init.cpp:24-42: cand / ref are N columns of length L (column c at c * L);
 // lexicographic permutations, the first strict maximum of the summed
 // correlation of cand column perm[c] with ref column c wins
 std::vector<int> best_perm(const double* cand, const double* ref, size_t L, int N) {
   std::vector<double> corr((size_t)N * N);
+  const Centred cu(cand, L, N), cv(ref, L, N);
   for (int a = 0; a < N; ++a)
-    for (int c = 0; c < N; ++c) corr[(size_t)a * N + c] = pearson(cand + a * L, ref + c * L, L);
+    for (int c = 0; c < N; ++c) {
+      const double* du = &cu.d[a * L];
+      const double* dv = &cv.d[c * L];
+      double d = 0.0;
+      for (size_t j = 0; j < L; ++j) d += du[j] * dv[j];
+      const double den = std::sqrt(cu.ss[a]) * std::sqrt(cv.ss[c]);
+      corr[(size_t)a * N + c] = den <= 0 ? 0.0 : d / den;  // = pearson(cand_a, ref_c)
+    }
   std::vector<int> perm(N), best(N);
   std::iota(perm.begin(), perm.end(), 0);
   best = perm;

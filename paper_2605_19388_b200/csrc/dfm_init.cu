@@ -27,6 +27,7 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "dfm_internal.cuh"
@@ -707,8 +708,10 @@ int is_nmf_dev(const double* h0_dev, int F, int T, int N, int K, int max_iters, 
       case 3: case 4: kern = k_tupd_mma<4>; break;
       default: kern = k_tupd_mma<8>; break;
     }
+    // rec = T_new V fused (skipped with the update for converged sources,
+    // whose rec is unchanged)
     kern<<<dim3((F + 7) / 8, N), 32 * kTupdWarps, 0, s>>>(F, T, N, K, Tf.p, V.p, Aw.p, Bw.p, kEpsNmf, done.p,
-                                                          nullptr);
+                                                          H.p);
     DFM_CK_LAUNCH();
   };
   auto vupd = [&]() {
@@ -720,7 +723,7 @@ int is_nmf_dev(const double* h0_dev, int F, int T, int N, int K, int max_iters, 
       default: kern = k_vupd_mma<8>; break;
     }
     kern<<<dim3((T + 7) / 8, N), 32 * kVupdMWarps, 0, s>>>(F, T, N, K, Tf.p, Aw.p, Bw.p, V.p, nullptr, kEpsNmf,
-                                                         done.p, nullptr);
+                                                         done.p, H.p);
     DFM_CK_LAUNCH();
   };
   spec();
@@ -732,11 +735,9 @@ int is_nmf_dev(const double* h0_dev, int F, int T, int N, int K, int max_iters, 
   if (max_iters > 0) {
     DFM_CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
     weights();
-    tupd();
-    spec();
+    tupd();  // + rec = T_new V
     weights();
-    vupd();
-    spec();
+    vupd();  // + rec = T V_new
     divergence(0);
     DFM_CK(cudaStreamEndCapture(s, &g));
     DFM_CK(cudaGraphInstantiate(&ge, g, 0));
@@ -910,9 +911,16 @@ int dfm_init_pipeline(const double* x, int F, int T, int nblocks, const int* siz
   }
   md.download(mh.data(), mh.size(), s);
   DFM_CK(cudaStreamSynchronize(s));
-  for (int l = 0; l < L; ++l) {
-    rc = dfm_align_frequency_permutations(mh.data() + (size_t)l * FNT, F, T, N, neighborhood, rounds);
-    if (rc != DFM_OK) return rc;
+  {  // the subarrays' frequency alignments are independent: one host thread each
+    std::vector<int> rcs(L, DFM_OK);
+    std::vector<std::thread> th;
+    for (int l = 0; l < L; ++l)
+      th.emplace_back([&, l] {
+        rcs[l] = dfm_align_frequency_permutations(mh.data() + (size_t)l * FNT, F, T, N, neighborhood, rounds);
+      });
+    for (auto& t : th) t.join();
+    for (int l = 0; l < L; ++l)
+      if (rcs[l] != DFM_OK) return rcs[l];
   }
   if (L > 1) {
     std::vector<int> perms((size_t)L * N);
