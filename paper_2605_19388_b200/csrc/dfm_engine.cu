@@ -351,12 +351,15 @@ void drop_graph(dfm_ctx* c) {
   c->step_exec = nullptr;
 }
 
-// Captures one steady-state iteration (k_em_bin finish+start writing cost
-// slot 1, then the five follow-up kernels, with the split events) into a CUDA
-// graph; replays cut the per-launch gaps.  Not used when sharded (the NCCL
-// allreduce stays a stream launch).
+// Captures one steady-state iteration (k_em_bin finish+start writing the
+// scratch cost slot, then the follow-up kernels -- and, when sharded, the
+// NCCL allreduce, k_vapply and H = T V) into a CUDA graph; replays cut the
+// per-launch gaps.
 bool step_graph(dfm_ctx* c) {
-  if (!c->use_graph || collective(c) || c->host_exchange) return false;
+  // sharded runs capture the NCCL allreduce too (NCCL supports stream
+  // capture; every rank captures the same sequence); the host-exchange
+  // stepping API returns to the caller mid-iteration and is never captured
+  if (!c->use_graph || c->host_exchange) return false;
   if (c->step_exec) return true;
   if (c->cost_step.n < (size_t)c->F) c->cost_step.alloc(c->F);
   cudaGraph_t g = nullptr;

@@ -1,0 +1,31 @@
+"""Small runs of every device path, for compute-sanitizer:
+
+  compute-sanitizer --tool memcheck python tools/sanitize_run.py
+  compute-sanitizer --tool racecheck python tools/sanitize_run.py"""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2605_19388_b200 as dfm  # noqa: E402
+from paper_2605_19388_b200 import init as di  # noqa: E402
+from paper_2605_19388_b200 import stft as st  # noqa: E402
+
+F, T, N, K, sizes = 9, 70, 3, 4, [4, 4, 4]   # static shapes (4, 3, 5) need N=5: this is the generic path
+layout = dfm.BlockLayout(sizes)
+x = dfm.generate_mixture(0, F, T, layout.total, N, K, 3)
+init = dfm.random_init(F, T, layout, N, K, 4)
+fit = dfm.fit_distributed(x, layout, init, 3, True)
+dfm.wiener_block(x, fit.models, fit.spatial)
+F2, N2, K2 = 11, 5, 16  # static-shape kernels (config 1 layout)
+x2 = dfm.generate_mixture(1, F2, 150, 12, N2, K2, 5)
+i2 = dfm.random_init(F2, 150, layout, N2, K2, 6)
+f2 = dfm.fit_distributed(x2, layout, i2, 3, True)
+dfm.wiener_block(x2, f2.models, f2.spatial)
+sig = np.random.default_rng(1).standard_normal((1200, 2))
+X = st.stft_forward(sig, st.StftConfig(8000.0, 256, 64))
+st.stft_inverse(X, st.StftConfig(8000.0, 256, 64), 1200)
+st.stft_forward(sig[:300], st.StftConfig(8000.0, 12, 3))
+b = di.init_distributed(x, layout, di.InitConfig(N, K, 20), 7)
+print("sanitize run ok", fit.report.cost_trace[-1], f2.report.cost_trace[-1], b.lambda0.min())

@@ -1,7 +1,9 @@
 """Per-GPU EM step time of a frequency shard of a BASELINE workload, on one
 GPU (the compute part of an N-GPU run; no collective):
 
-  python tools/shard_bench.py [config1] [shards...]   e.g. 1 2 4 8"""
+  python tools/shard_bench.py [config1] [shards...]   e.g. 1 2 4 8
+  DFM_COLLECTIVE=1 python tools/shard_bench.py ...     with the NCCL path on a
+                                                       one-rank communicator"""
 import ctypes
 import os
 import sys
@@ -23,6 +25,11 @@ init = dfm.random_init(F, T, layout, N, K, bench.SEED_INIT)
 for S in shards:
     f0, f1 = shard_bins(F, S, 0)
     eng = dfm.Engine(F, T, layout, N, K, f_begin=f0, f_end=f1)
+    if os.environ.get("DFM_COLLECTIVE"):
+        buf = ctypes.create_string_buffer(128)
+        dfm._capi.check(eng.lib.dfm_nccl_get_unique_id(buf))
+        eng.comm_init(buf.raw, 1, 0)
+        dfm._capi.check(eng.lib.dfm_force_collective(eng.ctx, 1))
     eng.set_obs(np.ascontiguousarray(x[f0:f1]))
     eng.set_model(init.nmf, init.w0, init.lambda0)
     lib = eng.lib
