@@ -2,9 +2,11 @@
 // src/stft.cpp:74-141; the steps either side of the EM path).
 //
 //   k_stft_fft   one CTA per (frame, channel): the windowed frame in shared
-//                memory, in-place radix-2 FFT (power-of-two windows; twiddles
-//                from a host table of cos/sin(-2 pi k / n)), bins written in
-//                the ObsTensor layout [F][T][M].
+//                memory (bit-reversed, padded), in-place DIT FFT in radix-16
+//                register passes (power-of-two windows; twiddles from a host
+//                table of cos/sin(-2 pi k / n) staged in shared memory);
+//                channel-major spectra, then k_obs_transpose to the
+//                ObsTensor layout [F][T][M].
 //   k_stft_dft   the same for other window lengths as a direct O(n^2) DFT with
 //                the reference's angle 2 pi (k t mod n) / n (stft.cpp:39-50).
 //   k_istft_frame  inverse of one frame (conjugate-symmetric completion of
@@ -40,57 +42,55 @@ std::vector<double> hann(int len) {  // stft.cpp:63-68, periodic Hann
 __device__ __forceinline__ int pad(int i) { return i + (i >> 5); }
 
 // In-place DIT FFT over smem buf[pad(i)] (input in bit-reversed order),
-// twiddles tws[k] = exp(-2 pi i k / n), k < n/2, staged in shared memory
-// (conjugated for the inverse).  Stages are taken two at a time (radix 2^2):
-// a thread owns {a, a+h, a+2h, a+3h} and applies the stages of half-length h
-// and 2h in registers, so a pair of stages costs one barrier and one
-// shared-memory round trip; an odd stage count ends with one radix-2 stage.
-// Every butterfly is the reference's u +- w v (stft.cpp:26-31).
-__device__ void fft_smem(cd* buf, int n, int lg, const cd* tws, bool inverse) {
-  auto twd = [&](int idx) {
-    cd w = tws[idx];
-    if (inverse) w.im = -w.im;
-    return w;
-  };
-  int s = 0;  // log2 of the current half-length
-  for (; s + 2 <= lg; s += 2) {
-    const int h = 1 << s;
-    for (int g = threadIdx.x; g < (n >> 2); g += blockDim.x) {
-      const int k = g & (h - 1);
-      const int a = ((g >> s) << (s + 2)) + k;
-      const int i0 = pad(a), i1 = pad(a + h), i2 = pad(a + 2 * h), i3 = pad(a + 3 * h);
-      const cd w1 = twd(k << (lg - s - 1));          // stage of half-length h
-      const cd w2 = twd(k << (lg - s - 2));          // stage of half-length 2h
-      const cd w3 = twd((k + h) << (lg - s - 2));
-      cd x0 = buf[i0], x1 = buf[i1], x2 = buf[i2], x3 = buf[i3];
-      cd v = x1 * w1;
-      const cd y0 = x0 + v, y1 = x0 - v;
-      v = x3 * w1;
-      const cd y2 = x2 + v, y3 = x2 - v;
-      v = y2 * w2;
-      x0 = y0 + v;
-      x2 = y0 - v;
-      v = y3 * w3;
-      x1 = y1 + v;
-      x3 = y1 - v;
-      buf[i0] = x0;
-      buf[i1] = x1;
-      buf[i2] = x2;
-      buf[i3] = x3;
+// twiddles tw[k] = exp(-2 pi i k / n), k < n/2 (read through L1; conjugated
+// for the inverse).  Stages are taken R at a time (radix 2^R, R <= 4): a
+// thread owns the 2^R elements {a + j h} of a group and applies the R stages
+// of half-lengths h, 2h, ..., 2^(R-1) h in registers, so four stages cost one
+// barrier and one shared-memory round trip.  Every butterfly is the
+// reference's u +- w v (stft.cpp:26-31) with the twiddle of its stage.
+template <int R>
+__device__ __forceinline__ void fft_pass(cd* buf, int n, int lg, int s, const cd* tw, bool inverse) {
+  constexpr int G = 1 << R;
+  const int h = 1 << s;
+  for (int g = threadIdx.x; g < (n >> R); g += blockDim.x) {
+    const int k = g & (h - 1);
+    const int a = ((g >> s) << (s + R)) + k;
+    cd x[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) x[j] = buf[pad(a + j * h)];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {  // stage of half-length H = h 2^i
+      const int sh = lg - s - i - 1;  // twiddle stride n / (2H)
+#pragma unroll
+      for (int jj = 0; jj < G / 2; ++jj) {
+        const int lo = jj & ((1 << i) - 1);
+        const int j = ((jj >> i) << (i + 1)) | lo;  // pair (j, j + 2^i), bit i of j clear
+        const double2 wv = reinterpret_cast<const double2*>(tw)[(k + lo * h) << sh];
+        const cd w{wv.x, inverse ? -wv.y : wv.y};
+        const cd v = x[j + (1 << i)] * w;
+        x[j + (1 << i)] = x[j] - v;
+        x[j] = x[j] + v;
+      }
     }
-    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < G; ++j) buf[pad(a + j * h)] = x[j];
   }
-  if (s < lg) {  // last radix-2 stage, half-length n/2
-    const int h = 1 << s;
-    for (int k = threadIdx.x; k < h; k += blockDim.x) {
-      const int i0 = pad(k), i1 = pad(k + h);
-      const cd u = buf[i0], v = buf[i1] * twd(k);
-      buf[i0] = u + v;
-      buf[i1] = u - v;
-    }
-    __syncthreads();
+  __syncthreads();
+}
+
+__device__ void fft_smem(cd* buf, int n, int lg, const cd* tw, bool inverse) {
+  int s = 0;  // log2 of the current half-length
+  for (; s + 4 <= lg; s += 4) fft_pass<4>(buf, n, lg, s, tw, inverse);
+  switch (lg - s) {
+    case 3: fft_pass<3>(buf, n, lg, s, tw, inverse); break;
+    case 2: fft_pass<2>(buf, n, lg, s, tw, inverse); break;
+    case 1: fft_pass<1>(buf, n, lg, s, tw, inverse); break;
+    default: break;
   }
 }
+
+// threads per frame for the radix-16 passes (one group of 16 per thread)
+inline int fft_threads(int n) { return std::max(32, std::min(256, n / 16)); }
 
 __device__ __forceinline__ int bitrev(int i, int lg) { return lg ? (int)(__brev((unsigned)i) >> (32 - lg)) : 0; }
 
@@ -99,7 +99,7 @@ __global__ void k_stft_fft(const double* __restrict__ sig, int len, int M, const
                            int lg, int hop, int T, const cd* __restrict__ tw, cd* __restrict__ X) {
   extern __shared__ __align__(16) unsigned char sm[];
   cd* buf = (cd*)sm;
-  cd* tws = buf + (n + n / 32 + 1);
+  cd* tws = buf + (n + n / 32 + 1);  // twiddles staged in shared memory
   const int j = blockIdx.x, m = blockIdx.y;
   const double* s = sig + (size_t)m * len + (size_t)j * hop;
   for (int t = threadIdx.x; t < n; t += blockDim.x) buf[pad(bitrev(t, lg))] = cd{s[t] * win[t], 0.0};
@@ -277,7 +277,7 @@ void stft_forward_dev(const double* sig, int len, int M, int n, int hop, cd* X, 
   const dim3 grid(T, M);
   ensure_attrs();
   if (p2) {
-    k_stft_fft<<<grid, 256, sm, s>>>(sig, len, M, tw.win.p, n, log2i(n), hop, T, tw.tw.p, stage);
+    k_stft_fft<<<grid, fft_threads(n), sm, s>>>(sig, len, M, tw.win.p, n, log2i(n), hop, T, tw.tw.p, stage);
   } else {
     k_stft_dft<<<grid, 256, sm, s>>>(sig, len, M, tw.win.p, n, hop, T, stage);
   }
@@ -298,7 +298,8 @@ void stft_inverse_dev(const cd* X, int T, int M, int n, int hop, int out_len, do
   if (T > 0) {
     k_obs_transpose<false><<<dim3(T, (F + 31) / 32), 256, (size_t)32 * (M + 1) * sizeof(cd), s>>>(X, stage, F, T, M);
     DFM_CK_LAUNCH();
-    k_istft_frame<<<dim3(T, M), 256, sm, s>>>(stage, F, T, M, tw.win.p, n, log2i(n), p2, tw.tw.p, yscratch);
+    k_istft_frame<<<dim3(T, M), p2 ? fft_threads(n) : 256, sm, s>>>(stage, F, T, M, tw.win.p, n, log2i(n), p2,
+                                                                   tw.tw.p, yscratch);
     DFM_CK_LAUNCH();
   }
   if (out_len > 0) {
