@@ -152,6 +152,7 @@ class FitReport:
     stages: dict = field(default_factory=lambda: dict(w_update=0.0, mm_update=0.0, eta=0.0,
                                                       decorrelate=0.0))
     fallbacks: int = 0
+    ops: dict = field(default_factory=lambda: dict(w_update=0.0, mm_update=0.0))  # OpCounts, model.hpp:60-67
 
     def total_seconds(self) -> float:
         return float(np.sum(self.wall_seconds))
@@ -530,6 +531,18 @@ def fit_many(engines: Sequence["Engine"], iters: int):
     return cost, secs.value, fb
 
 
+def op_counts(F: int, T: int, sizes: Sequence[int], N: int, M: int, K: int, iters: int) -> dict:
+    """The reference's analytic operation counters (OpCounts, engine.cpp:55-57,
+    110-112, 121, 131, 146) for `iters` EM iterations:
+      w_update  += F (T mb^2 + mb^3) per IP column, mb columns per block;
+      mm_update += 2 F T N M per T/V weight build (two per iteration),
+                   2 F K T per source for the T and for the V update,
+                   2 N M T per bin for the Lambda update."""
+    w = sum(mb * F * (float(T) * mb * mb + float(mb) ** 3) for mb in sizes)
+    mm = 2 * (2.0 * F * T * N * M) + N * (2.0 * F * K * T) * 2 + F * (2.0 * N * M * T)
+    return dict(w_update=iters * w, mm_update=iters * mm)
+
+
 def _run_engine(x, layout: BlockLayout, init: InitBundle, iters: int, options: FitOptions):
     """detail::run_engine (engine.cpp:167-272) on the device."""
     x = _obs(x)
@@ -570,7 +583,7 @@ def _run_engine(x, layout: BlockLayout, init: InitBundle, iters: int, options: F
         eng.close()
     report = FitReport(np.concatenate(costs), np.concatenate(walls) if walls else np.zeros(0), iters,
                        dict(w_update=stages[0], mm_update=stages[1], eta=stages[2], decorrelate=stages[3]),
-                       fb)
+                       fb, op_counts(F, T, layout.sizes, init.nmf.num_sources(), M, init.nmf.K, iters))
     return nmf, wb, lam, report
 
 
@@ -604,6 +617,7 @@ def fit_distributed(x, layout: BlockLayout, init: InitBundle, iters: int, share_
     cost = np.zeros(iters + 1)
     wall = np.zeros(iters)
     stages = dict(w_update=0.0, mm_update=0.0, eta=0.0, decorrelate=0.0)
+    ops = dict(w_update=0.0, mm_update=0.0)
     fb = 0
     for l in range(layout.num_blocks()):
         fit = fit_single(extract_block(x, layout, l), slice_init(init, l), iters, options)
@@ -615,8 +629,11 @@ def fit_distributed(x, layout: BlockLayout, init: InitBundle, iters: int, share_
         wall += fit.report.wall_seconds
         for k in stages:
             stages[k] += fit.report.stages[k]
+        for k in ops:  # dist.cpp:91
+            ops[k] += fit.report.ops[k]
         fb += fit.report.fallbacks
-    return DistFit(models, BlockSpatialModel(layout, wbs, lam), FitReport(cost, wall, iters, stages, fb), False)
+    return DistFit(models, BlockSpatialModel(layout, wbs, lam), FitReport(cost, wall, iters, stages, fb, ops),
+                   False)
 
 
 # ------------------------------------------------------------------- wiener

@@ -108,3 +108,16 @@ def test_slice_init_and_extract_block(dfm):
     assert np.array_equal(sub.w0[0], init.w0[1])
     x = np.arange(4 * 5 * 5).reshape(4, 5, 5).astype(complex)
     assert np.array_equal(dfm.extract_block(x, layout, 1), x[:, :, 2:])
+
+
+def test_op_counts_follow_the_reference_formulas():
+    # test_bench.cpp:34-52: W-stage ops per iteration and bin are M^4 + J M^3
+    from paper_2605_19388_b200.fastmnmf import op_counts
+
+    full = op_counts(4, 16, [6], 2, 6, 2, 2)
+    assert full["w_update"] == 4.0 * 2 * (6 ** 4 + 16.0 * 6 ** 3)
+    dist = op_counts(4, 16, [2, 2, 2], 2, 6, 2, 2)
+    assert dist["w_update"] == 4.0 * 2 * 3 * (2 ** 4 + 16.0 * 2 ** 3)
+    # mm: two weight builds (2FTNM each), T and V updates (2FKT per source each), Lambda (2NMT per bin)
+    F, T, N, M, K = 3, 5, 2, 4, 6
+    assert op_counts(F, T, [4], N, M, K, 1)["mm_update"] == 4 * F * T * N * M + 4 * N * F * K * T + 2 * F * N * M * T

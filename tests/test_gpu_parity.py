@@ -465,3 +465,15 @@ def test_full_size_config_parity(dfm, oracle, workload):
     ref = oracle.run_engine(x, c["sizes"], _init_dict(init), 3)
     assert _rel(fit.report.cost_trace, ref["cost_trace"]) < TRAJ_RTOL
     assert np.all(np.diff(fit.report.cost_trace) <= 1e-9 * np.abs(fit.report.cost_trace[:-1]))
+
+
+def test_fit_reports_operation_counts(dfm, oracle):
+    # test_bench.cpp:34-52 through the fits: full M=6 and distributed {2,2,2}
+    # (shared and independent spectrograms count the same W-stage work)
+    x, layout, init = _inst(oracle, 4, 16, 6, 2, 2, 17, [6])
+    r = dfm.fit_full(x, init, 2).report
+    assert r.ops["w_update"] == pytest.approx(4.0 * 2 * (6 ** 4 + 16.0 * 6 ** 3))
+    x, layout, init = _inst(oracle, 4, 16, 6, 2, 2, 17, [2, 2, 2])
+    for shared in (True, False):
+        r = dfm.fit_distributed(x, layout, init, 2, shared).report
+        assert r.ops["w_update"] == pytest.approx(4.0 * 2 * 3 * (2 ** 4 + 16.0 * 2 ** 3))
