@@ -477,3 +477,87 @@ def test_fit_reports_operation_counts(dfm, oracle):
     for shared in (True, False):
         r = dfm.fit_distributed(x, layout, init, 2, shared).report
         assert r.ops["w_update"] == pytest.approx(4.0 * 2 * 3 * (2 ** 4 + 16.0 * 2 ** 3))
+
+
+def _wiener_paths(dfm, x, T, V, lam, w_blocks, sizes):
+    """Both device Wiener paths: the step kernel (wiener_block) and the engine
+    context kernel (Engine.wiener, k_wiener_ctx incl. the in-CTA inverse)."""
+    layout = dfm.BlockLayout(sizes)
+    a = dfm.wiener_block(x, dfm.NmfModel(T, V), dfm.BlockSpatialModel(layout, w_blocks, lam)).images
+    F, Tn, _ = x.shape
+    e = dfm.Engine(F, Tn, layout, T.shape[0], T.shape[2])
+    e.set_obs(x)
+    e.set_model(dfm.NmfModel(T, V), w_blocks, lam)
+    b = e.wiener()
+    e.close()
+    return a, b
+
+
+def test_wiener_reference_cases_on_device(dfm, oracle):
+    # test_wiener.cpp:39-141 on both device paths
+    x, T, V, lam, w = oracle.random_instance(3, 6, 3, 1, 2, 1)  # single source passes through
+    for s in _wiener_paths(dfm, x, T, V, lam, [w], [3]):
+        assert np.linalg.norm(s[0] - x) <= 1e-12 * np.linalg.norm(x)
+    x, T, V, lam, w = oracle.random_instance(2, 5, 3, 2, 2, 3)  # equal sources split in half
+    T[1] = T[0]
+    V[1] = V[0]
+    lam[:, 1] = lam[:, 0]
+    for s in _wiener_paths(dfm, x, T, V, lam, [w], [3]):
+        for n in range(2):
+            assert np.linalg.norm(s[n] - 0.5 * x) <= 1e-12 * np.linalg.norm(x)
+    for seed in range(4):  # direct-covariance formula, completeness
+        x, T, V, lam, w = oracle.random_instance(3, 7, 3, 2, 2, seed + 10)
+        ref = naive.wiener_direct(x, T, V, lam, w)
+        for s in _wiener_paths(dfm, x, T, V, lam, [w], [3]):
+            for n in range(2):
+                for i in range(3):
+                    assert np.linalg.norm(s[n, i] - ref[n, i]) <= 1e-9 * (1 + np.linalg.norm(ref[n, i]))
+            assert np.linalg.norm(s.sum(0) - x) <= 1e-9 * np.linalg.norm(x)
+    x, T, V, lam, w = oracle.random_instance(3, 8, 4, 2, 2, 41)  # one block == full, bitwise
+    full = dfm.wiener_full(x, dfm.NmfModel(T, V), dfm.SpatialModel(w, lam)).images
+    blk = dfm.wiener_block(x, dfm.NmfModel(T, V), dfm.BlockSpatialModel(dfm.BlockLayout([4]), [w], lam)).images
+    assert np.array_equal(full, blk)
+    x, T, V, lam, w = oracle.random_instance(3, 8, 6, 2, 2, 47)  # per-block oracle
+    sizes, o, wb = [2, 3, 1], 0, []
+    for mb in sizes:
+        wb.append(np.ascontiguousarray(w[:, o:o + mb, o:o + mb]))
+        o += mb
+    for s in _wiener_paths(dfm, x, T, V, lam, wb, sizes):
+        o = 0
+        for l, mb in enumerate(sizes):
+            ref = naive.wiener_direct(x[:, :, o:o + mb], T, V, lam[:, :, o:o + mb], wb[l])
+            for n in range(2):
+                for i in range(3):
+                    got = s[n, i, :, o:o + mb]
+                    assert np.linalg.norm(got - ref[n, i]) <= 1e-9 * (1 + np.linalg.norm(ref[n, i]))
+            o += mb
+        assert np.linalg.norm(s.sum(0) - x) <= 1e-9 * np.linalg.norm(x)
+
+
+def test_wiener_static_context_kernel_matches_step_kernel(dfm, oracle):
+    # the config-1 static-shape context kernel (in-CTA (W^H)^-1, reciprocal
+    # gains, per-warp staging) against the generic step kernel
+    F, T, N, K, sizes = 21, 300, 5, 16, [4, 4, 4]
+    layout = dfm.BlockLayout(sizes)
+    x = dfm.generate_mixture(1, F, T, 12, N, K, 91)
+    init = dfm.random_init(F, T, layout, N, K, 92)
+    a, b = _wiener_paths(dfm, x, init.nmf.T, init.nmf.V, init.lambda0, init.w0, sizes)
+    assert np.linalg.norm(a - b) <= 1e-12 * np.linalg.norm(a)
+    assert np.linalg.norm(b.sum(0) - x) <= 1e-9 * np.linalg.norm(x)
+
+
+def test_reconstruct_inverts_clean_images(dfm):
+    # test_wiener.cpp:143-160
+    from paper_2605_19388_b200 import stft as st
+
+    cfg = st.StftConfig(8000.0, 256, 64)
+    clean = np.random.default_rng(51).standard_normal((4096, 2))
+    waves = st.reconstruct([st.stft_forward(clean, cfg)], cfg, 4096)
+    assert len(waves) == 1
+    sl = slice(256, 4096 - 256)
+    assert np.linalg.norm(waves[0][sl] - clean[sl]) <= 1e-9 * np.linalg.norm(clean[sl])
+    zero = st.reconstruct([np.zeros((129, 60, 2), complex)], cfg, 4096)
+    assert not np.any(zero[0])
+    X = st.stft_forward(clean, cfg)
+    lin = st.reconstruct([2.0 * X, X], cfg, 4096)
+    assert np.linalg.norm(lin[0] - 2.0 * lin[1]) <= 1e-12 * np.linalg.norm(lin[0])
