@@ -511,20 +511,28 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     int fbs = 0;
     if constexpr (SB && MB_ <= 4) {
       constexpr int E = MB_ * (MB_ + 1) / 2;
-      for (int idx = tid; idx < nb * MB_; idx += FT) {
-        const int b = idx / MB_, mu = idx - b * MB_;
-        IpWork<MB_>& w = *(IpWork<MB_>*)(smem + sp.ipscr + b * ipscr_bytes<MAXMB>());
-        w.ok[mu] = chol_thread<MB_>(Qsum + a.qofs[b] + mu * E, w.L[mu], w.dinv[mu]) ? 1 : 0;
-      }
+      // block b -> warp b % nw, lanes 4 (b / nw) .. +3: the blocks' latency-bound
+      // sweeps run on different warps (schedulers), not all in warp 0
+      const int iw = tid >> 5, il = tid & 31, nw = FT >> 5;
+      const int l = il & 3;
+      for (int b = (il >> 2) * nw + iw; b < nb; b += 8 * nw)
+        if (l < MB_) {
+          IpWork<MB_>& w = *(IpWork<MB_>*)(smem + sp.ipscr + b * ipscr_bytes<MAXMB>());
+          w.ok[l] = chol_thread<MB_>(Qsum + a.qofs[b] + l * E, w.L[l], w.dinv[l]) ? 1 : 0;
+        }
       __syncthreads();
       em_stamp(a, 6);
-      const int l = tid & 3;
-      const unsigned qmask = 0xFu << (tid & 28);
-      for (int b = tid >> 2; b < nb; b += FT >> 2) {
+      // one quad per (bin, block) system; with at least as many warps as
+      // blocks each quad is lanes 0-3 of its own warp and the shuffle mask is
+      // the compile-time 0xF (a runtime mask makes every __shfl_sync carry
+      // convergence code: MATCH / REDUX / VOTE around each shuffle)
+      auto sweep = [&](int b, unsigned qmask) {
         IpWork<MB_>& w = *(IpWork<MB_>*)(smem + sp.ipscr + b * ipscr_bytes<MAXMB>());
         cd* wb = Wsm + b * MB_ * MB_;
         const cd* qb = Qsum + a.qofs[b];
+        const long long c0 = clock64();
         const bool ok = ip_sweep_quad<MB_>(wb, w, qb, floor_, l, qmask);
+        if (a.trace && b == 0 && l == 0) a.trace[blockIdx.x * 16 + 8] = (unsigned long long)(clock64() - c0);
         if (!ok && l == 0 && a.trace) atomicAdd(a.trace + blockIdx.x * 16 + 7, 1ull);
         if (!ok && l == 0) {
           // exact path (engine.cpp:47-49: LU, residual test, pinv) from W_old
@@ -534,6 +542,11 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
           if (fb) atomicAdd(a.fallbacks, fb);
         }
         __syncwarp(qmask);
+      };
+      if (nb <= nw) {
+        if (iw < nb && il < 4) sweep(iw, 0xFu);
+      } else {
+        for (int b = (il >> 2) * nw + iw; b < nb; b += 8 * nw) sweep(b, 0xFu << (il & 28));
       }
     } else {
       const int warp = tid >> 5, lane = tid & 31;

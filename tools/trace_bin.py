@@ -79,6 +79,9 @@ def main():
     chol = (buf.reshape(-1, 16)[:, 6].astype(np.int64) - t0 - tr[:, 3]) / 1e3
     if (buf.reshape(-1, 16)[:, 6] > 0).all():
         out["ip_cholesky_us_mean"] = round(float(chol.mean()), 3)
+    cyc = buf.reshape(-1, 16)[:, 8].astype(np.float64)
+    if cyc.max() > 0:
+        out["ip_sweep_cycles_block0_mean"] = float(cyc.mean())
     slow = buf.reshape(-1, 16)[:, 7]
     out["ip_slow_path_blocks"] = int(slow.sum())
     out["ip_slow_path_bins"] = int((slow > 0).sum())
