@@ -93,6 +93,13 @@ int dfm_set_model(dfm_ctx* ctx, const double* Tm, const double* V, const double*
                   const double* w);
 int dfm_get_model(dfm_ctx* ctx, double* Tm, double* V, double* lam, double* w);
 
+/* The same state in the context's device layouts, with no host-side
+ * transposes (a fast path for bindings whose arrays already have these
+ * shapes): T [F_local][N][K], V [N][K][T], lam [F_local][N][M],
+ * w [F_local][sum M_b^2] complex (per bin, each block col-major). */
+int dfm_set_model_native(dfm_ctx* ctx, const double* T, const double* V, const double* lam, const double* w);
+int dfm_get_model_native(dfm_ctx* ctx, double* T, double* V, double* lam, double* w);
+
 /* Multi-GPU frequency sharding: one NCCL communicator per context
  * (nccl_unique_id = the 128-byte ncclUniqueId broadcast by the caller).
  * The only per-iteration exchange is one allreduce of the V ("H") update

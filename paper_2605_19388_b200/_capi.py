@@ -43,6 +43,8 @@ _SIGS = {
     "dfm_set_obs": (_i, [_vp, _vp]),
     "dfm_set_model": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "dfm_get_model": (_i, [_vp, _vp, _vp, _vp, _vp]),
+    "dfm_set_model_native": (_i, [_vp, _vp, _vp, _vp, _vp]),
+    "dfm_get_model_native": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "dfm_comm_init": (_i, [_vp, _vp, _i, _i]),
     "dfm_nccl_get_unique_id": (_i, [_vp]),
     "dfm_fit": (_i, [_vp, _i, _vp, _vp, _vp]),

@@ -582,6 +582,36 @@ int dfm_get_model(dfm_ctx* c, double* Tm, double* V, double* lam, double* w) {
   DFM_API_END
 }
 
+// The device layouts directly (no host transposes): T [F][N][K], V [N][K][T],
+// lam [F][N][M], w [F][wsz] complex (per bin the blocks' col-major matrices).
+// For the Python mirror, whose math shapes are (nearly) these layouts.
+int dfm_set_model_native(dfm_ctx* c, const double* Tf, const double* V, const double* lam, const double* w) {
+  if (!c || !Tf || !V || !lam || !w) return DFM_ERR_ARG;
+  DFM_API_BEGIN
+  DFM_CK(cudaSetDevice(c->device));
+  c->Tf.upload(Tf, c->Tf.n, c->stream);
+  c->V.upload(V, c->V.n, c->stream);
+  c->lam.upload(lam, c->lam.n, c->stream);
+  c->W.upload((const cd*)w, c->W.n, c->stream);
+  DFM_CK(cudaStreamSynchronize(c->stream));
+  c->has_model = true;
+  return DFM_OK;
+  DFM_API_END
+}
+
+int dfm_get_model_native(dfm_ctx* c, double* Tf, double* V, double* lam, double* w) {
+  if (!c) return DFM_ERR_ARG;
+  DFM_API_BEGIN
+  DFM_CK(cudaSetDevice(c->device));
+  if (Tf) c->Tf.download(Tf, c->Tf.n, c->stream);
+  if (V) c->V.download(V, c->V.n, c->stream);
+  if (lam) c->lam.download(lam, c->lam.n, c->stream);
+  if (w) c->W.download((cd*)w, c->W.n, c->stream);
+  DFM_CK(cudaStreamSynchronize(c->stream));
+  return DFM_OK;
+  DFM_API_END
+}
+
 int dfm_nccl_get_unique_id(void* out128) {
   DFM_API_BEGIN
   ncclUniqueId id;

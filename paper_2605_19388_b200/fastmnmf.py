@@ -473,15 +473,43 @@ class Engine:
             raise ShapeMismatchError("run_engine: init has wrong number of demixer blocks")
         if lam.shape != (self.F, self.N, self.layout.total):
             raise ShapeMismatchError("run_engine: Lambda shape mismatch")
-        check(self.lib.dfm_set_model(self.ctx, _ptr(_c(nmf.T)), _ptr(_c(nmf.V)), _ptr(_c(lam)),
-                                     _ptr(_w_to_c(w_blocks))), "set_model")
+        # the context's device layouts (dfm_set_model_native): T (F, N, K),
+        # V (N, K, T) and Lambda (F, N, M) are the math shapes up to one
+        # transpose of T; W per bin is the blocks' col-major matrices
+        f0, f1 = self.f_begin, self.f_end
+        Tn = np.ascontiguousarray(np.asarray(nmf.T, dtype=np.float64)[:, f0:f1].transpose(1, 0, 2))
+        Vn = np.ascontiguousarray(nmf.V, dtype=np.float64)
+        ln = np.ascontiguousarray(np.asarray(lam, dtype=np.float64)[f0:f1])
+        wn = np.ascontiguousarray(np.concatenate(
+            [np.asarray(w, dtype=np.complex128)[f0:f1].transpose(0, 2, 1).reshape(f1 - f0, -1) for w in w_blocks],
+            axis=1))
+        check(self.lib.dfm_set_model_native(self.ctx, _ptr(Tn), _ptr(Vn), _ptr(ln), _ptr(wn)), "set_model")
 
     def get_model(self):
-        Tc = np.zeros((self.N, self.K, self.F)); Vc = np.zeros((self.N, self.T, self.K))
-        lc = np.zeros((self.F, self.layout.total, self.N))
-        wc = np.zeros(sum(self.F * s * s for s in self.layout.sizes), dtype=np.complex128)
-        check(self.lib.dfm_get_model(self.ctx, _ptr(Tc), _ptr(Vc), _ptr(lc), _ptr(wc)), "get_model")
-        return NmfModel(_uc(Tc), _uc(Vc)), _w_from_c(wc, self.F, self.layout.sizes), _uc(lc)
+        """(NmfModel, W blocks, Lambda) in global shapes; a frequency shard
+        fills its own bins [f_begin, f_end) (the others are zero)."""
+        Fl, f0, f1 = self.local_bins, self.f_begin, self.f_end
+        Tn = np.empty((Fl, self.N, self.K)); Vn = np.empty((self.N, self.K, self.T))
+        ln = np.empty((Fl, self.N, self.layout.total))
+        wn = np.empty((Fl, sum(s * s for s in self.layout.sizes)), dtype=np.complex128)
+        check(self.lib.dfm_get_model_native(self.ctx, _ptr(Tn), _ptr(Vn), _ptr(ln), _ptr(wn)), "get_model")
+        full = f0 == 0 and f1 == self.F
+        T = np.zeros((self.N, self.F, self.K))
+        T[:, f0:f1] = Tn.transpose(1, 0, 2)
+        lam = ln if full else np.zeros((self.F, self.N, self.layout.total))
+        if not full:
+            lam[f0:f1] = ln
+        wb, o = [], 0
+        for mb in self.layout.sizes:
+            blk = wn[:, o:o + mb * mb].reshape(Fl, mb, mb).transpose(0, 2, 1)
+            if full:
+                wb.append(np.ascontiguousarray(blk))
+            else:
+                g = np.zeros((self.F, mb, mb), dtype=np.complex128)
+                g[f0:f1] = blk
+                wb.append(g)
+            o += mb * mb
+        return NmfModel(T, Vn), wb, lam
 
     def comm_init(self, unique_id: bytes, nranks: int, rank: int) -> None:
         buf = C.create_string_buffer(bytes(unique_id), 128)
