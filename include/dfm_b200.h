@@ -20,6 +20,12 @@
  *   dfm_comm_init                   (new) frequency sharding, SURVEY.md §8e
  *   dfm_step_*                      per-update API (src/fastmnmf.cpp:43-116,
  *                                   src/dist.cpp:20-49)
+ *   dfm_fit_many                    (new) batches of independent mixtures
+ *   dfm_init_pipeline, dfm_cluster_masks, dfm_align_*, dfm_init_scm_spectrogram,
+ *   dfm_is_nmf, dfm_init_spatial    init_full / init_distributed and their stages
+ *                                   (src/init.cpp:76-472, src/hermlin.cpp:25-53)
+ *   dfm_stft_forward / _inverse     stft_forward / stft_inverse (src/stft.cpp:70-139)
+ *   dfm_fmnm_*                      save_model / load_model (src/io.cpp:49-135)
  *
  * Buffer conventions: every buffer is HOST memory owned by the caller, laid
  * out exactly as the reference's Eigen column-major containers, concatenated:
@@ -141,10 +147,10 @@ int dfm_fit_many(dfm_ctx* const* ctxs, int n, int iters, double* cost_traces,
                  double* elapsed_seconds);
 
 /* Benchmark hooks: one steady-state EM iteration (per-bin kernel in
- * "finish previous + start next" mode, T update, V weights, V update,
- * spectrogram), enqueued on the context stream; dfm_prime runs the first
- * (cost-only) launch.  Device time
- * of the last dfm_bench_step is returned by dfm_bench_last_ms. */
+ * "finish previous + start next" mode, T update + h' = T V, V weights,
+ * V update + H = T V), enqueued on the context stream; dfm_prime runs the
+ * first (cost-only) launch.  Device time of the last dfm_bench_step is
+ * returned by dfm_bench_last_ms. */
 int dfm_prime(dfm_ctx* ctx);
 int dfm_bench_step(dfm_ctx* ctx);
 int dfm_sync(dfm_ctx* ctx);
@@ -157,7 +163,8 @@ int dfm_bench_step_many(dfm_ctx* const* ctxs, int n, double* ms_out);
 /* dfm_bench_step replays the iteration as a CUDA graph (one launch).
  * dfm_bench_split_step runs the same iteration as stream launches with events
  * between the kernels; dfm_bench_last_split then returns the device time of
- * each kernel (ms): {k_em_bin, k_tupd, k_spec+k_pdw, k_vupd (+ allreduce), k_spec}. */
+ * each part (ms): {k_em_bin, k_tupd + h', k_pdw, k_vupd + H (sharded: partial
+ * V update + allreduce + k_vapply), tail (sharded: H = T V)}. */
 int dfm_bench_split_step(dfm_ctx* ctx);
 int dfm_bench_last_split(dfm_ctx* ctx, double* ms5);
 /* Kernel launches issued by the context so far (for the bench's gpu_launches). */
@@ -176,14 +183,17 @@ int dfm_get_trace(dfm_ctx* ctx, unsigned long long* out, int n);
  * frame reduction, bit1 the Q accumulation of the per-bin kernel. */
 int dfm_debug_bits(dfm_ctx* ctx, int bits);
 /* Tests: run the frequency-sharded path (V-update {num, den} through
- * ncclAllReduce, then k_vapply; no graph) even on a one-rank communicator. */
+ * ncclAllReduce, then k_vapply and H = T V; captured in the step graph) even
+ * on a one-rank communicator. */
 int dfm_force_collective(dfm_ctx* ctx, int on);
 
 /* Use the generic (runtime-shape) bin kernel even when a compile-time-shape
  * instantiation matches the layout (A/B testing of the two code paths). */
 int dfm_force_generic(dfm_ctx* ctx, int on);
-int dfm_get_tiling(const dfm_ctx* ctx, int* bins_per_cta, int* cluster_size, int* frames_per_cta,
-                   int* threads, int* smem_bytes);
+/* Current tiling: frame_tile (threads per bin CTA), pd_frames, the bin
+ * kernel's CTA count, threads per CTA and dynamic shared memory. */
+int dfm_get_tiling(const dfm_ctx* ctx, int* frame_tile, int* pd_frames, int* ctas, int* threads,
+                   int* smem_bytes);
 
 /* Multichannel Wiener separation of the context's local bins with the
  * current model (wiener_block, wiener.cpp:50-69, shared spectrograms).
