@@ -318,4 +318,237 @@ __device__ __forceinline__ double rsqrt_pos(double x) {
   return r;
 }
 
+// Fast IP path for blocks handled by a whole warp (the large-block
+// counterpart of ip_sweep_quad in dfm_ip.cuh; engine.cpp:40-51 for
+// mu = 0..mb-1).  The work that does not depend on the sweep order runs
+// first, spread over the CTA's warps:
+//   ip_winv_warp       W^-1 (warp LU of W, lanes solve the identity columns)
+//                      and the entry value of W (restored on a failure),
+//   herm_inverse_warp  Q_mu^-1 for every mu (Hermitian sweep operator),
+// so that each column of ip_sweep_warp is a handful of lane-parallel
+// matrix-vector products instead of dependent triangular solves.
+// sum_{c < n} term(c) with four independent accumulators: a dependent FP64
+// FMA costs ~23 cycles on sm_100, so a single running sum over a row of a
+// small matrix is latency-bound four times over.
+template <class F>
+__device__ __forceinline__ cd dot4(int n, const F& term) {
+  cd a0{0.0, 0.0}, a1{0.0, 0.0}, a2{0.0, 0.0}, a3{0.0, 0.0};
+  int c = 0;
+  for (; c + 4 <= n; c += 4) {
+    a0 = a0 + term(c);
+    a1 = a1 + term(c + 1);
+    a2 = a2 + term(c + 2);
+    a3 = a3 + term(c + 3);
+  }
+  for (; c < n; ++c) a0 = a0 + term(c);
+  return (a0 + a1) + (a2 + a3);
+}
+
+// W^-1 by Gauss-Jordan with partial pivoting on [W | I], one lane per column
+// of the augmented matrix (lanes 0..mb-1: W in s.V, lanes mb..2mb-1: I in
+// s.S, which ends as W^-1); the entry value of W is kept in s.S0.  A zero
+// pivot column (singular W) poisons W^-1(0, 0) with NaN, which sends the
+// sweep to the exact path at its first column.
+template <int MB>
+__device__ void ip_winv_warp(int mb, const cd* W, IpScratch<MB>& s) {
+  const int lane = threadIdx.x & 31;
+  const int n2 = mb * mb;
+  for (int i = lane; i < n2; i += 32) {
+    s.S0[i] = W[i];
+    s.V[i] = W[i];
+    s.S[i] = cd{(i % mb) == (i / mb) ? 1.0 : 0.0, 0.0};
+  }
+  __syncwarp();
+  const bool act = lane < 2 * mb;
+  cd* col = lane < mb ? s.V + lane * mb : s.S + (act ? lane - mb : 0) * mb;
+  for (int k = 0; k < mb; ++k) {
+    const cd* ck = s.V + k * mb;
+    // pivot: largest |W(r, k)|, r >= k (lane-parallel argmax)
+    double best = (lane >= k && lane < mb) ? norm2(ck[lane]) : -1.0;
+    int piv = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int op = __shfl_xor_sync(0xffffffffu, piv, o);
+      if (ob > best || (ob == best && op < piv)) {
+        best = ob;
+        piv = op;
+      }
+    }
+    if (!(best > 0.0) || !isfinite(best)) {
+      __syncwarp();
+      if (lane == 0) s.S[0] = cd{NAN, 0.0};
+      __syncwarp();
+      return;
+    }
+    const cd p = ck[piv];
+    const double ib = rcp_pos(best);
+    const cd ip{p.re * ib, -p.im * ib};
+    __syncwarp();
+    // column k (lane k) would become e_k; it is read in this step only
+    if (act && lane != k) {
+      const cd xk = col[piv] * ip;  // the new pivot-row entry of this column
+      if (piv != k) col[piv] = col[k];
+      col[k] = xk;
+#pragma unroll 4
+      for (int r = 0; r < mb; ++r)
+        if (r != k) col[r] = col[r] - (r == piv ? ck[k] : ck[r]) * xk;
+    }
+    __syncwarp();
+  }
+}
+
+// Packed Hermitian entry (r, c): the upper triangle is stored, (r, c) with
+// r <= c at c (c + 1) / 2 + r.
+__device__ __forceinline__ cd herm_at(const cd* P, int r, int c) {
+  const bool up = r <= c;
+  const cd v = P[up ? c * (c + 1) / 2 + r : r * (r + 1) / 2 + c];
+  return cd{v.re, up ? v.im : -v.im};
+}
+
+// In-place inverses of nq packed Hermitian positive-definite matrices stored
+// back to back (stride mb (mb + 1) / 2), one warp, by the sweep operator:
+// sweeping pivot k maps
+//   a_kk -> -1/a_kk,  a_ik -> a_ik / a_kk,  a_ij -> a_ij - a_ik a_kj / a_kk,
+// and after every pivot each array holds -P^-1 (negated at the end).  All nq
+// matrices advance together, so their dependent FP64 chains overlap.  The
+// pivots are the successive Schur complements, positive for a positive
+// definite P; a non-positive one poisons that matrix's entry (0, 0) with NaN,
+// which makes the sweep's u non-finite and sends the system to the exact
+// path.  NE bounds the entries per lane (nq * E <= 32 * NE).
+template <int NE>
+__device__ void herm_inverse_warp(int mb, int nq, cd* P) {
+  const int lane = threadIdx.x & 31;
+  const int E = mb * (mb + 1) / 2, tot = nq * E;
+  int rr[NE], cc[NE], base[NE];
+#pragma unroll
+  for (int j = 0; j < NE; ++j) {
+    const int g = lane + 32 * j;
+    const int q = g < tot ? g / E : 0, e = g < tot ? g - q * E : 0;
+    int c = 0;
+    while ((c + 1) * (c + 2) / 2 <= e) ++c;
+    rr[j] = e - c * (c + 1) / 2;
+    cc[j] = c;
+    base[j] = q * E;
+  }
+  bool bad = false;
+  for (int k = 0; k < mb; ++k) {
+    const int kk = k * (k + 1) / 2 + k;
+    cd nv[NE];
+#pragma unroll
+    for (int j = 0; j < NE; ++j) {
+      if (32 * j >= tot) break;  // warp-uniform: no predicated-off copies of empty slots
+      const int g = lane + 32 * j;
+      if (g < tot) {  // branch-free: the three cases would serialise three FP64 chains
+        const cd* M = P + base[j];
+        const int r = rr[j], c = cc[j];
+        const double d = M[kk].re;
+        bad |= !(d > 0.0);
+        const double id = rcp_pos(d);
+        const cd t = P[g];
+        const cd gen = t - herm_at(M, r, k) * herm_at(M, k, c) * id;
+        const cd h = t * id;
+        const bool rk = r == k, ck = c == k;
+        nv[j] = (rk && ck) ? cd{-id, 0.0} : ((rk || ck) ? h : gen);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < NE; ++j) {
+      if (32 * j >= tot) break;
+      if (lane + 32 * j < tot) P[lane + 32 * j] = nv[j];
+    }
+    __syncwarp();
+  }
+  // a failed pivot of matrix q: poison (0, 0) after the negation below
+#pragma unroll
+  for (int j = 0; j < NE; ++j) {
+    const int g = lane + 32 * j;
+    if (g < tot) P[g] = cd{-P[g].re, -P[g].im};
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < NE; ++j) {
+    const int g = lane + 32 * j;
+    if (g < tot && bad) P[base[j]] = cd{NAN, 0.0};
+  }
+  __syncwarp();
+}
+
+// The column sweep (lane r owns row r), given s.S = W^-1, s.S0 = W and the
+// packed Q_mu^-1 in qi:
+//   u = Q_mu^-1 W^-H e_mu  (= (W^H Q_mu)^-1 e_mu),
+//   u /= sqrt(max(Re(u^H Q u), floor)), W[:, mu] = u, and W^-1 refreshed
+//   by Sherman-Morrison.
+// The reference's per-column test ||W^H Q u - e_mu|| <= 1e-6 (against the
+// W of that column, engine.cpp:47-49) and the finiteness checks are
+// recorded per column and evaluated once after the sweep: a failure anywhere
+// discards the whole fast sweep (W restored, false returned) and the caller
+// reruns the exact ip_column_warp sweep from the same W, so deferring the
+// test changes nothing but the critical path.  Scalars every lane needs
+// (Re u^H Q u, z_mu) are formed redundantly from shared vectors instead of
+// by shuffle reductions.  qb / qi: packed upper triangles of Q_0..Q_{mb-1}
+// and of their inverses.  s.V holds the per-column residual partials.
+template <int MB>
+__device__ bool ip_sweep_warp(int mb, cd* W, const cd* qb, const cd* qi, double floor_, IpScratch<MB>& s) {
+  const int lane = threadIdx.x & 31;
+  const int n2 = mb * mb, E = mb * (mb + 1) / 2;
+  const bool act = lane < mb;
+  const int la = act ? lane : 0;
+  double* res = reinterpret_cast<double*>(s.V);  // res[mu * mb + lane] = |(W^H Q u - e_mu)_lane|^2
+  bool bad = false;
+#pragma unroll 1
+  for (int mu = 0; mu < mb; ++mu) {
+    const cd* qp = qb + mu * E;
+    const cd* ip = qi + mu * E;
+    // u_r = sum_c Q^-1(r, c) conj(W^-1(mu, c))
+    const cd u = dot4(mb, [&](int c) { return herm_at(ip, la, c) * conjg(s.S[c * mb + mu]); });
+    const cd rowmu = s.S[la * mb + mu];  // W^-1(mu, la), for the rank-one update
+    bad |= act && !cfinite(u);
+    if (act) s.u[lane] = u;
+    __syncwarp();
+    const cd qu = dot4(mb, [&](int c) { return herm_at(qp, la, c) * s.u[c]; });
+    if (act) s.e[lane] = qu;
+    __syncwarp();
+    const double nq = dot4(mb, [&](int a) { return cmulc(s.u[a], s.e[a]); }).re;  // every lane
+    cd r = dot4(mb, [&](int k) { return cmulc(W[la * mb + k], s.e[k]); });
+    if (lane == mu) r.re -= 1.0;
+    if (act) res[mu * mb + lane] = norm2(r);
+    const double isc = rsqrt_pos(fmax(nq, floor_));
+    const cd un{u.re * isc, u.im * isc};
+    const cd d = un - W[mu * mb + la];
+    __syncwarp();
+    if (act) s.u[lane] = d;
+    __syncwarp();
+    // Sherman-Morrison: (W + d e_mu^T)^-1 = W^-1 - z (e_mu^T W^-1) / (1 + z_mu), z = W^-1 d
+    const cd z = dot4(mb, [&](int c) { return s.S[c * mb + la] * s.u[c]; });
+    const cd zmu = dot4(mb, [&](int c) { return s.S[c * mb + mu] * s.u[c]; });  // every lane
+    const cd den{1.0 + zmu.re, zmu.im};
+    const double dn = norm2(den);
+    bad |= !(dn > 0.0);
+    const double idn = rcp_pos(dn);
+    const cd iden{den.re * idn, -den.im * idn};
+    if (act) s.e[lane] = rowmu * iden;
+    __syncwarp();
+    if (act) {
+#pragma unroll 4
+      for (int c = 0; c < mb; ++c) s.S[c * mb + la] = s.S[c * mb + la] - z * s.e[c];
+      W[mu * mb + la] = un;
+    }
+    __syncwarp();
+  }
+  // lane mu < mb: the residual of column mu
+  if (act) {
+    double r2 = 0.0;
+    for (int a = 0; a < mb; ++a) r2 += res[lane * mb + a];
+    bad |= !(r2 <= 1e-12);
+  }
+  if (__any_sync(0xffffffffu, bad)) {
+    for (int i = lane; i < n2; i += 32) W[i] = s.S0[i];
+    __syncwarp();
+    return false;
+  }
+  return true;
+}
+
 }  // namespace dfm

@@ -550,19 +550,54 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
       }
     } else {
       const int warp = tid >> 5, lane = tid & 31;
+      // order-independent work first, one task per warp: W^-1 of every
+      // block, then Q_mu^-1 of every (block, mu) into the free reduction area
+      cd* Qinv = (cd*)(smem + sp.red);
+      {
+        const int nw = sp.nwarps;
+        for (int b = warp; b < nb; b += nw)
+          ip_winv_warp<MAXMB>(MBof(b), Wsm + WOFF(b),
+                              *(IpScratch<MAXMB>*)(smem + sp.ipscr + b * ipscr_bytes<MAXMB>()));
+        // each block's Q_mu^-1 in contiguous mu chunks, inverted together; on
+        // the warps without a W^-1 task when there are enough of them
+        const int w0 = (nb < nw && nw - nb >= nb) ? nb : 0, nq_w = nw - w0;
+        if (warp >= w0)
+          for (int b = 0; b < nb; ++b) {
+            const int mb = MBof(b), E = mb * (mb + 1) / 2;
+            const int per = (mb + nq_w - 1) / nq_w;
+            const int m0 = (warp - w0) * per, m1 = min(mb, m0 + per);
+            const int g = max(1, 320 / E);
+            for (int q0 = m0; q0 < m1; q0 += g) {
+              const int nq = min(g, m1 - q0);
+              const cd* src = Qsum + a.qofs[b] + q0 * E;
+              cd* dst = Qinv + a.qofs[b] + q0 * E;
+              for (int e = lane; e < nq * E; e += 32) dst[e] = src[e];
+              __syncwarp();
+              herm_inverse_warp<10>(mb, nq, dst);
+            }
+          }
+      }
+      __syncthreads();
+      em_stamp(a, 6);
       for (int b = warp; b < nb; b += sp.nwarps) {
         const int mb = MBof(b);
         const int E = mb * (mb + 1) / 2;
         IpScratch<MAXMB>& sc = *(IpScratch<MAXMB>*)(smem + sp.ipscr + b * ipscr_bytes<MAXMB>());
         cd* wb = Wsm + WOFF(b);
         fbs = 0;
-        for (int mu = 0; mu < mb; ++mu) {
-          const cd* qp = Qsum + a.qofs[b] + mu * E;
-          auto qget = [&](int r, int c) {
-            return r <= c ? qp[c * (c + 1) / 2 + r] : conjg(qp[r * (r + 1) / 2 + c]);
-          };
-          fbs += ip_column_warp<MAXMB>(mb, wb, mu, qget, floor_, sc);
-        }
+        const long long c0 = clock64();
+        const bool ok = ip_sweep_warp<MAXMB>(mb, wb, Qsum + a.qofs[b], Qinv + a.qofs[b], floor_, sc);
+        if (a.trace && b == 0 && lane == 0) a.trace[blockIdx.x * 16 + 8] = (unsigned long long)(clock64() - c0);
+        if (!ok && lane == 0 && a.trace) atomicAdd(a.trace + blockIdx.x * 16 + 7, 1ull);
+        // exact path (engine.cpp:47-49: LU, residual test, pinv), W restored
+        if (!ok)
+          for (int mu = 0; mu < mb; ++mu) {
+            const cd* qp = Qsum + a.qofs[b] + mu * E;
+            auto qget = [&](int r, int c) {
+              return r <= c ? qp[c * (c + 1) / 2 + r] : conjg(qp[r * (r + 1) / 2 + c]);
+            };
+            fbs += ip_column_warp<MAXMB>(mb, wb, mu, qget, floor_, sc);
+          }
         if (lane == 0 && fbs) atomicAdd(a.fallbacks, fbs);
       }
     }
