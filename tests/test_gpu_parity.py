@@ -226,9 +226,11 @@ def test_engine_zero_iterations_and_final_cost(dfm, oracle):
     assert final == pytest.approx(a.report.cost_trace[-1], rel=1e-12)
 
 
-def test_engine_adversarial_stays_finite(dfm, oracle):
-    # test_fastmnmf.cpp:377-404 — exercises the device pinv fallback
-    x, layout, init = _inst(oracle, 3, 10, 4, 2, 2, 77)
+@pytest.mark.parametrize("M", [4, 8])
+def test_engine_adversarial_stays_finite(dfm, oracle, M):
+    # test_fastmnmf.cpp:377-404 — exercises the device pinv fallback (M = 4:
+    # the quad fast path; M = 8: the warp fast path with precomputed inverses)
+    x, layout, init = _inst(oracle, 3, 10, M, 2, 2, 77)
     x[:, :, 1] = 0
     x[:, :, 3] = x[:, :, 2]
     fit = dfm.fit_full(x, init, 60)
@@ -237,8 +239,12 @@ def test_engine_adversarial_stays_finite(dfm, oracle):
     assert np.all(np.isfinite(fit.spatial.W))
     assert not np.any(np.isnan(fit.report.cost_trace))
     assert fit.report.fallbacks > 0
-    ref = oracle.run_engine(x, [4], _init_dict(init), 60)
+    ref = oracle.run_engine(x, [M], _init_dict(init), 60)
     assert fit.report.fallbacks == ref["fallbacks"]
+    c, r = fit.report.cost_trace, ref["cost_trace"]
+    fin = np.isfinite(r)  # a singular W gives the reference's +inf cost
+    assert np.array_equal(np.isfinite(c), fin) and np.array_equal(c[~fin], r[~fin])
+    assert np.all(np.abs(c[fin] - r[fin]) <= 1e-6 * np.abs(r[fin]))
 
 
 def test_engine_underdetermined_and_independent_mode(dfm, oracle):
