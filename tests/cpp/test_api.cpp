@@ -1,0 +1,356 @@
+// The C++ host API (include/fastmnmf_b200.hpp) exercised the way the
+// reference's own C++ tests exercise proj/include (test_fastmnmf.cpp,
+// test_dist.cpp, test_wiener.cpp, test_stft.cpp, test_io.cpp), with the CPU
+// oracle (oracle/, test infrastructure only) as the checker on the same
+// seeded inputs.  Built by __graft_entry__.build(); run on a GPU by
+// tests/test_cpp_api.py.  Prints "ALL PASSED" and exits 0 on success.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "dfm_oracle.h"
+#include "fastmnmf_b200.hpp"
+
+using namespace fastmnmf;
+
+namespace {
+
+int g_checks = 0, g_failed = 0;
+
+void expect(bool ok, const std::string& what) {
+  ++g_checks;
+  if (!ok) {
+    ++g_failed;
+    std::printf("FAIL: %s\n", what.c_str());
+  }
+}
+
+double rel(double a, double b) { return std::abs(a - b) / std::max(std::abs(b), 1e-300); }
+
+template <class F>
+bool throws(F&& f, const std::function<bool(const std::exception&)>& kind) {
+  try {
+    f();
+  } catch (const std::exception& e) {
+    return kind(e);
+  }
+  return false;
+}
+
+// the oracle's reference-order buffers for a bundle (the same order the C ABI uses)
+struct Flat {
+  std::vector<double> T, V, lam;
+  std::vector<cplx> w;
+};
+Flat flatten(const InitBundle& b) {
+  Flat f;
+  for (const auto& t : b.nmf.T) f.T.insert(f.T.end(), t.data(), t.data() + t.size());
+  for (const auto& v : b.nmf.V) f.V.insert(f.V.end(), v.data(), v.data() + v.size());
+  for (const auto& L : b.lambda0) f.lam.insert(f.lam.end(), L.data(), L.data() + L.size());
+  for (const auto& blk : b.w0)
+    for (const auto& w : blk) f.w.insert(f.w.end(), w.data(), w.data() + w.size());
+  return f;
+}
+
+ObsTensor mixture(int F, int T, int M, int N, int K, uint64_t seed, std::vector<cplx>& flat) {
+  flat.assign(static_cast<size_t>(F) * T * M, cplx{});
+  dfo_generate_mixture(1, F, T, M, N, K, seed, reinterpret_cast<double*>(flat.data()));
+  ObsTensor x(F, T, M);
+  for (int f = 0; f < F; ++f)
+    std::memcpy(x.bins[f].data(), flat.data() + static_cast<size_t>(f) * T * M, sizeof(cplx) * T * M);
+  return x;
+}
+
+// random_init is bit-exact with the reference's RNG streams (init.cpp:496-521)
+void test_random_init() {
+  const BlockLayout layout({2, 3});
+  const int F = 7, T = 11, N = 3, K = 4;
+  const InitBundle b = random_init(F, T, layout, N, K, 99);
+  Flat o;
+  o.T.resize(static_cast<size_t>(N) * F * K);
+  o.V.resize(static_cast<size_t>(N) * K * T);
+  o.lam.resize(static_cast<size_t>(F) * N * 5);
+  o.w.resize(static_cast<size_t>(F) * (4 + 9));
+  dfo_random_init(F, T, 2, layout.sizes.data(), N, K, 99, o.T.data(), o.V.data(), o.lam.data(),
+                  reinterpret_cast<double*>(o.w.data()));
+  const Flat d = flatten(b);
+  expect(d.T == o.T && d.V == o.V && d.lam == o.lam && d.w == o.w, "random_init bit-exact with the oracle");
+}
+
+// fit trajectory against the oracle's run_engine (north_star: 1e-8 relative
+// over 20 iterations), monotone, final cost == cost_dist (test_fastmnmf.cpp:351-375)
+void test_fit_matches_oracle(const std::vector<int>& sizes) {
+  const BlockLayout layout(sizes);
+  const int F = 9, T = 40, M = layout.total, N = 3, K = 4, iters = 20;
+  std::vector<cplx> xf;
+  const ObsTensor x = mixture(F, T, M, N, K, 5, xf);
+  const InitBundle init = random_init(F, T, layout, N, K, 17);
+  const DistFit fit = fit_distributed(x, layout, init, iters, true);
+  Flat o = flatten(init);
+  std::vector<double> cost(iters + 1), wall(iters), stages(4), ops(2);
+  const int fb = dfo_run_engine(F, T, M, reinterpret_cast<const double*>(xf.data()), layout.num_blocks(),
+                                layout.sizes.data(), N, K, o.T.data(), o.V.data(), o.lam.data(),
+                                reinterpret_cast<double*>(o.w.data()), iters, kFloor, cost.data(), wall.data(),
+                                stages.data(), ops.data());
+  std::string tag = "layout {";
+  for (int s : sizes) tag += std::to_string(s) + ",";
+  tag += "}";
+  expect(fit.report.cost_trace.size() == static_cast<size_t>(iters + 1), tag + ": trace length");
+  double worst = 0;
+  for (int i = 0; i <= iters; ++i) worst = std::max(worst, rel(fit.report.cost_trace[i], cost[i]));
+  expect(worst < 1e-8, tag + ": cost trajectory within 1e-8 of the oracle (" + std::to_string(worst) + ")");
+  bool mono = true;
+  for (int i = 1; i <= iters; ++i)
+    mono = mono && fit.report.cost_trace[i] <= fit.report.cost_trace[i - 1] + 1e-9 * std::abs(fit.report.cost_trace[i - 1]);
+  expect(mono, tag + ": cost non-increasing");
+  expect(fit.report.fallbacks == fb, tag + ": pinv fallback count equals the oracle's");
+  expect(fit.report.ops.w_update == ops[0] && fit.report.ops.mm_update == ops[1], tag + ": op counters");
+  double tmax = 0;
+  for (int n = 0; n < N; ++n)
+    for (int k = 0; k < K; ++k)
+      for (int f = 0; f < F; ++f)
+        tmax = std::max(tmax, rel(fit.models[0].T[n](f, k), o.T[(static_cast<size_t>(n) * K + k) * F + f]));
+  expect(tmax < 1e-7, tag + ": fitted T within 1e-7");
+  const double final_cost = cost_dist(x, fit.models[0], fit.spatial);
+  expect(rel(final_cost, fit.report.cost_trace.back()) < 1e-10, tag + ": cost_dist equals the last trace entry");
+  double oc = 0;
+  o = flatten(init);  // cost of the initial model through both paths
+  dfo_cost_dist(F, T, M, reinterpret_cast<const double*>(xf.data()), layout.num_blocks(), layout.sizes.data(), N, K,
+                o.T.data(), o.V.data(), o.lam.data(), reinterpret_cast<const double*>(o.w.data()), kFloor, &oc);
+  BlockSpatialModel s0{layout, init.w0, init.lambda0};
+  expect(rel(cost_dist(x, init.nmf, s0), oc) < 1e-10, tag + ": cost_dist of the init equals the oracle's");
+}
+
+// independent mode equals fit_single per block (test_dist.cpp:184-213)
+void test_independent_mode() {
+  const BlockLayout layout({2, 3});
+  const int F = 5, T = 24, N = 2, K = 3, iters = 8;
+  std::vector<cplx> xf;
+  const ObsTensor x = mixture(F, T, layout.total, N, K, 8, xf);
+  const InitBundle init = random_init(F, T, layout, N, K, 3);
+  const DistFit dist = fit_distributed(x, layout, init, iters, false);
+  expect(!dist.shared && dist.models.size() == 2, "independent: one model per block");
+  double sum0 = 0;
+  for (int l = 0; l < 2; ++l) {
+    const FullFit single = fit_single(extract_block(x, layout, l), slice_init(init, l), iters);
+    bool same = true;
+    for (int n = 0; n < N; ++n) {
+      same = same && std::memcmp(single.nmf.T[n].data(), dist.models[l].T[n].data(), sizeof(double) * F * K) == 0;
+      same = same && std::memcmp(single.nmf.V[n].data(), dist.models[l].V[n].data(), sizeof(double) * K * T) == 0;
+    }
+    for (int f = 0; f < F; ++f)
+      same = same && std::memcmp(single.spatial.W[f].data(), dist.spatial.W[l][f].data(),
+                                 sizeof(cplx) * single.spatial.W[f].size()) == 0;
+    expect(same, "independent: block " + std::to_string(l) + " bitwise equal to fit_single");
+    sum0 += single.report.cost_trace[0];
+  }
+  expect(rel(dist.report.cost_trace[0], sum0) < 1e-14, "independent: cost trace is the sum of the blocks'");
+  expect(rel(cost_dist(x, dist.models, dist.spatial), dist.report.cost_trace.back()) < 1e-10,
+         "independent: cost_dist (one model per block) equals the last trace entry");
+}
+
+// Wiener against the oracle, completeness (test_wiener.cpp:39-141)
+void test_wiener() {
+  const BlockLayout layout({2, 2});
+  const int F = 6, T = 20, M = 4, N = 3, K = 3;
+  std::vector<cplx> xf;
+  const ObsTensor x = mixture(F, T, M, N, K, 12, xf);
+  const InitBundle init = random_init(F, T, layout, N, K, 4);
+  const DistFit fit = fit_distributed(x, layout, init, 5, true);
+  const SourceImages img = wiener_block(x, fit.models, fit.spatial);
+  expect(img.num_sources() == N, "wiener: one image per source");
+  InitBundle fitted{layout, fit.models[0], fit.spatial.W, fit.spatial.Lambda, {}, {}};
+  Flat o = flatten(fitted);
+  std::vector<cplx> ref(static_cast<size_t>(N) * F * T * M);
+  dfo_wiener_block(F, T, M, reinterpret_cast<const double*>(xf.data()), 2, layout.sizes.data(), N, K, o.T.data(),
+                   o.V.data(), o.lam.data(), reinterpret_cast<const double*>(o.w.data()), kFloor,
+                   reinterpret_cast<double*>(ref.data()));
+  double num = 0, den = 0, comp = 0, xn = 0;
+  for (int n = 0; n < N; ++n)
+    for (int f = 0; f < F; ++f)
+      for (int t = 0; t < T; ++t)
+        for (int m = 0; m < M; ++m) {
+          const cplx a = img.images[n].bins[f](m, t), b = ref[((static_cast<size_t>(n) * F + f) * T + t) * M + m];
+          num += std::norm(a - b);
+          den += std::norm(b);
+        }
+  for (int f = 0; f < F; ++f)
+    for (int t = 0; t < T; ++t)
+      for (int m = 0; m < M; ++m) {
+        cplx s{};
+        for (int n = 0; n < N; ++n) s += img.images[n].bins[f](m, t);
+        comp += std::norm(s - x.bins[f](m, t));
+        xn += std::norm(x.bins[f](m, t));
+      }
+  expect(std::sqrt(num / den) < 1e-9, "wiener_block matches the oracle");
+  expect(std::sqrt(comp / xn) < 1e-9, "wiener images add up to the mixture");
+}
+
+// exception types of the reference API
+void test_errors() {
+  const BlockLayout layout({2, 2});
+  std::vector<cplx> xf;
+  const ObsTensor x = mixture(3, 10, 4, 2, 2, 1, xf);
+  const InitBundle init = random_init(3, 10, layout, 2, 2, 1);
+  auto is_shape = [](const std::exception& e) { return dynamic_cast<const ShapeMismatch*>(&e) != nullptr; };
+  expect(throws([&] { fit_distributed(x, BlockLayout({3, 2}), init, 1, true); }, is_shape),
+         "layout/channel mismatch throws ShapeMismatch");
+  expect(throws([&] { fit_full(x, init, 1); }, is_shape), "a two-block init in fit_full throws ShapeMismatch");
+  SpatialModel sing;
+  for (int f = 0; f < 3; ++f) {
+    sing.W.push_back(MatrixXcd::Identity(4));
+    sing.Lambda.push_back(MatrixXd::Constant(2, 4, 1.0));
+  }
+  sing.W[1] = MatrixXcd::Zero(4, 4);
+  expect(throws([&] { cost_full(x, init.nmf, sing); },
+                [](const std::exception& e) { return dynamic_cast<const SingularDemixer*>(&e) != nullptr; }),
+         "cost_full with a singular W throws SingularDemixer");
+  expect(throws([&] { stft_forward(MatrixXd::Zero(100, 2), StftConfig{16000.0, 256, 64}); },
+                [](const std::exception& e) { return dynamic_cast<const SignalTooShort*>(&e) != nullptr; }),
+         "stft_forward of a short signal throws SignalTooShort");
+  expect(throws([&] { fit_distributed(x, layout, init, -1, true); },
+                [](const std::exception& e) { return dynamic_cast<const std::invalid_argument*>(&e) != nullptr; }),
+         "negative iteration count throws invalid_argument");
+}
+
+// STFT round trip on the fully-overlapped interior (test_stft.cpp)
+void test_stft() {
+  const int L = 4096, C = 2;
+  MatrixXd s(L, C);
+  uint64_t st = 7;
+  for (int c = 0; c < C; ++c)
+    for (int i = 0; i < L; ++i) s(i, c) = std::sin(0.01 * i * (c + 1)) + 0.1 * (dfo_splitmix64(&st) % 1000) / 1000.0;
+  const StftConfig cfg{16000.0, 512, 128};
+  const ObsTensor X = stft_forward(s, cfg);
+  expect(X.num_bins() == 257 && X.num_frames() == stft_num_frames(cfg, L) && X.num_channels() == C, "stft shape");
+  const MatrixXd back = stft_inverse(X, cfg, L);
+  double e = 0, n = 0;
+  for (int c = 0; c < C; ++c)
+    for (int i = 512; i < L - 512; ++i) {
+      e += (back(i, c) - s(i, c)) * (back(i, c) - s(i, c));
+      n += s(i, c) * s(i, c);
+    }
+  expect(std::sqrt(e / n) < 1e-10, "stft -> istft round trip (interior)");
+}
+
+// FMNM v2 round trip (test_io.cpp)
+void test_container() {
+  const BlockLayout layout({2, 1});
+  const InitBundle b = random_init(4, 6, layout, 2, 3, 11);
+  ModelDump d;
+  d.config.n_sources = 2;
+  d.config.k_bases = 3;
+  d.config.iterations = 7;
+  d.config.seed = 11;
+  d.config.sample_rate = 16000;
+  d.config.window_len = 1024;
+  d.config.hop_len = 256;
+  d.layout = layout;
+  d.models = {b.nmf};
+  d.lambda = b.lambda0;
+  d.w = b.w0;
+  const std::string path = "/tmp/fastmnmf_b200_cpp_api_test.fmnm";
+  save_model(path, d);
+  const ModelDump r = load_model(path);
+  bool same = r.layout.sizes == d.layout.sizes && r.shared && r.config.iterations == 7 && r.config.seed == 11 &&
+              r.models.size() == 1;
+  for (int n = 0; n < 2 && same; ++n)
+    same = std::memcmp(r.models[0].T[n].data(), b.nmf.T[n].data(), sizeof(double) * 4 * 3) == 0 &&
+           std::memcmp(r.models[0].V[n].data(), b.nmf.V[n].data(), sizeof(double) * 3 * 6) == 0;
+  for (int f = 0; f < 4 && same; ++f)
+    same = std::memcmp(r.lambda[f].data(), b.lambda0[f].data(), sizeof(double) * 2 * 3) == 0 &&
+           std::memcmp(r.w[0][f].data(), b.w0[0][f].data(), sizeof(cplx) * 4) == 0;
+  expect(same, "save_model -> load_model is bitwise");
+  std::remove(path.c_str());
+  expect(throws([&] { load_model("/tmp/does_not_exist_fastmnmf_b200.fmnm"); },
+                [](const std::exception& e) { return dynamic_cast<const std::runtime_error*>(&e) != nullptr; }),
+         "load_model of a missing file throws runtime_error");
+}
+
+// per-update API: every update non-increasing (test_fastmnmf.cpp:315-349)
+void test_per_update_monotone() {
+  const int F = 5, T = 30, M = 3, N = 2, K = 3;
+  std::vector<cplx> xf;
+  const ObsTensor x = mixture(F, T, M, N, K, 21, xf);
+  InitBundle init = random_init(F, T, BlockLayout::full(M), N, K, 6);
+  NmfModel model = init.nmf;
+  std::vector<MatrixXcd> w = init.w0[0];
+  std::vector<MatrixXd> lam = init.lambda0;
+  auto cost = [&] { return cost_full(x, model, SpatialModel{w, lam}); };
+  double prev = cost();
+  bool mono = true;
+  for (int it = 0; it < 3; ++it) {
+    std::vector<MatrixXd> eta = compute_eta(model, lam);
+    for (int m = 0; m < M; ++m) ip_update_w(x, eta, w, m);
+    double c = cost();
+    mono = mono && c <= prev + 1e-9 * std::abs(prev);
+    prev = c;
+    const auto pow_y = power_of(decorrelate(x, w));
+    mm_update_t(model, lam, pow_y, eta);
+    c = cost();
+    mono = mono && c <= prev + 1e-9 * std::abs(prev);
+    prev = c;
+    mm_update_v(model, lam, pow_y, eta);
+    c = cost();
+    mono = mono && c <= prev + 1e-9 * std::abs(prev);
+    prev = c;
+    mm_update_lambda(model, lam, pow_y, eta);
+    c = cost();
+    mono = mono && c <= prev + 1e-9 * std::abs(prev);
+    prev = c;
+  }
+  expect(mono, "per-update API: cost non-increasing after every update");
+  // the per-update sequence is the engine's iteration (engine.cpp:209-270)
+  const FullFit fit = fit_full(x, init, 3);
+  expect(rel(fit.report.cost_trace.back(), prev) < 1e-8, "per-update sequence reproduces fit_full");
+}
+
+// eval callbacks between chunks (engine.cpp:257-269)
+void test_eval_callback() {
+  const BlockLayout layout({2, 2});
+  std::vector<cplx> xf;
+  const ObsTensor x = mixture(4, 16, 4, 2, 2, 2, xf);
+  const InitBundle init = random_init(4, 16, layout, 2, 2, 2);
+  std::vector<int> seen;
+  std::vector<double> costs;
+  FitOptions opt;
+  opt.eval_every = 3;
+  opt.on_eval = [&](const FitSnapshot& s) {
+    seen.push_back(s.iteration);
+    costs.push_back(s.cost);
+  };
+  const DistFit a = fit_distributed(x, layout, init, 9, true, opt);
+  const DistFit b = fit_distributed(x, layout, init, 9, true);
+  expect(seen == std::vector<int>({3, 6, 9}), "on_eval at every eval_every-th iteration");
+  expect(costs.size() == 3 && costs[0] == a.report.cost_trace[3] && costs[2] == a.report.cost_trace[9],
+         "snapshot cost equals the trace");
+  expect(a.report.cost_trace == b.report.cost_trace, "callbacks do not change the trajectory");
+}
+
+}  // namespace
+
+int main() {
+  try {
+    test_random_init();
+    test_fit_matches_oracle({4});
+    test_fit_matches_oracle({2, 2});
+    test_fit_matches_oracle({3, 5});
+    test_independent_mode();
+    test_wiener();
+    test_errors();
+    test_stft();
+    test_container();
+    test_per_update_monotone();
+    test_eval_callback();
+  } catch (const std::exception& e) {
+    std::printf("FAIL: uncaught exception: %s\n", e.what());
+    return 2;
+  }
+  std::printf("%d checks, %d failed\n", g_checks, g_failed);
+  if (g_failed) return 1;
+  std::printf("ALL PASSED\n");
+  return 0;
+}
