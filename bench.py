@@ -391,7 +391,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="config1", choices=sorted(CONFIGS))
-    ap.add_argument("--e2e-iters", type=int, default=20)
+    ap.add_argument("--e2e-iters", type=int, default=0,
+                    help="EM iterations per e2e call (default: the config's own iteration count, e.g. 200 for config 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tiling", default="", help="FT,TB override: frame tile of the per-bin kernel and of k_pd")
     ap.add_argument("--batch", type=int, default=0, help="config4: number of mixtures (default 64)")
@@ -399,6 +400,8 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     c = CONFIGS[args.workload]
+    if args.e2e_iters <= 0:  # one e2e call = one full fit of the BASELINE config
+        args.e2e_iters = c["iters"]
     world, rank, local = dist_setup()
 
     if args.impl == "reference":

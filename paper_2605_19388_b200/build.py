@@ -41,14 +41,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     objdir = os.path.join(ROOT, "build")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
-    for src in SOURCES:
-        obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
+    objs = [os.path.join(objdir, os.path.splitext(src)[0] + ".o") for src in SOURCES]
+
+    def compile_one(src, obj):
         cmd = [_nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(ROOT, "include"),
                "-c", os.path.join(CSRC, src), "-o", obj]
         subprocess.run(cmd, check=True)
-        objs.append(obj)
+
+    # translation units are independent: compile them concurrently
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+        for fut in [ex.submit(compile_one, s, o) for s, o in zip(SOURCES, objs)]:
+            fut.result()
     tmp = LIB + ".tmp"
     cmd = [_nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-ldl"]
     subprocess.run(cmd, check=True)
