@@ -196,11 +196,12 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     double* is = zs + M * FTp;       // [M][FTp]
     const int NM = N * M, SL = sp.SL;
     for (int u = tid; u < NM * SL; u += FT) red[2 * u] = red[2 * u + 1] = 0.0;
-    // DMMA jobs per warp: (mic tile of 8, num|den) pairs over the CTA's warps
-    // (static shapes: enough for >= 2 warps; else the SIMT reduction)
-    constexpr int kLamJobs = SB ? ((MB_ * NB_ + 7) / 8 * 2 + 1) / 2 : 8;
+    // DMMA jobs per warp: column tiles of 8 of the stacked [z; 1/eta] rows
+    // (2M columns: num and den share tiles) over the CTA's warps (static
+    // shapes: enough for >= 2 warps; else the SIMT reduction)
+    constexpr int kLamJobs = SB ? ((2 * MB_ * NB_ + 7) / 8 + 1) / 2 : 8;
     const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3, nwarps = FT >> 5;
-    const int njobs = 2 * ((M + 7) / 8);
+    const int njobs = (2 * M + 7) / 8;
     const bool use_mma = N <= 8 && njobs <= kLamJobs * nwarps;
     // spare warps split each job's frames into slices (large frame tiles);
     // slice partials land in red[] slice rows, summed in a fixed order below
@@ -260,9 +261,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
         for (int jj = 0; jj < kLamJobs; ++jj) {
           const int jg = warp + jj * nwarps, job = jg % njobs, slc = jg / njobs;
           if (slc < nsl) {
-            const int j = job >> 1;
-            const double* brow = (job & 1) ? is : zs;
-            const int m = 8 * j + g;
+            const int col = 8 * job + g;  // row of the stacked [z; 1/eta] (is = zs + M rows)
             const int chunk = (((tn + 7) >> 3) + nsl - 1) / nsl * 8;
             const int s0 = slc * chunk, s1 = min(tn, s0 + chunk);
             // two independent accumulator chains (even / odd k-steps), added at
@@ -271,9 +270,9 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
             for (int t0 = s0; t0 < s1; t0 += 8) {
               const int t = t0 + q, u = t0 + 4 + q;
               const double av = (g < N && t < tn) ? hs[g * FTp + t] : 0.0;
-              const double bv = (m < M && t < tn) ? brow[m * FTp + t] : 0.0;
+              const double bv = (col < 2 * M && t < tn) ? zs[col * FTp + t] : 0.0;
               const double au = (g < N && u < tn) ? hs[g * FTp + u] : 0.0;
-              const double bu = (m < M && u < tn) ? brow[m * FTp + u] : 0.0;
+              const double bu = (col < 2 * M && u < tn) ? zs[col * FTp + u] : 0.0;
               dmma(c0, c1, av, bv);
               dmma(d0, d1, au, bu);
             }
@@ -301,16 +300,17 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     }
     if (use_mma) {
       __syncthreads();
-      // scatter the DMMA accumulators (C[n][m] at c0 = (g, 2q), c1 = (g, 2q+1)) into red[]
+      // scatter the DMMA accumulators (C[n][col] at c0 = (g, 2q), c1 = (g, 2q+1);
+      // col < M: numerator of mic col, else denominator of mic col - M) into red[]
 #pragma unroll
       for (int jj = 0; jj < kLamJobs; ++jj) {
         const int jg = warp + jj * nwarps, job = jg % njobs, slc = jg / njobs;
         if (slc < nsl && g < N) {
-          const int j = job >> 1, w = job & 1;
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
-            const int m = 8 * j + 2 * q + i;
-            if (m < M) red[2 * (slc * NM + g * M + m) + w] = i ? lj1[jj] : lj0[jj];
+            const int col = 8 * job + 2 * q + i;
+            const int w = col >= M, m = col - (w ? M : 0);
+            if (col < 2 * M) red[2 * (slc * NM + g * M + m) + w] = i ? lj1[jj] : lj0[jj];
           }
         }
       }
