@@ -57,7 +57,6 @@ __host__ __device__ inline EmPlan plan_em(const EmArgs& a, int FT) {
   p.lsm = o; o += al(N * M * sizeof(double));
   p.lst = o; o += al(M * (size_t)((N + 1) & ~1) * sizeof(double));  // Lambda^T [m][N rounded to even]
   p.wsm = o; o += al((size_t)a.wsz * sizeof(cd));
-  p.qsum = o; o += al((size_t)a.qper * sizeof(cd));
   p.ipscr = o; o += (size_t)a.nb * ipscr_bytes<MAXMB>();
   size_t r1 = (size_t)p.SL * NM * 2 * sizeof(double);
   size_t r2 = (size_t)p.SQ * p.nitems * MAXMB * sizeof(cd);
@@ -67,7 +66,15 @@ __host__ __device__ inline EmPlan plan_em(const EmArgs& a, int FT) {
   const size_t FTp = FT + 1;  // odd row stride: conflict-free item-parallel reads
   const size_t tA = (N + 2 * M) * FTp * sizeof(double);  // h, z, 1/eta
   const size_t tB = (3 * M) * FTp * sizeof(double);      // x (complex), 1/eta
-  p.tile = o; o += al(tA > tB ? tA : tB);
+  // Q_mu (written after pass B, read by the IP sweep) lives at the end of the
+  // frame tile, which pass B no longer needs by then; pass C's first-frame
+  // prefetch (M x (FT + 1) samples from the tile start) is issued early only
+  // when it does not overlap it
+  const size_t qb = al((size_t)a.qper * sizeof(cd));
+  size_t tb = al(tA > tB ? tA : tB);
+  if (tb < qb) tb = qb;
+  p.tile = o; o += tb;
+  p.qsum = p.tile + tb - qb;
   p.total = o;
   return p;
 }
@@ -479,9 +486,10 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   // sweep (thread-private slots of the free frame tile)
   const int FTpc = FT + 1;
   cd* xst = (cd*)tile;  // [M][FTpc]
+  const bool pf_early = (size_t)M * FTpc * sizeof(cd) <= sp.qsum - sp.tile;
+  __syncthreads();  // the Q tile reads of pass B are done (Qsum overwrites the tile end)
   if constexpr (SB) {
-    __syncthreads();  // the Q tile reads of pass B are done
-    if (tid < T)
+    if (pf_early && tid < T)
 #pragma unroll
       for (int m = 0; m < MS; ++m) cp_async16(xst + m * FTpc + tid, xf + (size_t)tid * M + m);
   }
@@ -603,6 +611,11 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     }
   }
   __syncthreads();
+  if constexpr (SB) {  // Q_mu is dead: pass C's first frame into the tile start
+    if (!pf_early && tid < T)
+#pragma unroll
+      for (int m = 0; m < MS; ++m) cp_async16(xst + m * FTpc + tid, xf + (size_t)tid * M + m);
+  }
   for (int e = tid; e < wsz; e += FT) a.W[(size_t)f * wsz + e] = Wsm[e];
   em_stamp(a, 4);
 

@@ -205,7 +205,9 @@ bool choose_tiling(dfm_ctx* c) {
   double best = 1e30;
   int bestFT = 0;
   // 512 threads per bin when the bins are few (frequency shards): one CTA per SM
-  std::vector<int> cands = {512, 256, 128, 64, 32};
+  // (non-power-of-two tiles fill the SM when shared memory, not registers,
+  // bounds the CTAs per SM: a 12-mic block runs 4 x 96-thread CTAs per SM)
+  std::vector<int> cands = {512, 384, 256, 192, 160, 128, 96, 64, 32};
   if (c->req_FT) cands = {c->req_FT};
   for (int FT : cands) {
     const size_t sm = em_smem(a, FT, c->kmaxmb);

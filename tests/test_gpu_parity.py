@@ -184,9 +184,12 @@ def test_engine_trajectory_matches_oracle(dfm, oracle, F, T, sizes, N, K, iters)
         assert _rel(a, b) < 1e-7
 
 
-@pytest.mark.parametrize("FT,TB", [(32, 32), (64, 64), (128, 128), (256, 32), (96, 64), (512, 128)])
-def test_engine_tilings_agree(dfm, oracle, FT, TB):
-    F, T, sizes, N, K, iters = 11, 70, [4, 4, 4], 5, 8, 10
+@pytest.mark.parametrize("FT,TB,sizes", [(32, 32, [4, 4, 4]), (64, 64, [4, 4, 4]), (128, 128, [4, 4, 4]),
+                                         (256, 32, [4, 4, 4]), (96, 64, [4, 4, 4]), (512, 128, [4, 4, 4]),
+                                         (160, 128, [4, 4, 4]), (96, 128, [12]), (160, 64, [12]),
+                                         (192, 128, [12])])
+def test_engine_tilings_agree(dfm, oracle, FT, TB, sizes):
+    F, T, N, K, iters = 11, 70, 5, 8, 10
     layout = dfm.BlockLayout(sizes)
     x = dfm.generate_mixture(1, F, T, layout.total, N, K, 9)
     init = dfm.random_init(F, T, layout, N, K, 2)
