@@ -1232,12 +1232,13 @@ __global__ void __launch_bounds__(kWienFT, 4) k_wiener_ctx(const EmArgs a, const
   const int f = blockIdx.y, t0 = blockIdx.x * kWienFT, tid = threadIdx.x;
   const int tn = min(kWienFT, T - t0);
   for (int e = tid; e < wsz; e += kWienFT) Ws[e] = a.W[(size_t)f * wsz + e];
-  if (!SB)
+  constexpr bool GREG = SB && MB_ <= 4;  // (W^H)^-1 per CTA in registers, else precomputed
+  if (!GREG)
     for (int e = tid; e < wsz; e += kWienFT) Gs[e] = G[(size_t)f * wsz + e];
   for (int e = tid; e < N * M; e += kWienFT) Ls[e] = a.lam[(size_t)f * N * M + e];
   __syncthreads();
-  if constexpr (SB) {  // (W_b^H)^-1 of this bin's blocks, one thread each (wiener.cpp:25)
-    if (tid < NB_) wh_inverse_regs<MB_>(Ws + tid * MB_ * MB_, Gs + tid * MB_ * MB_);
+  if constexpr (GREG) {  // (W_b^H)^-1 of this bin's blocks, one thread each (wiener.cpp:25)
+    if (tid < NB_) wh_inverse_regs<MB_ <= 4 ? MB_ : 1>(Ws + tid * MB_ * MB_, Gs + tid * MB_ * MB_);
     __syncthreads();
   }
   const int t = t0 + tid;

@@ -398,8 +398,10 @@ void run_step(dfm_ctx* c, bool split) {
 // [N][F][T][M]: (W^H)^-1 per (bin, block), H = T V, then k_wiener_ctx.
 void launch_wiener_ctx(dfm_ctx* c, cd* img) {
   if (c->Ginv.n < (size_t)c->F * c->L.wsz) c->Ginv.alloc((size_t)c->F * c->L.wsz);
-  // the static-shape kernels invert W^H per CTA in registers
-  if (!c->static_shapes) launch_wh_inverse(c->F, c->L, c->W.p, c->L.wsz, c->Ginv.p, c->stream);
+  // the static-shape kernels with blocks of <= 4 mics invert W^H per CTA in
+  // registers; larger blocks and the generic kernels read it precomputed
+  const bool ginv = !c->static_shapes || c->kmaxmb > 4;
+  if (ginv) launch_wh_inverse(c->F, c->L, c->W.p, c->L.wsz, c->Ginv.p, c->stream);
   launch_spec(c);
   const size_t smem = (size_t)(2 * c->L.wsz + kWienFT * (c->M + 1)) * sizeof(cd) + (size_t)c->N * c->M * 8;
   DFM_CK(cudaFuncSetAttribute(c->kwien, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -407,7 +409,7 @@ void launch_wiener_ctx(dfm_ctx* c, cd* img) {
   const dim3 grid((c->T + kWienFT - 1) / kWienFT, c->F);
   c->kwien<<<grid, kWienFT, smem, c->stream>>>(a, c->Ginv.p, img);
   DFM_CK_LAUNCH();
-  c->launches += c->static_shapes ? 2 : 3;
+  c->launches += ginv ? 3 : 2;
 }
 
 }  // namespace

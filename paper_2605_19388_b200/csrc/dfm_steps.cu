@@ -394,8 +394,38 @@ void launch_wiener(const Layout& L, int F, int T, int N, int K, const cd* x, con
   if (!Gbuf) DFM_CK(cudaStreamSynchronize(s));  // Gown is freed on return
 }
 
+// (W_b^H)^-1 for blocks above 4 mics: one warp per (bin, block), W^-1 by the
+// lane-parallel Gauss-Jordan of the IP path (ip_winv_warp), then
+// G = (W^-1)^H.  The serial per-thread LU above keeps a 16 x 16 complex
+// matrix in local memory, which at 12 mics dominated the whole separation.
+constexpr int kWhWarps = 2;
+__global__ void __launch_bounds__(32 * kWhWarps) k_wh_inverse_warp(int F, Layout L, const cd* __restrict__ W,
+                                                                  long long wstride, cd* __restrict__ G) {
+  __shared__ IpScratch<DFM_MAX_MB> scr[kWhWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long idx = (long long)blockIdx.x * kWhWarps + warp;
+  if (idx >= (long long)F * L.nb) return;
+  const int b = (int)(idx % L.nb), f = (int)(idx / L.nb);
+  const int mb = L.mb[b];
+  IpScratch<DFM_MAX_MB>& sc = scr[warp];
+  ip_winv_warp<DFM_MAX_MB>(mb, W + (size_t)f * wstride + L.woff[b], sc);
+  __syncwarp();
+  cd* g = G + (size_t)f * wstride + L.woff[b];
+  for (int e = lane; e < mb * mb; e += 32) {
+    const int c = e / mb, r = e - c * mb;  // G(r, c) = conj(W^-1(c, r))
+    g[e] = conjg(sc.S[r * mb + c]);
+  }
+}
+
 void launch_wh_inverse(int F, const Layout& L, const cd* W, long long wstride, cd* G, cudaStream_t s) {
-  k_wh_inverse<<<nblk((long long)F * L.nb, 128), 128, 0, s>>>(F, L, W, wstride, G);
+  int maxmb = 0;
+  for (int b = 0; b < L.nb; ++b) maxmb = maxmb > L.mb[b] ? maxmb : L.mb[b];
+  if (maxmb > 4) {
+    k_wh_inverse_warp<<<(unsigned)(((long long)F * L.nb + kWhWarps - 1) / kWhWarps), 32 * kWhWarps, 0, s>>>(
+        F, L, W, wstride, G);
+  } else {
+    k_wh_inverse<<<nblk((long long)F * L.nb, 128), 128, 0, s>>>(F, L, W, wstride, G);
+  }
   DFM_CK_LAUNCH();
 }
 

@@ -267,8 +267,12 @@ def test_engine_underdetermined_and_independent_mode(dfm, oracle):
     assert final == pytest.approx(fit_ind.report.cost_trace[-1], rel=1e-10)
 
 
-def test_engine_wiener_matches_oracle_after_fit(dfm, oracle):
-    F, T, sizes, N, K = 8, 45, [2, 2], 3, 4
+@pytest.mark.parametrize("sizes,N,K", [([2, 2], 3, 4), ([4, 4, 4], 5, 4), ([12], 5, 4), ([8, 3], 4, 4)])
+def test_engine_wiener_matches_oracle_after_fit(dfm, oracle, sizes, N, K):
+    """Engine.wiener on the static kernels (in-CTA (W^H)^-1 for blocks <= 4
+    mics; the warp Gauss-Jordan inverse for the 12-mic block) and the generic
+    kernel (8 + 3 mics)."""
+    F, T = 8, 45
     layout = dfm.BlockLayout(sizes)
     x = dfm.generate_mixture(0, F, T, layout.total, N, K, 1)
     init = dfm.random_init(F, T, layout, N, K, 2)
@@ -280,8 +284,16 @@ def test_engine_wiener_matches_oracle_after_fit(dfm, oracle):
         nmf, wb, lam = eng.get_model()
     ref = oracle.run_engine(x, sizes, _init_dict(init), 30)
     ref_img = oracle.wiener_block(x, sizes, ref)
-    assert _rel(img, ref_img) < 1e-6
+    # after 30 iterations the two fits differ by their rounding history
+    # (amplified for a 12-mic block on 45 frames); the filter itself is
+    # checked on the oracle's fitted model, where it must agree to 1e-10
+    assert _rel(img, ref_img) < (1e-4 if max(sizes) > 4 else 1e-6)
     assert np.linalg.norm(img.sum(0) - x) <= 1e-9 * np.linalg.norm(x)
+    with dfm.Engine(F, T, layout, N, K) as eng:
+        eng.set_obs(x)
+        eng.set_model(dfm.NmfModel(ref["T"], ref["V"]), [np.asarray(w) for w in ref["w"]], ref["lam"])
+        img2 = eng.wiener()
+    assert _rel(img2, ref_img) < 1e-10
 
 
 def test_eval_callback_chunks_match_single_run(dfm, oracle):
