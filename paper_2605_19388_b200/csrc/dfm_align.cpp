@@ -27,53 +27,100 @@ namespace {
 // once (mean, then u - mean and its sum of squares, in the reference's
 // sequential order); the N^2 correlations then reuse the centred columns, so
 // each equals the reference's pearson(u, v) with a third of the work.
+// Column c of length L is read through col(c, j) in the reference's order
+// j = 0 .. L-1; columns (and the N^2 dot products) are independent, so they
+// run on up to `nth` host threads, each in its own sequential order.
+template <class Src>
+void parallel_for(int n, int nth, const Src& body) {
+  if (nth <= 1 || n <= 1) {
+    for (int i = 0; i < n; ++i) body(i);
+    return;
+  }
+  std::vector<std::thread> pool;
+  const int w = std::min(nth, n);
+  for (int k = 0; k < w; ++k)
+    pool.emplace_back([&, k] {
+      for (int i = k; i < n; i += w) body(i);
+    });
+  for (auto& th : pool) th.join();
+}
+
 struct Centred {
   std::vector<double> d, ss;
-  Centred(const double* m, size_t L, int N) : d((size_t)N * L), ss(N) {
-    for (int c = 0; c < N; ++c) {
-      const double* u = m + c * L;
+  size_t L;
+  // src(c, out): writes column c (L values, reference order) into out
+  template <class Src>
+  Centred(const Src& src, size_t L_, int N, int nth) : d((size_t)N * L_), ss(N), L(L_) {
+    parallel_for(N, nth, [&](int c) {
+      double* u = &d[c * L];
+      src(c, u);
       double mu = 0.0;
       for (size_t j = 0; j < L; ++j) mu += u[j];
       mu /= (double)L;
       double s2 = 0.0;
       for (size_t j = 0; j < L; ++j) {
         const double a = u[j] - mu;
-        d[c * L + j] = a;
+        u[j] = a;
         s2 += a * a;
       }
       ss[c] = s2;
-    }
+    });
   }
 };
 
-// init.cpp:24-42: cand / ref are N columns of length L (column c at c * L);
-// lexicographic permutations, the first strict maximum of the summed
-// correlation of cand column perm[c] with ref column c wins
-std::vector<int> best_perm(const double* cand, const double* ref, size_t L, int N) {
+// corr[a][c] = pearson(cand_a, ref_c)
+std::vector<double> correlations(const Centred& cu, const Centred& cv, int N, int nth) {
   std::vector<double> corr((size_t)N * N);
-  const Centred cu(cand, L, N), cv(ref, L, N);
-  for (int a = 0; a < N; ++a)
-    for (int c = 0; c < N; ++c) {
-      const double* du = &cu.d[a * L];
-      const double* dv = &cv.d[c * L];
-      double d = 0.0;
-      for (size_t j = 0; j < L; ++j) d += du[j] * dv[j];
-      const double den = std::sqrt(cu.ss[a]) * std::sqrt(cv.ss[c]);
-      corr[(size_t)a * N + c] = den <= 0 ? 0.0 : d / den;  // = pearson(cand_a, ref_c)
-    }
-  std::vector<int> perm(N), best(N);
+  const size_t L = cu.L;
+  parallel_for(N * N, nth, [&](int ac) {
+    const int a = ac / N, c = ac % N;
+    const double* du = &cu.d[a * L];
+    const double* dv = &cv.d[c * L];
+    double d = 0.0;
+    for (size_t j = 0; j < L; ++j) d += du[j] * dv[j];
+    const double den = std::sqrt(cu.ss[a]) * std::sqrt(cv.ss[c]);
+    corr[ac] = den <= 0 ? 0.0 : d / den;
+  });
+  return corr;
+}
+
+// init.cpp:24-42: permutations in lexicographic order (std::next_permutation
+// from the identity), the first strict maximum of sum_c corr[perm[c]][c]
+// wins.  The successor step leaves the prefix before its pivot k unchanged,
+// so the running prefix sums pre[0..k] are kept and only pre[k+1..N] are
+// recomputed: every total is the reference's left-to-right sum (same
+// rounding) at about 2-3 additions per permutation instead of N.
+std::vector<int> perm_search(const std::vector<double>& corr, int N) {
+  std::vector<int> perm(N);
   std::iota(perm.begin(), perm.end(), 0);
-  best = perm;
+  std::vector<int> best = perm;
+  std::vector<double> pre(N + 1, 0.0);
+  for (int c = 0; c < N; ++c) pre[c + 1] = pre[c] + corr[(size_t)perm[c] * N + c];
   double top = -std::numeric_limits<double>::infinity();
-  do {
-    double s = 0.0;
-    for (int c = 0; c < N; ++c) s += corr[(size_t)perm[c] * N + c];
-    if (s > top) {
-      top = s;
+  if (pre[N] > top) top = pre[N];
+  for (;;) {
+    int k = N - 2;
+    while (k >= 0 && perm[k] >= perm[k + 1]) --k;
+    if (k < 0) break;
+    int l = N - 1;
+    while (perm[l] <= perm[k]) --l;
+    std::swap(perm[k], perm[l]);
+    std::reverse(perm.begin() + k + 1, perm.end());
+    for (int c = k; c < N; ++c) pre[c + 1] = pre[c] + corr[(size_t)perm[c] * N + c];
+    if (pre[N] > top) {
+      top = pre[N];
       best = perm;
     }
-  } while (std::next_permutation(perm.begin(), perm.end()));
+  }
   return best;
+}
+
+std::vector<int> best_perm(const double* cand, const double* ref, size_t L, int N, int nth = 1) {
+  auto from = [&](const double* m) {
+    return [m, L](int c, double* out) { std::memcpy(out, m + c * L, sizeof(double) * L); };
+  };
+  const Centred cu(from(cand), L, N, nth), cv(from(ref), L, N, nth);
+  return perm_search(correlations(cu, cv, N, nth), N);
 }
 
 void permute_cols(double* m, size_t L, const std::vector<int>& perm) {
@@ -148,19 +195,19 @@ int dfm_align_subarray_permutations(const double* masks, int L, int F, int T, in
     return DFM_ERR_ARG;
   }
   const size_t FT = (size_t)F * T;
-  // flatten source n over every (bin, frame) (init.cpp:233-239)
-  auto flatten = [&](const double* m, std::vector<double>& out) {
-    out.resize((size_t)N * FT);
-    for (int i = 0; i < F; ++i)
-      for (int n = 0; n < N; ++n)
-        std::memcpy(&out[(size_t)n * FT + (size_t)i * T], m + ((size_t)i * N + n) * T, sizeof(double) * T);
+  // source n flattened over every (bin, frame) (init.cpp:233-239), read in
+  // place: column n is bin 0's frames, then bin 1's, ...
+  auto column = [&](const double* m) {
+    return [m, F, T, N](int n, double* out) {
+      for (int i = 0; i < F; ++i) std::memcpy(out + (size_t)i * T, m + ((size_t)i * N + n) * T, sizeof(double) * T);
+    };
   };
-  std::vector<double> ref, cand;
-  flatten(masks, ref);
+  const int nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  const Centred cv(column(masks), FT, N, nth);  // the first subarray, once
   for (int n = 0; n < N; ++n) perms[n] = n;
   for (int l = 1; l < L; ++l) {
-    flatten(masks + (size_t)l * F * N * T, cand);
-    const std::vector<int> p = best_perm(cand.data(), ref.data(), FT, N);
+    const Centred cu(column(masks + (size_t)l * F * N * T), FT, N, nth);
+    const std::vector<int> p = perm_search(correlations(cu, cv, N, nth), N);
     std::copy(p.begin(), p.end(), perms + (size_t)l * N);
   }
   return DFM_OK;
