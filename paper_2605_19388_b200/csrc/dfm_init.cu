@@ -227,15 +227,27 @@ __global__ void k_kmeans_bin(const cd* __restrict__ x, int T, int Mt, int off, i
 
 // one CTA per (bin f, source n): R_nf, then h0 (init.cpp:268-304).
 // masks [nb][F][N][T]; R [N][F] x (M x M) col-major; h0 [F][N][T]
+// The masked samples c_t = w_t x_t of a tile of kScmTile frames are staged
+// in shared memory once (one global read of x and of the mask per (frame,
+// channel)); every thread then accumulates its covariance entries from the
+// tile in registers, each entry summing the frames in the reference's
+// ascending order (so R is unchanged bitwise).  The per-frame solves of h0
+// read c from the same staged tile and keep z in registers (compile-time
+// sizes up to MAXM).
+constexpr int kScmThreads = 128, kScmTile = 64;
 template <int MAXM>
-__global__ void k_scm_spec(const cd* __restrict__ x, int F, int T, int M, int N, int nb, const int* __restrict__ bsz,
-                           const double* __restrict__ masks, cd* __restrict__ R, double* __restrict__ h0) {
+__global__ void __launch_bounds__(kScmThreads) k_scm_spec(const cd* __restrict__ x, int F, int T, int M, int N,
+                                                          int nb, const int* __restrict__ bsz,
+                                                          const double* __restrict__ masks, cd* __restrict__ R,
+                                                          double* __restrict__ h0) {
   extern __shared__ __align__(16) unsigned char sm[];
-  cd* Rs = (cd*)sm;       // M x M
-  cd* Ls = Rs + M * M;    // M x M (lower Cholesky factor of R + ridge)
+  cd* Rs = (cd*)sm;             // M x M
+  cd* Ls = Rs + M * M;          // M x M (lower Cholesky factor of R + ridge)
+  cd* cs = Ls + M * M;          // [kScmTile][M + 1] masked samples
+  const int Mp = M + 1;
   __shared__ int blk[kMaxCh];
   __shared__ int ok;
-  const int f = blockIdx.x, n = blockIdx.y, tid = threadIdx.x, nt = blockDim.x;
+  const int f = blockIdx.x, n = blockIdx.y, tid = threadIdx.x;
   if (tid == 0) {
     int b = 0, o = 0;
     for (int m = 0; m < M; ++m) {
@@ -244,20 +256,47 @@ __global__ void k_scm_spec(const cd* __restrict__ x, int F, int T, int M, int N,
     }
   }
   __syncthreads();
-  auto cval = [&](int t, int m) -> cd {
-    const double w = masks[(((size_t)blk[m] * F + f) * N + n) * T + t];
-    const cd v = x[((size_t)f * T + t) * M + m];
-    return cd{v.re * w, v.im * w};
+  auto stage = [&](int t0, int tn) {
+    for (int e = tid; e < tn * M; e += kScmThreads) {
+      const int tt = e / M, m = e - tt * M, t = t0 + tt;
+      const double w = masks[(((size_t)blk[m] * F + f) * N + n) * T + t];
+      const cd v = x[((size_t)f * T + t) * M + m];
+      cs[tt * Mp + m] = cd{v.re * w, v.im * w};
+    }
   };
-  for (int e = tid; e < M * M; e += nt) {
-    const int col = e / M, row = e - col * M;
-    cd s{0.0, 0.0};
-    for (int t = 0; t < T; ++t) s = s + cval(t, row) * conjg(cval(t, col));
-    Rs[e] = cd{s.re / (double)T, s.im / (double)T};
+  constexpr int EPT = (MAXM * MAXM + kScmThreads - 1) / kScmThreads;  // entries per thread
+  cd acc[EPT];
+#pragma unroll
+  for (int j = 0; j < EPT; ++j) acc[j] = cd{0.0, 0.0};
+  const int MM = M * M;
+  for (int t0 = 0; t0 < T; t0 += kScmTile) {
+    const int tn = min(kScmTile, T - t0);
+    __syncthreads();
+    stage(t0, tn);
+    __syncthreads();
+    // frames outer, the thread's entries inner: EPT independent chains, each
+    // entry still summing its frames in ascending order
+    int ro[EPT], co[EPT];
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) {
+      const int e = min(tid + j * kScmThreads, MM - 1);
+      co[j] = e / M;
+      ro[j] = e - co[j] * M;
+    }
+    for (int tt = 0; tt < tn; ++tt) {
+      const cd* ct = cs + tt * Mp;
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) acc[j] = acc[j] + ct[ro[j]] * conjg(ct[co[j]]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < EPT; ++j) {
+    const int e = tid + j * kScmThreads;
+    if (e < MM) Rs[e] = cd{acc[j].re / (double)T, acc[j].im / (double)T};
   }
   __syncthreads();
   cd* Rg = R + ((size_t)n * F + f) * M * M;
-  for (int e = tid; e < M * M; e += nt) Rg[e] = Rs[e];
+  for (int e = tid; e < M * M; e += kScmThreads) Rg[e] = Rs[e];
   double* hf = h0 + ((size_t)f * N + n) * T;
   if (tid == 0) {  // ridge LLT (init.cpp:288-293)
     double tr = 0.0;
@@ -284,27 +323,39 @@ __global__ void k_scm_spec(const cd* __restrict__ x, int F, int T, int M, int N,
     }
   }
   __syncthreads();
-  for (int t = tid; t < T; t += nt) {
-    if (!ok) {
-      hf[t] = 0.0;
-      continue;
+  if (!ok) {
+    for (int t = tid; t < T; t += kScmThreads) hf[t] = 0.0;
+    return;
+  }
+  // h0 = Re(c^H (L L^H)^-1 c) / M = ||L^-1 c||^2 / M per frame: one forward
+  // solve, its inner products split over two accumulator chains
+  for (int t0 = 0; t0 < T; t0 += kScmTile) {
+    const int tn = min(kScmTile, T - t0);
+    __syncthreads();
+    stage(t0, tn);
+    __syncthreads();
+    for (int tt = tid; tt < tn; tt += kScmThreads) {
+      const cd* c = cs + tt * Mp;
+      cd y[MAXM];
+      double sum = 0.0;
+#pragma unroll
+      for (int i = 0; i < MAXM; ++i)
+        if (i < M) {
+          cd s0 = c[i], s1{0.0, 0.0};
+#pragma unroll
+          for (int k = 0; k + 1 < i; k += 2) {
+            s0 = s0 - Ls[k * M + i] * y[k];
+            s1 = s1 + Ls[(k + 1) * M + i] * y[k + 1];
+          }
+          if (i & 1) s0 = s0 - Ls[(i - 1) * M + i] * y[i - 1];
+          const cd v = s0 - s1;
+          const double il = 1.0 / Ls[i * M + i].re;
+          y[i] = cd{v.re * il, v.im * il};
+          sum += norm2(y[i]);
+        }
+      const double h = sum / M;
+      hf[t0 + tt] = h > 0.0 ? h : 0.0;
     }
-    cd c[MAXM], z[MAXM];
-    for (int m = 0; m < M; ++m) z[m] = c[m] = cval(t, m);
-    for (int i = 0; i < M; ++i) {
-      cd s = z[i];
-      for (int k = 0; k < i; ++k) s = s - Ls[k * M + i] * z[k];
-      z[i] = cd{s.re / Ls[i * M + i].re, s.im / Ls[i * M + i].re};
-    }
-    for (int i = M - 1; i >= 0; --i) {
-      cd s = z[i];
-      for (int k = i + 1; k < M; ++k) s = s - conjg(Ls[i * M + k]) * z[k];
-      z[i] = cd{s.re / Ls[i * M + i].re, s.im / Ls[i * M + i].re};
-    }
-    double s = 0.0;
-    for (int m = 0; m < M; ++m) s += (conjg(c[m]) * z[m]).re;
-    const double h = s / M;
-    hf[t] = h > 0.0 ? h : 0.0;
   }
 }
 
@@ -592,14 +643,19 @@ void kmeans_masks(const cd* x, int F, int T, int Mt, int off, int M, int N, uint
 
 void launch_scm_spec(const cd* x, int F, int T, int M, int N, int nb, const int* bsz, const double* masks, cd* R,
                      double* h0, cudaStream_t s) {
-  const size_t sm = 2 * (size_t)M * M * sizeof(cd);
-  if (M <= 16) {
-    DFM_CK(cudaFuncSetAttribute(k_scm_spec<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    k_scm_spec<16><<<dim3(F, N), 128, sm, s>>>(x, F, T, M, N, nb, bsz, masks, R, h0);
-  } else {
-    DFM_CK(cudaFuncSetAttribute(k_scm_spec<kMaxCh>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    k_scm_spec<kMaxCh><<<dim3(F, N), 128, sm, s>>>(x, F, T, M, N, nb, bsz, masks, R, h0);
-  }
+  const size_t sm = (2 * (size_t)M * M + (size_t)kScmTile * (M + 1)) * sizeof(cd);
+  auto go = [&](auto kern) {
+    DFM_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    kern<<<dim3(F, N), kScmThreads, sm, s>>>(x, F, T, M, N, nb, bsz, masks, R, h0);
+  };
+  if (M <= 8)
+    go(k_scm_spec<8>);
+  else if (M <= 16)
+    go(k_scm_spec<16>);
+  else if (M <= 32)
+    go(k_scm_spec<32>);
+  else
+    go(k_scm_spec<kMaxCh>);
   DFM_CK_LAUNCH();
 }
 
