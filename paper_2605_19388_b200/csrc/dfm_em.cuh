@@ -193,6 +193,27 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
 #pragma unroll
     for (int m = 0; m < MS; ++m) pv[m] = Pf[(size_t)m * T + t];
   };
+  // raw[m] = sum_n h[n] Lambda(n, m) for every mic of the frame, sources
+  // outer: MS independent FMA chains instead of MS dependent ones in turn
+  // (each raw[m] still sums n = 0..N-1 in order, so the values are the
+  // m-outer form's bitwise).  Lambda rows [n][M] are read as 16-byte pairs.
+  constexpr bool IL = SB && MS <= 16 && (MS % 2 == 0);
+  constexpr int MI = IL ? MS : 1;
+  auto eta_raw = [&](const double* h, double* raw) {
+#pragma unroll
+    for (int m = 0; m < MI; ++m) raw[m] = 0.0;
+#pragma unroll
+    for (int n = 0; n < kMaxN; ++n)
+      if (n < N) {
+        const double* lr = Lsm + n * MI;
+#pragma unroll
+        for (int m = 0; m < MI; m += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(lr + m);
+          raw[m] = fma(h[n], v.x, raw[m]);
+          raw[m + 1] = fma(h[n], v.y, raw[m + 1]);
+        }
+      }
+  };
 
   // ================================================================ pass A
   // finish iteration i-1: Lambda update with eta = max(h Lambda_old, floor)
@@ -243,6 +264,16 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
 #pragma unroll
         for (int n = 0; n < kMaxN; ++n)
           if (n < N) hs[n * FTp + tid] = h[n];
+        if constexpr (IL) {
+          double raw[MI];
+          eta_raw(h, raw);
+#pragma unroll
+          for (int m = 0; m < MI; ++m) {
+            const double ie = rcp_pos(fmax(raw[m], floor_));
+            is[m * FTp + tid] = ie;
+            zs[m * FTp + tid] = pv[m] * ie * ie;
+          }
+        } else
 #pragma unroll
         for (int m = 0; m < (SB ? MS : M); ++m) {
           double lv[kMaxN];
@@ -412,6 +443,17 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
       if constexpr (SB && !PF)
         if (tid < tn) load_power(t, pv);
       if (tid < tn) {
+        if constexpr (IL) {
+          double raw[MI];
+          eta_raw(h, raw);
+#pragma unroll
+          for (int m = 0; m < MI; ++m) {
+            const double ie = rcp_pos(fmax(raw[m], floor_));
+            cost += pv[m] * ie;
+            lacc.mul(fmax(raw[m], 1e-300));
+            if (a.start) is[m * FTp + tid] = ie;
+          }
+        } else
 #pragma unroll
         for (int m = 0; m < (SB ? MS : M); ++m) {
           double lv[kMaxN];
@@ -630,6 +672,8 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     double A[kMaxN], B[kMaxN];
 #pragma unroll
     for (int n = 0; n < kMaxN; ++n) A[n] = B[n] = 0.0;
+    double rawc[MI];
+    if constexpr (IL) eta_raw(h, rawc);
 #pragma unroll
     for (int b = 0; b < nb; ++b) {
       double P[MAXMB];
@@ -656,9 +700,13 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
           double lv[kMaxN];
           load_lam(m, lv);
           double raw = 0.0;
+          if constexpr (IL) {
+            raw = rawc[IL ? m : 0];
+          } else {
 #pragma unroll
-          for (int n = 0; n < kMaxN; ++n)
-            if (n < N) raw += h[n] * lv[n];
+            for (int n = 0; n < kMaxN; ++n)
+              if (n < N) raw += h[n] * lv[n];
+          }
           const double ie = rcp_pos(fmax(raw, floor_));
           const double z = P[mu] * ie * ie;
           Pf[(size_t)m * T + t] = P[mu];
