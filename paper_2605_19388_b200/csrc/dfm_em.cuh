@@ -1074,6 +1074,7 @@ template <int MB_, int NB_, int NS_, int MAXMB>
 __global__ void __launch_bounds__(128, 6) k_pdw(const EmArgs a) {
   constexpr bool SB = MB_ > 0 && NB_ > 0;
   __shared__ __align__(16) double Ls[kMaxN * 64];  // Lambda^T [m][NP] (one 16-byte load per source pair)
+  __shared__ __align__(16) double Lr[kMaxN * 16];  // Lambda [n][M] rows (static shapes with M <= 16)
   const int M = SB ? MB_ * NB_ : a.M;
   const int N = NS_ > 0 ? NS_ : a.N;
   const int T = a.T;
@@ -1086,6 +1087,10 @@ __global__ void __launch_bounds__(128, 6) k_pdw(const EmArgs a) {
       const int m = e / NP, n = e - m * NP;
       Ls[e] = n < N ? Lg[n * M + m] : 0.0;
     }
+  constexpr int MS = SB ? MB_ * NB_ : 1;
+  constexpr bool IL = SB && MS <= 16 && (MS % 2 == 0);  // sources-outer eta (as k_em_bin)
+  if constexpr (IL)
+    for (int e = threadIdx.x; e < N * MS; e += blockDim.x) Lr[e] = Lg[e];
   __syncthreads();
   if (t >= T) return;
   auto load_lam = [&](int m, double* lv) {
@@ -1115,14 +1120,32 @@ __global__ void __launch_bounds__(128, 6) k_pdw(const EmArgs a) {
   double A[kMaxN], B[kMaxN];
 #pragma unroll
   for (int n = 0; n < kMaxN; ++n) A[n] = B[n] = 0.0;
+  double rawv[IL ? MS : 1];
+  if constexpr (IL) {
+#pragma unroll
+    for (int m = 0; m < MS; ++m) rawv[m] = 0.0;
+#pragma unroll
+    for (int n = 0; n < kMaxN; ++n)
+      if (n < N)
+#pragma unroll
+        for (int m = 0; m < MS; m += 2) {
+          const double2 v = *reinterpret_cast<const double2*>(Lr + n * MS + m);
+          rawv[m] = fma(h[n], v.x, rawv[m]);
+          rawv[m + 1] = fma(h[n], v.y, rawv[m + 1]);
+        }
+  }
 #pragma unroll
   for (int m = 0; m < (SB ? MB_ * NB_ : M); ++m) {
     double lv[kMaxN];
     load_lam(m, lv);
     double raw = 0.0;
+    if constexpr (IL) {
+      raw = rawv[IL ? m : 0];
+    } else {
 #pragma unroll
-    for (int n = 0; n < kMaxN; ++n)
-      if (n < N) raw += h[n] * lv[n];
+      for (int n = 0; n < kMaxN; ++n)
+        if (n < N) raw += h[n] * lv[n];
+    }
     const double ie = rcp_pos(fmax(raw, a.floor_));
     const double p = SB ? pv[SB ? m : 0] : __ldg(Pt + (size_t)m * T);
     const double z = p * ie * ie;
