@@ -29,3 +29,13 @@ st.stft_inverse(X, st.StftConfig(8000.0, 256, 64), 1200)
 st.stft_forward(sig[:300], st.StftConfig(8000.0, 12, 3))
 b = di.init_distributed(x, layout, di.InitConfig(N, K, 20), 7)
 print("sanitize run ok", fit.report.cost_trace[-1], f2.report.cost_trace[-1], b.lambda0.min())
+# one 12-mic block (static <12, 1, 5, 12>: Q_mu in the frame tile, pass C's
+# late prefetch, the warp (W^H)^-1 for the Wiener filter)
+l3 = dfm.BlockLayout([12])
+x3 = dfm.generate_mixture(1, 7, 100, 12, 5, 16, 8)
+i3 = dfm.random_init(7, 100, l3, 5, 16, 9)
+with dfm.Engine(7, 100, l3, 5, 16) as e3:
+    e3.set_obs(x3)
+    e3.set_model(i3.nmf, i3.w0, i3.lambda0)
+    e3.fit(3)
+    e3.wiener()
