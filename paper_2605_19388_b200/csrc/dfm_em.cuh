@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
           cd qacc[MAXMB];
 #pragma unroll
           for (int mu = 0; mu < MAXMB; ++mu) qacc[mu] = cd{0.0, 0.0};
-#pragma unroll 2
+#pragma unroll 4
           for (int tt = qs; tt < tn; tt += SQ) {
             const cd pr = xr[tt] * conjg(xc[tt]);
 #pragma unroll
