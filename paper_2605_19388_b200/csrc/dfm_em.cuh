@@ -116,6 +116,9 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   const int ntiles = (T + FT - 1) / FT;
   const cd* xf = a.x + (size_t)f * T * M;
   double* Pf = a.P + (size_t)f * M * T;
+  // X is read by pass B and again by pass C after the IP sweep: pass B's
+  // copies ask L2 to keep the lines, pass C's (their last use) to drop them
+  const unsigned long long pol_keep = l2_evict_last(), pol_last = l2_evict_first();
   const double* Hf = a.H + (size_t)f * N * T;
   em_stamp(a, 0);
 
@@ -189,9 +192,11 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   // P of the next tile is prefetched into registers when the frame is small
   constexpr bool PF = SB && MS <= 16;
   constexpr int MP = PF ? MS : 1;
-  auto load_power = [&](int t, double* pv) {
+  // P is read by pass A (keep it in L2) and by pass B (its last use: pass C
+  // writes the new P)
+  auto load_power = [&](int t, double* pv, unsigned long long pol) {
 #pragma unroll
-    for (int m = 0; m < MS; ++m) pv[m] = Pf[(size_t)m * T + t];
+    for (int m = 0; m < MS; ++m) pv[m] = ld_hint(Pf + (size_t)m * T + t, pol);
   };
   // raw[m] = sum_n h[n] Lambda(n, m) for every mic of the frame, sources
   // outer: MS independent FMA chains instead of MS dependent ones in turn
@@ -242,7 +247,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     double hn[kMaxN], pn[MP];
     if (tid < T) {
       load_h(tid, hn);
-      if constexpr (PF) load_power(tid, pn);
+      if constexpr (PF) load_power(tid, pn, pol_keep);
     }
     for (int tl = 0; tl < ntiles; ++tl) {
       const int t = tl * FT + tid;
@@ -256,10 +261,10 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
       }
       if (t + FT < T) {
         load_h(t + FT, hn);
-        if constexpr (PF) load_power(t + FT, pn);
+        if constexpr (PF) load_power(t + FT, pn, pol_keep);
       }
       if constexpr (SB && !PF)
-        if (tid < tn) load_power(t, pv);
+        if (tid < tn) load_power(t, pv, pol_keep);
       if (tid < tn) {
 #pragma unroll
         for (int n = 0; n < kMaxN; ++n)
@@ -410,7 +415,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     double hn[kMaxN], pn[MP];
     if (tid < T) {
       load_h(tid, hn);
-      if constexpr (PF) load_power(tid, pn);
+      if constexpr (PF) load_power(tid, pn, pol_last);
     }
     for (int tl = 0; tl < ntiles; ++tl) {
       const int t = tl * FT + tid;
@@ -421,7 +426,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
       if (a.start && tid < tn) {
         if constexpr (SB) {
 #pragma unroll
-          for (int m = 0; m < MS; ++m) cp_async16(xsm + m * FTp + tid, xt + m);
+          for (int m = 0; m < MS; ++m) cp_async16_hint(xsm + m * FTp + tid, xt + m, pol_keep);
         } else {
           for (int m = 0; m < M; ++m) {
             const double2 v = __ldg(reinterpret_cast<const double2*>(xt + m));
@@ -438,10 +443,10 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
       }
       if (t + FT < T) {
         load_h(t + FT, hn);
-        if constexpr (PF) load_power(t + FT, pn);
+        if constexpr (PF) load_power(t + FT, pn, pol_last);
       }
       if constexpr (SB && !PF)
-        if (tid < tn) load_power(t, pv);
+        if (tid < tn) load_power(t, pv, pol_last);
       if (tid < tn) {
         if constexpr (IL) {
           double raw[MI];
@@ -533,7 +538,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   if constexpr (SB) {
     if (pf_early && tid < T)
 #pragma unroll
-      for (int m = 0; m < MS; ++m) cp_async16(xst + m * FTpc + tid, xf + (size_t)tid * M + m);
+      for (int m = 0; m < MS; ++m) cp_async16_hint(xst + m * FTpc + tid, xf + (size_t)tid * M + m, pol_last);
   }
   for (int idx = tid; idx < nitems * MAXMB; idx += FT) {
     const int it = idx / MAXMB, mu = idx - it * MAXMB;
@@ -656,7 +661,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   if constexpr (SB) {  // Q_mu is dead: pass C's first frame into the tile start
     if (!pf_early && tid < T)
 #pragma unroll
-      for (int m = 0; m < MS; ++m) cp_async16(xst + m * FTpc + tid, xf + (size_t)tid * M + m);
+      for (int m = 0; m < MS; ++m) cp_async16_hint(xst + m * FTpc + tid, xf + (size_t)tid * M + m, pol_last);
   }
   for (int e = tid; e < wsz; e += FT) a.W[(size_t)f * wsz + e] = Wsm[e];
   em_stamp(a, 4);
@@ -721,7 +726,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     if constexpr (SB) {
       if (t + FT < T) {  // the thread's next frame, after its slot has been read
 #pragma unroll
-        for (int m = 0; m < MS; ++m) cp_async16(xst + m * FTpc + tid, xt + (size_t)FT * M + m);
+        for (int m = 0; m < MS; ++m) cp_async16_hint(xst + m * FTpc + tid, xt + (size_t)FT * M + m, pol_last);
       }
     }
 #pragma unroll
