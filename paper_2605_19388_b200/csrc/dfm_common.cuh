@@ -328,7 +328,8 @@ __device__ __forceinline__ double rsqrt_pos(double x) {
 // so that each column of ip_sweep_warp is a handful of lane-parallel
 // matrix-vector products instead of dependent triangular solves.
 // sum_{c < n} term(c) with four independent accumulators: a dependent FP64
-// FMA costs ~23 cycles on sm_100, so a single running sum over a row of a
+// step (operand from shared memory, then FMA) costs ~23 cycles on sm_100
+// (tools/ip_warp_microbench.cu; a bare DFMA chain is 8), so a single running sum over a row of a
 // small matrix is latency-bound four times over.
 template <class F>
 __device__ __forceinline__ cd dot4(int n, const F& term) {

@@ -815,10 +815,32 @@ __global__ void __launch_bounds__(32 * kSpecWarps) k_spec_mma(int F, int T, int 
 // order as k_spec_mma, so H is bitwise the same).  spec_rows: bins f0..f0+7,
 // every frame (warps stride over 8-frame tiles); spec_cols: frames t0..t0+7,
 // every bin (warps stride over 8-bin tiles).
+// IS-NMF (init.cpp:346-358) passes tgt: each rec value also yields its
+// weights Bw = 1/max(rec, eps), Aw = Bw^2 tgt ([N][F][T], the k_is_weights
+// arithmetic), and spec_rows then skips the rec store (nothing reads it
+// before the V update rewrites it).
+__device__ __forceinline__ void is_weights2(int F, int T, int N, int n, int f, int t, double c0, double c1,
+                                            const double* __restrict__ tgt, double eps, double* __restrict__ Aw,
+                                            double* __restrict__ Bw) {
+  const double* tg = tgt + ((size_t)f * N + n) * T;
+  const size_t o = ((size_t)n * F + f) * T;
+  if (t < T) {
+    const double iv = 1.0 / fmax(c0, eps);
+    Bw[o + t] = iv;
+    Aw[o + t] = iv * iv * tg[t];
+  }
+  if (t + 1 < T) {
+    const double iv = 1.0 / fmax(c1, eps);
+    Bw[o + t + 1] = iv;
+    Aw[o + t + 1] = iv * iv * tg[t + 1];
+  }
+}
+
 template <int KS>
 __device__ __forceinline__ void spec_rows(int F, int T, int N, int K, int n, int f0, const double* __restrict__ Tf,
                                           const double* __restrict__ V, double* __restrict__ H, int warp, int nwarps,
-                                          int lane) {
+                                          int lane, const double* __restrict__ tgt = nullptr, double eps = 0.0,
+                                          double* __restrict__ Aw = nullptr, double* __restrict__ Bw = nullptr) {
   const int g = lane >> 2, q = lane & 3, f = f0 + g;
   double a[KS];
 #pragma unroll
@@ -838,6 +860,10 @@ __device__ __forceinline__ void spec_rows(int F, int T, int N, int K, int n, int
 #pragma unroll
     for (int s = 0; s < KS; ++s) dmma(c0, c1, a[s], b[s]);
     const int t = tile * 8 + 2 * q;
+    if (tgt) {
+      if (f < F) is_weights2(F, T, N, n, f, t, c0, c1, tgt, eps, Aw, Bw);
+      continue;
+    }
     if (f < F) {
       double* hp = H + ((size_t)f * N + n) * T;
       if (!(T & 1) && t + 1 < T) {
@@ -853,7 +879,8 @@ __device__ __forceinline__ void spec_rows(int F, int T, int N, int K, int n, int
 template <int KS>
 __device__ __forceinline__ void spec_cols(int F, int T, int N, int K, int n, int t0, const double* __restrict__ Tf,
                                           const double* __restrict__ V, double* __restrict__ H, int warp, int nwarps,
-                                          int lane) {
+                                          int lane, const double* __restrict__ tgt = nullptr, double eps = 0.0,
+                                          double* __restrict__ Aw = nullptr, double* __restrict__ Bw = nullptr) {
   const int g = lane >> 2, q = lane & 3, tl = t0 + g;
   double b[KS];
 #pragma unroll
@@ -873,6 +900,7 @@ __device__ __forceinline__ void spec_cols(int F, int T, int N, int K, int n, int
     double c0 = 0.0, c1 = 0.0;
 #pragma unroll
     for (int s = 0; s < KS; ++s) dmma(c0, c1, a[s], b[s]);
+    if (tgt && f < F) is_weights2(F, T, N, n, f, t, c0, c1, tgt, eps, Aw, Bw);  // rec is stored too (divergence)
     if (f < F) {
       double* hp = H + ((size_t)f * N + n) * T;
       if (!(T & 1) && t + 1 < T) {
@@ -895,7 +923,8 @@ __global__ void __launch_bounds__(32 * kTupdWarps, KT <= 2 ? 3 : 2) k_tupd_mma(i
                                                              const double* __restrict__ V,
                                                              const double* __restrict__ Aw,
                                                              const double* __restrict__ Bw, double floor_,
-                                                             const int* __restrict__ skip, double* __restrict__ Hout) {
+                                                             const int* __restrict__ skip, double* __restrict__ Hout,
+                                                             const double* __restrict__ tgt = nullptr) {
   __shared__ double part[kTupdWarps / 2][2][KT][64];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
@@ -973,7 +1002,9 @@ __global__ void __launch_bounds__(32 * kTupdWarps, KT <= 2 ? 3 : 2) k_tupd_mma(i
   }
   if (!Hout) return;
   __syncthreads();  // the CTA's new T rows are visible
-  spec_rows<2 * KT>(F, T, N, K, n, f0, Tf, V, Hout, warp, kTupdWarps, lane);  // h' = T_new V
+  // h' = T_new V (IS-NMF: the weights of rec = T_new V instead)
+  spec_rows<2 * KT>(F, T, N, K, n, f0, Tf, V, Hout, warp, kTupdWarps, lane, tgt, floor_, const_cast<double*>(Aw),
+                    const_cast<double*>(Bw));
 }
 
 // V update (engine.cpp:125-133): num[k][t] = sum_f T[f][n][k] A'[n][f][t].
@@ -987,7 +1018,8 @@ __global__ void __launch_bounds__(32 * kVupdMWarps, KT <= 2 ? 3 : 2) k_vupd_mma(
                                                               const double* __restrict__ Bw,
                                                               double* __restrict__ V, double* __restrict__ numden,
                                                               double floor_, const int* __restrict__ skip,
-                                                              double* __restrict__ Hout) {
+                                                              double* __restrict__ Hout,
+                                                              const double* __restrict__ tgt = nullptr) {
   __shared__ double part[kVupdMWarps / 2][2][KT][64];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
@@ -1068,7 +1100,9 @@ __global__ void __launch_bounds__(32 * kVupdMWarps, KT <= 2 ? 3 : 2) k_vupd_mma(
   }
   if (!Hout || numden) return;  // sharded: V is final only after the allreduce
   __syncthreads();  // the CTA's new V columns are visible
-  spec_cols<2 * KT>(F, T, N, K, n, t0, Tf, V, Hout, warp, kVupdMWarps, lane);  // H = T V_new
+  // H = T V_new (IS-NMF: and the next iteration's weights)
+  spec_cols<2 * KT>(F, T, N, K, n, t0, Tf, V, Hout, warp, kVupdMWarps, lane, tgt, floor_, const_cast<double*>(Aw),
+                    const_cast<double*>(Bw));
 }
 
 // Pass D as an elementwise kernel over (bin, frame): h' from H (= T_new V by

@@ -294,7 +294,7 @@ void launch_tupd(dfm_ctx* c) {
   }
   // h' = T_new V fused into the T update
   kern<<<grid, 32 * kTupdWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->V.p, c->Aw.p, c->Bw.p, c->floor_,
-                                                nullptr, c->H.p);
+                                                nullptr, c->H.p, nullptr);
   DFM_CK_LAUNCH();
   c->launches++;
 }
@@ -321,7 +321,7 @@ void launch_vupd(dfm_ctx* c) {
   }
   kern<<<grid, 32 * kVupdMWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->Aw.p, c->Bw.p, c->V.p,
                                                  sharded ? c->numden.p : nullptr, c->floor_, nullptr,
-                                                 sharded ? nullptr : c->H.p);  // H = T V_new fused (one GPU)
+                                                 sharded ? nullptr : c->H.p, nullptr);  // H = T V_new fused (one GPU)
   DFM_CK_LAUNCH();
   c->launches++;
   if (sharded && !c->host_exchange) {

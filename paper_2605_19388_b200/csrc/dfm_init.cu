@@ -767,7 +767,7 @@ int is_nmf_dev(const double* h0_dev, int F, int T, int N, int K, int max_iters, 
     // rec = T_new V fused (skipped with the update for converged sources,
     // whose rec is unchanged)
     kern<<<dim3((F + 7) / 8, N), 32 * kTupdWarps, 0, s>>>(F, T, N, K, Tf.p, V.p, Aw.p, Bw.p, kEpsNmf, done.p,
-                                                          H.p);
+                                                          H.p, tgt.p);
     DFM_CK_LAUNCH();
   };
   auto vupd = [&]() {
@@ -779,7 +779,7 @@ int is_nmf_dev(const double* h0_dev, int F, int T, int N, int K, int max_iters, 
       default: kern = k_vupd_mma<8>; break;
     }
     kern<<<dim3((T + 7) / 8, N), 32 * kVupdMWarps, 0, s>>>(F, T, N, K, Tf.p, Aw.p, Bw.p, V.p, nullptr, kEpsNmf,
-                                                         done.p, H.p);
+                                                         done.p, H.p, tgt.p);
     DFM_CK_LAUNCH();
   };
   spec();
@@ -789,11 +789,13 @@ int is_nmf_dev(const double* h0_dev, int F, int T, int N, int K, int max_iters, 
   cudaGraph_t g = nullptr;
   cudaGraphExec_t ge = nullptr;
   if (max_iters > 0) {
+    // the weights of each rec are formed in the epilogue that produces it
+    // (k_tupd: weights of T_new V; k_vupd: rec = T V_new and its weights for
+    // the next iteration), so only the first iteration's come from k_is_weights
+    weights();
     DFM_CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    weights();
-    tupd();  // + rec = T_new V
-    weights();
-    vupd();  // + rec = T V_new
+    tupd();  // -> weights of rec = T_new V
+    vupd();  // -> rec = T V_new and its weights
     divergence(0);
     DFM_CK(cudaStreamEndCapture(s, &g));
     DFM_CK(cudaGraphInstantiate(&ge, g, 0));
