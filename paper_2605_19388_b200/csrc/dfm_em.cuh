@@ -65,7 +65,9 @@ __host__ __device__ inline EmPlan plan_em(const EmArgs& a, int FT) {
   p.ldet = o; o += al((size_t)a.nb * sizeof(double));
   const size_t FTp = FT + 1;  // odd row stride: conflict-free item-parallel reads
   const size_t tA = (N + 2 * M) * FTp * sizeof(double);  // h, z, 1/eta
-  const size_t tB = (3 * M) * FTp * sizeof(double);      // x (complex), 1/eta
+  // x (complex, [M][FTp]) and 1/eta ([M][FTp], or frame-major [FT][M + 2]
+  // for the 4-mic Q loop)
+  const size_t tB = (2 * M * FTp + (M * FTp > FT * (M + 2) ? M * FTp : FT * (M + 2))) * sizeof(double);
   // Q_mu (written after pass B, read by the IP sweep) lives at the end of the
   // frame tile, which pass B no longer needs by then; pass C's first-frame
   // prefetch (M x (FT + 1) samples from the tile start) is issued early only
@@ -412,6 +414,11 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     const int FTp = FT + 1;
     cd* xsm = (cd*)tile;                              // [M][FTp]
     double* is = tile + 2 * (size_t)M * FTp;          // [M][FTp]
+    // 4-mic blocks: 1/eta frame-major [FT][ISP] (ISP = M + 2: 16-byte pairs,
+    // conflict-free 16-byte stores); a Q item then reads its block's four
+    // weights with two broadcast 16-byte loads instead of four 8-byte ones
+    constexpr bool IFM = SB && MB_ == 4 && IL;
+    constexpr int ISP = MS + 2;
     double hn[kMaxN], pn[MP];
     if (tid < T) {
       load_h(tid, hn);
@@ -452,11 +459,20 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
           double raw[MI];
           eta_raw(h, raw);
 #pragma unroll
-          for (int m = 0; m < MI; ++m) {
-            const double ie = rcp_pos(fmax(raw[m], floor_));
-            cost += pv[m] * ie;
+          for (int m = 0; m < MI; m += 2) {
+            const double ie0 = rcp_pos(fmax(raw[m], floor_)), ie1 = rcp_pos(fmax(raw[m + 1], floor_));
+            cost += pv[m] * ie0;
             lacc.mul(fmax(raw[m], 1e-300));
-            if (a.start) is[m * FTp + tid] = ie;
+            cost += pv[m + 1] * ie1;
+            lacc.mul(fmax(raw[m + 1], 1e-300));
+            if (a.start) {
+              if constexpr (IFM) {
+                *reinterpret_cast<double2*>(is + tid * ISP + m) = make_double2(ie0, ie1);
+              } else {
+                is[m * FTp + tid] = ie0;
+                is[(m + 1) * FTp + tid] = ie1;
+              }
+            }
           }
         } else
 #pragma unroll
@@ -498,6 +514,19 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
           cd qacc[MAXMB];
 #pragma unroll
           for (int mu = 0; mu < MAXMB; ++mu) qacc[mu] = cd{0.0, 0.0};
+          if constexpr (IFM) {
+            const double* ef = is + off;
+#pragma unroll 4
+            for (int tt = qs; tt < tn; tt += SQ) {
+              const cd pr = xr[tt] * conjg(xc[tt]);
+              const double2 e01 = *reinterpret_cast<const double2*>(ef + tt * ISP);
+              const double2 e23 = *reinterpret_cast<const double2*>(ef + tt * ISP + 2);
+              qacc[0] = qacc[0] + pr * e01.x;
+              qacc[1] = qacc[1] + pr * e01.y;
+              qacc[2] = qacc[2] + pr * e23.x;
+              qacc[3] = qacc[3] + pr * e23.y;
+            }
+          } else
 #pragma unroll 4
           for (int tt = qs; tt < tn; tt += SQ) {
             const cd pr = xr[tt] * conjg(xc[tt]);
