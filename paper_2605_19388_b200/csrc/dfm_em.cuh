@@ -64,7 +64,7 @@ __host__ __device__ inline EmPlan plan_em(const EmArgs& a, int FT) {
   p.wsum = o; o += al(64 * sizeof(double));
   p.ldet = o; o += al((size_t)a.nb * sizeof(double));
   const size_t FTp = FT + 1;  // odd row stride: conflict-free item-parallel reads
-  const size_t tA = (N + 2 * M) * FTp * sizeof(double);  // h, z, 1/eta
+  const size_t tA = (N + 2 * M) * (FTp + 3) * sizeof(double);  // h, z, 1/eta (pass A rows: FT + 4)
   // x (complex, [M][FTp]) and 1/eta ([M][FTp], or frame-major [FT][M + 2]
   // for the 4-mic Q loop)
   const size_t tB = (2 * M * FTp + (M * FTp > FT * (M + 2) ? M * FTp : FT * (M + 2))) * sizeof(double);
@@ -225,7 +225,9 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   // ================================================================ pass A
   // finish iteration i-1: Lambda update with eta = max(h Lambda_old, floor)
   if (a.finish == 2) {
-    const int FTp = FT + 1;
+    // row stride = 4 mod 32 (static shapes): the DMMA fragment loads (8 rows x
+    // 4 consecutive frames) hit 32 distinct banks
+    const int FTp = SB ? FT + 4 : FT + 1;
     double* hs = tile;               // [N][FTp]
     double* zs = tile + N * FTp;     // [M][FTp]
     double* is = zs + M * FTp;       // [M][FTp]
