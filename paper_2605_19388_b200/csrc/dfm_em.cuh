@@ -206,6 +206,22 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   // m-outer form's bitwise).  Lambda rows [n][M] are read as 16-byte pairs.
   constexpr bool IL = SB && MS <= 16 && (MS % 2 == 0);
   constexpr int MI = IL ? MS : 1;
+  // warp-cooperative copy of this bin's frames [fr0, fr0 + 32) (clipped to
+  // T) into the mic-major tile slots dst[m * stride + slot0 + i]: each lane
+  // takes 16-byte chunks of the contiguous global run (coalesced: 512 B per
+  // instruction) instead of walking its own frame with a 192-byte stride
+  auto warp_copy_x = [&](cd* dst, int stride, int slot0, int fr0, unsigned long long pol) {
+    const int lane = tid & 31;
+    const int nf = min(32, T - fr0);
+    if (nf <= 0) return;
+    const cd* src = xf + (size_t)fr0 * MS;
+#pragma unroll
+    for (int j = 0; j < MS; ++j) {
+      const int c = lane + 32 * j;  // chunk c: frame c / MS, mic c % MS
+      const int fl = c / MS, m = c - fl * MS;
+      if (fl < nf) cp_async16_hint(dst + m * stride + slot0 + fl, src + c, pol);
+    }
+  };
   auto eta_raw = [&](const double* h, double* raw) {
 #pragma unroll
     for (int m = 0; m < MI; ++m) raw[m] = 0.0;
@@ -432,10 +448,11 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
       const cd* xt = xf + (size_t)t * M;
       // the frame's samples for the Q tile: asynchronous copies that land
       // while the per-frame terms below are computed
+      if constexpr (SB) {
+        if (a.start) warp_copy_x(xsm, FTp, tid & ~31, tl * FT + (tid & ~31), pol_keep);
+      }
       if (a.start && tid < tn) {
         if constexpr (SB) {
-#pragma unroll
-          for (int m = 0; m < MS; ++m) cp_async16_hint(xsm + m * FTp + tid, xt + m, pol_keep);
         } else {
           for (int m = 0; m < M; ++m) {
             const double2 v = __ldg(reinterpret_cast<const double2*>(xt + m));
@@ -567,9 +584,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   const bool pf_early = (size_t)M * FTpc * sizeof(cd) <= sp.qsum - sp.tile;
   __syncthreads();  // the Q tile reads of pass B are done (Qsum overwrites the tile end)
   if constexpr (SB) {
-    if (pf_early && tid < T)
-#pragma unroll
-      for (int m = 0; m < MS; ++m) cp_async16_hint(xst + m * FTpc + tid, xf + (size_t)tid * M + m, pol_last);
+    if (pf_early) warp_copy_x(xst, FTpc, tid & ~31, tid & ~31, pol_last);
   }
   for (int idx = tid; idx < nitems * MAXMB; idx += FT) {
     const int it = idx / MAXMB, mu = idx - it * MAXMB;
@@ -690,9 +705,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   }
   __syncthreads();
   if constexpr (SB) {  // Q_mu is dead: pass C's first frame into the tile start
-    if (!pf_early && tid < T)
-#pragma unroll
-      for (int m = 0; m < MS; ++m) cp_async16_hint(xst + m * FTpc + tid, xf + (size_t)tid * M + m, pol_last);
+    if (!pf_early) warp_copy_x(xst, FTpc, tid & ~31, tid & ~31, pol_last);
   }
   for (int e = tid; e < wsz; e += FT) a.W[(size_t)f * wsz + e] = Wsm[e];
   em_stamp(a, 4);
@@ -700,14 +713,21 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   // ================================================================ pass C
   // P = |W_new^H x|^2 and the T-update weights with the pre-update eta
   // (engine.cpp:100-109), written per (source, bin, frame) for k_tupd
-  for (int t = tid; t < T; t += FT) {
-    double h[kMaxN];
-    load_h(t, h);
-    const cd* xt = xf + (size_t)t * M;
-    if constexpr (SB) cp_async_wait_all();
+  // uniform trip count over the frame tiles (the warp copies need every lane)
+  for (int t0 = 0; t0 < T; t0 += FT) {
+    const int t = t0 + tid;
+    const bool act = t < T;
+    if constexpr (SB) {
+      cp_async_wait_all();
+      __syncwarp();  // the warp's copies of this tile's frames have landed
+    }
     double A[kMaxN], B[kMaxN];
 #pragma unroll
     for (int n = 0; n < kMaxN; ++n) A[n] = B[n] = 0.0;
+    if (act) {
+    double h[kMaxN];
+    load_h(t, h);
+    const cd* xt = xf + (size_t)t * M;
     double rawc[MI];
     if constexpr (IL) eta_raw(h, rawc);
 #pragma unroll
@@ -754,19 +774,19 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
             }
         }
     }
+    }  // act
     if constexpr (SB) {
-      if (t + FT < T) {  // the thread's next frame, after its slot has been read
-#pragma unroll
-        for (int m = 0; m < MS; ++m) cp_async16_hint(xst + m * FTpc + tid, xt + (size_t)FT * M + m, pol_last);
-      }
+      __syncwarp();  // every lane has read its slot: the warp's next frames
+      if (t0 + FT < T) warp_copy_x(xst, FTpc, tid & ~31, t0 + FT + (tid & ~31), pol_last);
     }
+    if (act)
 #pragma unroll
-    for (int n = 0; n < kMaxN; ++n)
-      if (n < N) {
-        const size_t o = ((size_t)n * a.F + f) * T + t;
-        a.Aw[o] = A[n];
-        a.Bw[o] = B[n];
-      }
+      for (int n = 0; n < kMaxN; ++n)
+        if (n < N) {
+          const size_t o = ((size_t)n * a.F + f) * T + t;
+          a.Aw[o] = A[n];
+          a.Bw[o] = B[n];
+        }
   }
   em_stamp(a, 5);
 }
