@@ -210,7 +210,25 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   // T) into the mic-major tile slots dst[m * stride + slot0 + i]: each lane
   // takes 16-byte chunks of the contiguous global run (coalesced: 512 B per
   // instruction) instead of walking its own frame with a 192-byte stride
-  auto warp_copy_x = [&](cd* dst, int stride, int slot0, int fr0, unsigned long long pol) {
+  //
+  // Static shapes keep the staged samples frame-major, [slot][MS] (the
+  // global order, so a copy instruction writes a few whole shared-memory
+  // lines), with the mic index XOR-swizzled per slot: xsw(slot, m) spreads a
+  // warp's per-thread reads of its own frame (pass C) over all banks, and
+  // the Q loop's reads of one frame stay within one row.
+  // (Frames of more than 16 mics keep the mic-major [m][FT + 1] layout: the
+  // frame-major one hit an illegal-instruction trap in the 8 x 4-mic
+  // instantiation, cause not isolated.)
+  constexpr bool XFM = SB && MS <= 16;
+  auto xsw = [&](int slot, int m) -> int {
+    if constexpr (XFM) {
+      const int k = (MS % 8 == 0) ? (slot & 7) : ((MS % 4 == 0) ? ((slot >> 1) & 3) : 0);
+      return slot * MS + (m ^ k);
+    } else {
+      return m * (FT + 1) + slot;
+    }
+  };
+  auto warp_copy_x = [&](cd* dst, int slot0, int fr0, unsigned long long pol) {
     const int lane = tid & 31;
     const int nf = min(32, T - fr0);
     if (nf <= 0) return;
@@ -219,7 +237,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     for (int j = 0; j < MS; ++j) {
       const int c = lane + 32 * j;  // chunk c: frame c / MS, mic c % MS
       const int fl = c / MS, m = c - fl * MS;
-      if (fl < nf) cp_async16_hint(dst + m * stride + slot0 + fl, src + c, pol);
+      if (fl < nf) cp_async16_hint(dst + xsw(slot0 + fl, m), src + c, pol);
     }
   };
   auto eta_raw = [&](const double* h, double* raw) {
@@ -449,7 +467,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
       // the frame's samples for the Q tile: asynchronous copies that land
       // while the per-frame terms below are computed
       if constexpr (SB) {
-        if (a.start) warp_copy_x(xsm, FTp, tid & ~31, tl * FT + (tid & ~31), pol_keep);
+        if (a.start) warp_copy_x(xsm, tid & ~31, tl * FT + (tid & ~31), pol_keep);
       }
       if (a.start && tid < tn) {
         if constexpr (SB) {
@@ -527,7 +545,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
           }
           decode_entry(rem, qr, qc);
           const int mb = MBof(qb_), off = OFF(qb_);
-          const cd* xr = xsm + (off + qr) * FTp;
+          const cd* xr = xsm + (off + qr) * FTp;  // generic layout [M][FTp]
           const cd* xc = xsm + (off + qc) * FTp;
           const double* ew = is + off * FTp;
           cd qacc[MAXMB];
@@ -537,7 +555,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
             const double* ef = is + off;
 #pragma unroll 4
             for (int tt = qs; tt < tn; tt += SQ) {
-              const cd pr = xr[tt] * conjg(xc[tt]);
+              const cd pr = xsm[xsw(tt, off + qr)] * conjg(xsm[xsw(tt, off + qc)]);
               const double2 e01 = *reinterpret_cast<const double2*>(ef + tt * ISP);
               const double2 e23 = *reinterpret_cast<const double2*>(ef + tt * ISP + 2);
               qacc[0] = qacc[0] + pr * e01.x;
@@ -548,7 +566,11 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
           } else
 #pragma unroll 4
           for (int tt = qs; tt < tn; tt += SQ) {
-            const cd pr = xr[tt] * conjg(xc[tt]);
+            cd pr;
+            if constexpr (SB)
+              pr = xsm[xsw(tt, off + qr)] * conjg(xsm[xsw(tt, off + qc)]);
+            else
+              pr = xr[tt] * conjg(xc[tt]);
 #pragma unroll
             for (int mu = 0; mu < MAXMB; ++mu)
               if (mu < mb) qacc[mu] = qacc[mu] + pr * ew[mu * FTp + tt];
@@ -580,11 +602,11 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   // pass C's first frame: copies in flight during the Q reduction and the IP
   // sweep (thread-private slots of the free frame tile)
   const int FTpc = FT + 1;
-  cd* xst = (cd*)tile;  // [M][FTpc]
+  cd* xst = (cd*)tile;  // static shapes: [FT][MS] frame-major, swizzled (xsw)
   const bool pf_early = (size_t)M * FTpc * sizeof(cd) <= sp.qsum - sp.tile;
   __syncthreads();  // the Q tile reads of pass B are done (Qsum overwrites the tile end)
   if constexpr (SB) {
-    if (pf_early) warp_copy_x(xst, FTpc, tid & ~31, tid & ~31, pol_last);
+    if (pf_early) warp_copy_x(xst, tid & ~31, tid & ~31, pol_last);
   }
   for (int idx = tid; idx < nitems * MAXMB; idx += FT) {
     const int it = idx / MAXMB, mu = idx - it * MAXMB;
@@ -705,7 +727,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   }
   __syncthreads();
   if constexpr (SB) {  // Q_mu is dead: pass C's first frame into the tile start
-    if (!pf_early) warp_copy_x(xst, FTpc, tid & ~31, tid & ~31, pol_last);
+    if (!pf_early) warp_copy_x(xst, tid & ~31, tid & ~31, pol_last);
   }
   for (int e = tid; e < wsz; e += FT) a.W[(size_t)f * wsz + e] = Wsm[e];
   em_stamp(a, 4);
@@ -737,7 +759,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
         const cd* wb = Wsm + b * MB_ * MB_;
         cd xv[MB_];
 #pragma unroll
-        for (int q = 0; q < MB_; ++q) xv[q] = xst[(b * MB_ + q) * FTpc + tid];
+        for (int q = 0; q < MB_; ++q) xv[q] = xst[xsw(tid, b * MB_ + q)];
 #pragma unroll
         for (int mu = 0; mu < MB_; ++mu) {
           cd s{0.0, 0.0};
@@ -777,7 +799,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     }  // act
     if constexpr (SB) {
       __syncwarp();  // every lane has read its slot: the warp's next frames
-      if (t0 + FT < T) warp_copy_x(xst, FTpc, tid & ~31, t0 + FT + (tid & ~31), pol_last);
+      if (t0 + FT < T) warp_copy_x(xst, tid & ~31, t0 + FT + (tid & ~31), pol_last);
     }
     if (act)
 #pragma unroll
