@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   double cost = 0.0;
   LogAcc lacc;
   const int nitems = sp.nitems, SQ = sp.SQ;
-  cd* qpart = (cd*)red;  // [SQ][nitems][MAXMB] running sums over tiles
+  cd* qpart = (cd*)red;  // [MAXMB][SQ * nitems] running sums over tiles (item-slices contiguous)
   if (a.start)
     for (int e = tid; e < SQ * nitems * MAXMB; e += FT) qpart[e] = cd{0.0, 0.0};
   // log-det (+ W^-1 for the fast IP path) of the pre-IP demixers: threads
@@ -575,10 +575,11 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
             for (int mu = 0; mu < MAXMB; ++mu)
               if (mu < mb) qacc[mu] = qacc[mu] + pr * ew[mu * FTp + tt];
           }
-          cd* dst = qpart + (size_t)u * MAXMB;
+          cd* dst = qpart + u;
+          const int NU = nitems * SQ;
 #pragma unroll
           for (int mu = 0; mu < MAXMB; ++mu)
-            if (mu < mb) dst[mu] = dst[mu] + qacc[mu];
+            if (mu < mb) dst[mu * NU] = dst[mu * NU] + qacc[mu];
         }
         __syncthreads();
       }
@@ -622,7 +623,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     const int mb = MBof(b);
     if (mu >= mb) continue;
     cd sum{0.0, 0.0};
-    for (int s = 0; s < SQ; ++s) sum = sum + qpart[(s * nitems + it) * MAXMB + mu];
+    for (int s = 0; s < SQ; ++s) sum = sum + qpart[mu * (SQ * nitems) + s * nitems + it];
     const int E = mb * (mb + 1) / 2;
     Qsum[a.qofs[b] + mu * E + rem] = cd{sum.re / (double)T, sum.im / (double)T};
   }
