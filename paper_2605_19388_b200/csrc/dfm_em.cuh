@@ -235,9 +235,17 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     const cd* src = xf + (size_t)fr0 * MS;
 #pragma unroll
     for (int j = 0; j < MS; ++j) {
-      const int c = lane + 32 * j;  // chunk c: frame c / MS, mic c % MS
+      const int c = lane + 32 * j;  // frame c / MS, mic c % MS
       const int fl = c / MS, m = c - fl * MS;
-      if (fl < nf) cp_async16_hint(dst + xsw(slot0 + fl, m), src + c, pol);
+      if constexpr (XFM) {
+        // lane order = destination order: the lane writing (slot, m) fetches
+        // the sample whose swizzled position that is (XOR is an involution;
+        // the source stays within the same 64-byte group)
+        const int k = xsw(slot0 + fl, 0) - (slot0 + fl) * MS;  // the slot's XOR key
+        if (fl < nf) cp_async16_hint(dst + (slot0 + fl) * MS + m, src + fl * MS + (m ^ k), pol);
+      } else {
+        if (fl < nf) cp_async16_hint(dst + xsw(slot0 + fl, m), src + c, pol);
+      }
     }
   };
   auto eta_raw = [&](const double* h, double* raw) {
