@@ -1101,11 +1101,12 @@ __global__ void __launch_bounds__(32 * kVupdMWarps, KT <= 2 ? 3 : 2) k_vupd_mma(
                                                               double* __restrict__ V, double* __restrict__ numden,
                                                               double floor_, const int* __restrict__ skip,
                                                               double* __restrict__ Hout,
-                                                              const double* __restrict__ tgt = nullptr) {
+                                                              const double* __restrict__ tgt = nullptr,
+                                                              int n_base = 0) {
   __shared__ double part[kVupdMWarps / 2][2][KT][64];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
-  const int n = blockIdx.y, t0 = blockIdx.x * 8;
+  const int n = n_base + blockIdx.y, t0 = blockIdx.x * 8;  // n_base: source chunk (sharded overlap)
   if (skip && skip[n]) return;  // IS-NMF: this source has converged
   constexpr int kt = KT;
   const int steps = (F + 3) / 4;

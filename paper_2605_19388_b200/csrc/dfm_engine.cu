@@ -85,6 +85,10 @@ NcclApi& nccl() {
     }                                                                              \
   } while (0)
 
+namespace dfm {
+constexpr int kVupdChunks = 2;  // source chunks of the sharded V update (allreduce overlap)
+}
+
 struct dfm_ctx {
   int device = 0;
   int Fg = 0, f0 = 0, f1 = 0, F = 0, T = 0, M = 0, N = 0, K = 0;
@@ -111,6 +115,10 @@ struct dfm_ctx {
   int nranks = 1, rank = 0;
   long long launches = 0;
   cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  // sharded V update: the allreduce of one source chunk's {num, den} runs on
+  // comm_stream while the next chunk is computed (SURVEY §8e overlap)
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_chunk[kVupdChunks] = {}, ev_join = nullptr;
   cudaGraphExec_t step_exec = nullptr;  // one steady-state iteration
   long long graph_launches = 0;         // kernels in one replay
   int dbg = 0;
@@ -319,18 +327,48 @@ void launch_vupd(dfm_ctx* c) {
     case 3: case 4: kern = k_vupd_mma<4>; break;
     default: kern = k_vupd_mma<8>; break;
   }
-  kern<<<grid, 32 * kVupdMWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->Aw.p, c->Bw.p, c->V.p,
-                                                 sharded ? c->numden.p : nullptr, c->floor_, nullptr,
-                                                 sharded ? nullptr : c->H.p, nullptr);  // H = T V_new fused (one GPU)
-  DFM_CK_LAUNCH();
-  c->launches++;
-  if (sharded && !c->host_exchange) {
-    const size_t nkt = (size_t)c->N * c->K * c->T;
-    NCCL_CK(nccl().AllReduce(c->numden.p, c->numden.p, 2 * nkt, ncclDouble, ncclSum, c->comm, c->stream));
-    k_vapply<<<(unsigned)((nkt + 255) / 256), 256, 0, c->stream>>>(nkt, c->numden.p, c->V.p, c->floor_);
+  if (!sharded || c->host_exchange) {
+    kern<<<grid, 32 * kVupdMWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->Aw.p, c->Bw.p, c->V.p,
+                                                   sharded ? c->numden.p : nullptr, c->floor_, nullptr,
+                                                   sharded ? nullptr : c->H.p, nullptr, 0);  // H = T V_new fused
     DFM_CK_LAUNCH();
     c->launches++;
+    return;
   }
+  // NCCL path: sources in chunks; chunk j's {num, den} rows ([n][K][T] slices
+  // of both halves of numden, contiguous) are allreduced on comm_stream while
+  // chunk j + 1 is computed; k_vapply waits for the last allreduce
+  const size_t nkt = (size_t)c->N * c->K * c->T, kt = (size_t)c->K * c->T;
+  static const int env_ch = [] {
+    const char* e = getenv("DFM_VUPD_CHUNKS");  // 1 = one allreduce after the whole V update
+    return e ? std::max(1, std::min(kVupdChunks, atoi(e))) : kVupdChunks;
+  }();
+  const int nch = std::min(env_ch, c->N);
+  if (!c->comm_stream) {
+    DFM_CK(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    for (auto& e : c->ev_chunk) DFM_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    DFM_CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  }
+  for (int j = 0; j < nch; ++j) {
+    const int n0 = c->N * j / nch, n1 = c->N * (j + 1) / nch;
+    const dim3 gj((c->T + 7) / 8, n1 - n0);
+    kern<<<gj, 32 * kVupdMWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->Aw.p, c->Bw.p, c->V.p,
+                                                 c->numden.p, c->floor_, nullptr, nullptr, nullptr, n0);
+    DFM_CK_LAUNCH();
+    c->launches++;
+    DFM_CK(cudaEventRecord(c->ev_chunk[j], c->stream));
+    DFM_CK(cudaStreamWaitEvent(c->comm_stream, c->ev_chunk[j], 0));
+    double* num = c->numden.p + n0 * kt;
+    double* den = c->numden.p + nkt + n0 * kt;
+    const size_t cnt = (size_t)(n1 - n0) * kt;
+    NCCL_CK(nccl().AllReduce(num, num, cnt, ncclDouble, ncclSum, c->comm, c->comm_stream));
+    NCCL_CK(nccl().AllReduce(den, den, cnt, ncclDouble, ncclSum, c->comm, c->comm_stream));
+  }
+  DFM_CK(cudaEventRecord(c->ev_join, c->comm_stream));
+  DFM_CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+  k_vapply<<<(unsigned)((nkt + 255) / 256), 256, 0, c->stream>>>(nkt, c->numden.p, c->V.p, c->floor_);
+  DFM_CK_LAUNCH();
+  c->launches++;
 }
 
 // The "start" half of an iteration after k_em_bin: T update, V-update
@@ -494,6 +532,10 @@ void dfm_destroy(dfm_ctx* c) {
   for (auto e : c->iter_ev) cudaEventDestroy(e);
   for (auto e : c->ev)
     if (e) cudaEventDestroy(e);
+  for (auto e : c->ev_chunk)
+    if (e) cudaEventDestroy(e);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
