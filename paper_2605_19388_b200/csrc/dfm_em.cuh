@@ -355,18 +355,25 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
             const int s0 = slc * chunk, s1 = min(tn, s0 + chunk);
             // two independent accumulator chains (even / odd k-steps), added at
             // the end of the tile in a fixed order
-            double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
-            for (int t0 = s0; t0 < s1; t0 += 8) {
-              const int t = t0 + q, u = t0 + 4 + q;
-              const double av = (g < N && t < tn) ? hs[g * FTp + t] : 0.0;
-              const double bv = (col < 2 * M && t < tn) ? zs[col * FTp + t] : 0.0;
-              const double au = (g < N && u < tn) ? hs[g * FTp + u] : 0.0;
-              const double bu = (col < 2 * M && u < tn) ? zs[col * FTp + u] : 0.0;
-              dmma(c0, c1, av, bv);
-              dmma(d0, d1, au, bu);
+            // four independent accumulator chains (k-steps mod 4), added at
+            // the end of the tile in a fixed order
+            double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0, k0 = 0.0, k1 = 0.0;
+            for (int t0 = s0; t0 < s1; t0 += 16) {
+              double av[4], bv[4];
+#pragma unroll
+              for (int r = 0; r < 4; ++r) {
+                const int t = t0 + 4 * r + q;
+                const bool ok = t < s1 && t < tn;
+                av[r] = (g < N && ok) ? hs[g * FTp + t] : 0.0;
+                bv[r] = (col < 2 * M && ok) ? zs[col * FTp + t] : 0.0;
+              }
+              dmma(c0, c1, av[0], bv[0]);
+              dmma(d0, d1, av[1], bv[1]);
+              dmma(e0, e1, av[2], bv[2]);
+              dmma(k0, k1, av[3], bv[3]);
             }
-            lj0[jj] += c0 + d0;
-            lj1[jj] += c1 + d1;
+            lj0[jj] += (c0 + d0) + (e0 + k0);
+            lj1[jj] += (c1 + d1) + (e1 + k1);
           }
         }
       } else
