@@ -468,7 +468,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     // 4-mic blocks: 1/eta frame-major [FT][ISP] (ISP = M + 2: 16-byte pairs,
     // conflict-free 16-byte stores); a Q item then reads its block's four
     // weights with two broadcast 16-byte loads instead of four 8-byte ones
-    constexpr bool IFM = SB && MB_ == 4 && IL;
+    constexpr bool IFM = SB && IL && (MB_ % 2 == 0);
     constexpr int ISP = MS + 2;
     double hn[kMaxN], pn[MP];
     if (tid < T) {
@@ -568,15 +568,16 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
           for (int mu = 0; mu < MAXMB; ++mu) qacc[mu] = cd{0.0, 0.0};
           if constexpr (IFM) {
             const double* ef = is + off;
+            constexpr int MBI = IFM ? MB_ : 2;
 #pragma unroll 4
             for (int tt = qs; tt < tn; tt += SQ) {
               const cd pr = xsm[xsw(tt, off + qr)] * conjg(xsm[xsw(tt, off + qc)]);
-              const double2 e01 = *reinterpret_cast<const double2*>(ef + tt * ISP);
-              const double2 e23 = *reinterpret_cast<const double2*>(ef + tt * ISP + 2);
-              qacc[0] = qacc[0] + pr * e01.x;
-              qacc[1] = qacc[1] + pr * e01.y;
-              qacc[2] = qacc[2] + pr * e23.x;
-              qacc[3] = qacc[3] + pr * e23.y;
+#pragma unroll
+              for (int mu = 0; mu < MBI; mu += 2) {
+                const double2 e = *reinterpret_cast<const double2*>(ef + tt * ISP + mu);
+                qacc[mu] = qacc[mu] + pr * e.x;
+                qacc[mu + 1] = qacc[mu + 1] + pr * e.y;
+              }
             }
           } else
 #pragma unroll 4
