@@ -222,7 +222,9 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   constexpr bool XFM = SB && MS <= 16;
   auto xsw = [&](int slot, int m) -> int {
     if constexpr (XFM) {
-      const int k = (MS % 8 == 0) ? (slot & 7) : ((MS % 4 == 0) ? ((slot >> 1) & 3) : 0);
+      // even keys keep each 32-byte pair of samples whole (copies stay in
+      // sector order); measured better than the full 2-bit key and than none
+      const int k = (MS % 8 == 0) ? (slot & 7) : ((MS % 4 == 0) ? ((slot >> 1) & 2) : 0);
       return slot * MS + (m ^ k);
     } else {
       return m * (FT + 1) + slot;
