@@ -98,7 +98,7 @@ def peaks():
 class ClockSampler:
     """Samples SM clocks and throttle reasons via NVML during the timed region."""
 
-    def __init__(self, device: int, period_s: float = 0.02):
+    def __init__(self, device: int, period_s: float = 0.002):
         self.device, self.period, self.samples, self.reasons = device, period_s, [], set()
         self.max_mhz = None
         self._stop = threading.Event()
@@ -159,74 +159,121 @@ def shard(F: int, world: int, rank: int):
     return shard_bins(F, world, rank)
 
 
-def cpu_baseline(c, x, init_d, threads: int, target_s: float = 15.0):
-    """The oracle (C restatement of engine.cpp) timed on host cores over a
-    bounded sample of the workload: the first Fs bins, a few EM iterations."""
+def host_cpu() -> dict:
+    """nproc and the CPU model of this host (BASELINE.md CPU baseline plan)."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count() or 1
+    return {"nproc": usable, "cpu_count": os.cpu_count() or 1, "model": model}
+
+
+def cpu_protocol(workload: str, threads: int, steps: int, warmup: int, budget_s: float, mixture: int = 0) -> dict:
+    """The reference's CPU algorithm (oracle/ C restatement of engine.cpp;
+    the reference itself needs Eigen3, absent here) timed with the
+    reference's protocol (bench.cpp:31-71): one untimed warm-up run, then the
+    timed EM iterations split into repeats of >= 5 iterations (every repeat an
+    independent run from the same dumped start, the per-iteration cost
+    evaluation included as in engine.cpp:253), reported as mean +- SE over
+    the repeats.  The sample is the first Fs bins of the workload's own
+    mixture (every frame), Fs sized so the whole run fits `budget_s`.
+    Inputs come from the oracle's restatement of the BASELINE generator and
+    of random_init only: this process never loads the product library."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle
 
     oracle.build()
+    c = CONFIGS[workload]
+    F, T, N, K, sizes = c["F"], c["T"], c["N"], c["K"], c["sizes"]
+    oracle.set_threads(max(1, min(threads, 64)))
+    x = oracle.generate_mixture(c["kind"], F, T, sum(sizes), N, K, SEED_X + mixture)
+    init = oracle.random_init(F, T, sizes, N, K, SEED_INIT + mixture)
+    sub = lambda Fs: dict(T=np.ascontiguousarray(init["T"][:, :Fs]), V=init["V"],
+                          lam=np.ascontiguousarray(init["lam"][:Fs]),
+                          w=[np.ascontiguousarray(w[:Fs]) for w in init["w"]])
     oracle.set_threads(threads)
-    F, T = c["F"], c["T"]
-    # probe the per-bin cost on a small slice, then size the sample
-    Fp = min(F, 16)
-    sub = lambda Fs: dict(T=np.ascontiguousarray(init_d["T"][:, :Fs]), V=init_d["V"],
-                          lam=np.ascontiguousarray(init_d["lam"][:Fs]),
-                          w=[np.ascontiguousarray(w[:Fs]) for w in init_d["w"]])
-    r = oracle.run_engine(np.ascontiguousarray(x[:Fp]), c["sizes"], sub(Fp), 2)
-    per_bin_iter = max(float(np.mean(r["wall_seconds"])) / Fp, 1e-9)
-    iters = 3
-    Fs = int(max(Fp, min(F, target_s / (iters * per_bin_iter))))
-    r = oracle.run_engine(np.ascontiguousarray(x[:Fs]), c["sizes"], sub(Fs), iters)
-    t_iter = float(np.mean(r["wall_seconds"][1:]))  # first timed iteration treated as warm-up
-    return dict(value=Fs * T / t_iter, unit="TF-bin*iter/s", cores=threads, kind="port",
-                sample=f"oracle/ run_engine on the first {Fs} of {F} bins x {T} frames, {iters} EM iters "
-                       f"(mean of iters 2..{iters}; {t_iter:.3f} s/iter)",
-                seconds_per_iter_full=t_iter * F / Fs)
+    Fp = min(F, max(8, threads))
+    r = oracle.run_engine(np.ascontiguousarray(x[:Fp]), sizes, sub(Fp), 1)
+    per_bin_iter = max(float(np.sum(r["wall_seconds"])) / Fp, 1e-9)
+    Fs = int(max(min(F, 8), min(F, budget_s / ((steps + max(warmup, 1)) * per_bin_iter))))
+    xs = np.ascontiguousarray(x[:Fs])
+    oracle.run_engine(xs, sizes, sub(Fs), max(warmup, 1))  # untimed warm-up run
+    nrep = max(1, steps // 5)
+    lens = [5] * (nrep - 1) + [steps - 5 * (nrep - 1)]
+    per_rep, total = [], 0.0
+    for it in lens:
+        rr = oracle.run_engine(xs, sizes, sub(Fs), it)
+        t = float(np.sum(rr["wall_seconds"]))
+        total += t
+        per_rep.append(Fs * T * it / t)
+    mean = float(np.mean(per_rep))
+    se = float(np.std(per_rep, ddof=1) / np.sqrt(len(per_rep))) if len(per_rep) > 1 else 0.0
+    return {"value": Fs * T * steps / total, "unit": "TF-bin*iter/s", "mean": mean, "se": se,
+            "repeats": len(per_rep), "iters_per_repeat": lens, "per_repeat": per_rep, "cores": threads,
+            "kind": "port", "seconds_per_iter_sample": total / steps, "seconds_per_iter_full": total / steps * F / Fs,
+            "sample": (f"oracle/ run_engine (C restatement of engine.cpp, OpenMP over bins) on the first {Fs} of {F} "
+                       f"bins x {T} frames of the {workload} mixture; 1 warm-up run of {max(warmup, 1)} iteration(s), "
+                       f"then {steps} timed iterations in {len(per_rep)} repeats; mean +- SE over the repeats"),
+            "host": host_cpu()}
+
+
+def cpu_protocol_subprocess(workload: str, threads: int, steps: int, warmup: int, budget_s: float,
+                            mixture: int = 0) -> dict:
+    """cpu_protocol in a fresh interpreter (numpy + oracle only): no torch
+    OpenMP pool or CUDA context shares the cores, and the product library is
+    never mapped, so the bench's baseline and the reference arm measure the
+    same thing."""
+    import subprocess
+
+    spec = json.dumps(dict(workload=workload, threads=threads, steps=steps, warmup=warmup, budget_s=budget_s,
+                           mixture=mixture))
+    out = subprocess.run([sys.executable, os.path.abspath(__file__), "--cpu-worker", spec], check=True,
+                         capture_output=True, text=True).stdout
+    return json.loads(out.strip().splitlines()[-1])
+
+
+def bench_config(workload: str, world: int) -> dict:
+    """The workload's identity, identical in both arms' JSON lines."""
+    c = CONFIGS[workload]
+    out = {"workload": workload, **{k: c[k] for k in ("F", "T", "sizes", "N", "K", "iters")}}
+    if "batch" in c:
+        out["mixtures"] = c["batch"]
+    out["gpus"] = world
+    return out
 
 
 def run_reference(args, c, world, rank):
-    """--impl reference: the reference's CPU algorithm on all host threads."""
+    """--impl reference: the reference's CPU algorithm on all host threads,
+    rank 0 only, in the reference's timing protocol (cpu_protocol).  Each
+    step is one EM iteration over the sample bins of the workload."""
     if rank != 0:
         return None
-    import paper_2605_19388_b200 as dfm
-
-    layout = dfm.BlockLayout(c["sizes"])
-    x = dfm.generate_mixture(c["kind"], c["F"], c["T"], layout.total, c["N"], c["K"], SEED_X)
-    init = dfm.random_init(c["F"], c["T"], layout, c["N"], c["K"], SEED_INIT)
-    init_d = dict(T=init.nmf.T, V=init.nmf.V, lam=init.lambda0, w=init.w0)
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle
-
-    oracle.build()
-    threads = os.cpu_count() or 1
-    oracle.set_threads(threads)
-    F, T = c["F"], c["T"]
-    Fp = min(F, 32)
-    sub = lambda Fs: dict(T=np.ascontiguousarray(init_d["T"][:, :Fs]), V=init_d["V"],
-                          lam=np.ascontiguousarray(init_d["lam"][:Fs]),
-                          w=[np.ascontiguousarray(w[:Fs]) for w in init_d["w"]])
-    r = oracle.run_engine(np.ascontiguousarray(x[:Fp]), c["sizes"], sub(Fp), 2)
-    per_bin_iter = max(float(np.mean(r["wall_seconds"])) / Fp, 1e-9)
-    total_iters = args.warmup + args.steps
-    Fs = int(max(8, min(F, 150.0 / (total_iters * per_bin_iter))))
-    r = oracle.run_engine(np.ascontiguousarray(x[:Fs]), c["sizes"], sub(Fs), total_iters)
-    timed = r["wall_seconds"][args.warmup:]
-    total = float(np.sum(timed))
-    value = Fs * T * args.steps / total
-    sample = (f"oracle/ C restatement of engine.cpp (reference needs Eigen3, unbuildable here) on the first "
-              f"{Fs} of {F} bins x {T} frames per step, OpenMP over bins")
+    threads = host_cpu()["nproc"]
+    budget = 120.0
+    r = cpu_protocol_subprocess(args.workload, threads, args.steps, args.warmup, budget)
+    value = r["value"]
+    if "batch" in c:  # config 4: mixtures are independent; one mixture's rate is the per-mixture rate
+        r["sample"] += " (config 4: one mixture; the batch rate is the same per TF-bin)"
     return {
         "metric": f"dFastMNMF EM TF-bin*iter/s (BASELINE {args.workload})", "value": value,
         "unit": "TF-bin*iter/s", "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "ms_per_step": 1e3 * r["seconds_per_iter_sample"], "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, **{k: c[k] for k in ("F", "T", "sizes", "N", "K")}},
-        "cpu_baseline": {"value": value, "unit": "TF-bin*iter/s", "cores": threads, "kind": "port",
-                         "sample": sample},
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded STFT-domain mixture, BASELINE config generator)",
+        "config": bench_config(args.workload, world),
+        "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "mean", "se", "repeats",
+                                            "host")},
         "e2e": {"value": value, "unit": "TF-bin*iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "iter_per_s_full_config": value / (F * T),
+        "iter_per_s_full_config": value / (c["F"] * c["T"]),
     }
 
 
@@ -292,7 +339,7 @@ def run_batch(args, c, world, rank, local):
         e.set_model(init.nmf, init.w0, init.lambda0)
         dfm._capi.check(lib.dfm_prime(e.ctx))
         engines.append(e)
-        xs.append(torch.from_numpy(x).pin_memory().numpy())
+        xs.append(x)  # the caller's own pageable arrays
         inits.append(init)
     arr = (ctypes.c_void_p * len(engines))(*[e.ctx for e in engines])
 
@@ -358,9 +405,9 @@ def run_batch(args, c, world, rank, local):
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded STFT-domain mixtures, BASELINE config generator, one seed per mixture)",
-        "config": {"workload": args.workload, "mixtures": nb, "F": F, "T": T, "sizes": c["sizes"], "N": N, "K": K,
-                   "l2": f"working set of {len(engines)} contexts (~131 MB each) exceeds L2 (no flush)",
-                   "parallelism": f"mixtures sharded x{world}" if world > 1 else "1 GPU, one stream per mixture"},
+        "config": bench_config(args.workload, world),
+        "l2": f"working set of {len(engines)} contexts (~131 MB each) exceeds L2 (no flush)",
+        "parallelism": f"mixtures sharded x{world}" if world > 1 else "1 GPU, one stream per mixture",
         "iter_per_s": 1e3 / ms_step,
         "roofline": {"bound": "hbm", "achieved": ab / (ms_step * 1e-3) / 1e9, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": ab / (ms_step * 1e-3) / 1e9 / pk["hbm_gbs"], "traffic": None,
@@ -371,20 +418,23 @@ def run_batch(args, c, world, rank, local):
                           "peak_source": "measured in this run (DFMA microbenchmark, dfm_probe_fp64_tflops)"},
         "e2e": {"value": nb * F * T * args.e2e_iters / e2e_dt, "unit": "TF-bin*iter/s",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-                "step": f"set_obs/set_model of every mixture (pinned host X + init H2D), fit_many({args.e2e_iters}), "
+                "step": f"set_obs/set_model of every mixture (pageable host X + init H2D), fit_many({args.e2e_iters}), "
                         "get_model of every mixture; best of 2", "seconds_per_step": e2e_dt},
         "gpu_launches": int(launches),
         "clocks": clocks,
     }
     if not args.no_cpu_baseline:
-        init_d = dict(T=inits[0].nmf.T, V=inits[0].nmf.V, lam=inits[0].lambda0, w=inits[0].w0)
-        line["cpu_baseline"] = cpu_baseline(c, xs[0], init_d, threads=1)
+        line["cpu_baseline"] = cpu_protocol_subprocess(args.workload, 1, 15, 1, 20.0)
     for e in engines:
         e.close()
     return line
 
 
 def main():
+    if len(sys.argv) == 3 and sys.argv[1] == "--cpu-worker":  # cpu_protocol_subprocess
+        spec = json.loads(sys.argv[2])
+        print(json.dumps(cpu_protocol(**spec)), flush=True)
+        return
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
@@ -496,7 +546,8 @@ def main():
     # ---------------------------------------------------------------- e2e
     # one user call through the public API per e2e step: pinned host X +
     # init in (H2D), e2e_iters EM sweeps, cost trace + fitted model out (D2H)
-    xs = torch.from_numpy(np.ascontiguousarray(x[f0:f1])).pin_memory().numpy()
+    # the caller's own (pageable) numpy array, as a user passes it
+    xs = np.ascontiguousarray(x[f0:f1])
     h2d = xs.nbytes + (init.nmf.T.nbytes + init.nmf.V.nbytes + init.lambda0.nbytes
                        + sum(w.nbytes for w in init.w0)) * (f1 - f0) // F
     e2e_times = []
@@ -573,10 +624,10 @@ def main():
         "value": value, "unit": "TF-bin*iter/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded STFT-domain mixture, BASELINE config generator)",
-        "config": {"workload": args.workload, "F": F, "T": T, "sizes": c["sizes"], "N": N, "K": K,
-                   "l2": "flushed before every timed step (384 MB write, untimed)",
-                   "parallelism": f"freq-shard x{world}" if world > 1 else "1 GPU",
-                   "tiling": eng.tiling()},
+        "config": bench_config(args.workload, world),
+        "l2": "flushed before every timed step (384 MB write, untimed)",
+        "parallelism": f"freq-shard x{world}" if world > 1 else "1 GPU",
+        "tiling": eng.tiling(),
         "iter_per_s": 1e3 / ms_step,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / pk["hbm_gbs"], "traffic": traffic, "kernel": "k_em_bin",
@@ -593,7 +644,7 @@ def main():
         "stft": stft,
         "e2e": {"value": e2e_value, "unit": "TF-bin*iter/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h),
-                "step": f"Engine.set_obs/set_model (pinned host X + init H2D), Engine.fit({args.e2e_iters}) "
+                "step": f"Engine.set_obs/set_model (pageable host X + init H2D), Engine.fit({args.e2e_iters}) "
                         "(cost trace D2H), Engine.get_model (model D2H); best of 3",
                 "seconds_per_step": e2e_dt},
         "gpu_launches": int(launches),
@@ -603,10 +654,10 @@ def main():
     if world == 1 and not args.no_init:
         line["init_pipeline"] = init_measurement(c, x, local, cpu_sample=not args.no_cpu_baseline)
     if world == 1 and not args.no_cpu_baseline:
-        init_d = dict(T=init.nmf.T, V=init.nmf.V, lam=init.lambda0, w=init.w0)
-        line["cpu_baseline"] = cpu_baseline(c, x, init_d, threads=1)
-        mt = os.cpu_count() or 1
-        line["cpu_baseline_all_cores"] = cpu_baseline(c, x, init_d, threads=mt)
+        # the same protocol and sample as the reference arm: 1 thread (the
+        # reference's and the paper's protocol) and every host core
+        line["cpu_baseline"] = cpu_protocol_subprocess(args.workload, 1, 15, 1, 20.0)
+        line["cpu_baseline_all_cores"] = cpu_protocol_subprocess(args.workload, host_cpu()["nproc"], 15, 1, 20.0)
     print(json.dumps(line), flush=True)
     eng.close()
     if pg:

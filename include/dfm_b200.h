@@ -128,8 +128,13 @@ int dfm_shard_end(dfm_ctx* ctx, double* cost_trace_local);
 /* Runs `iters` EM sweeps on the device-resident state (engine.cpp:197-272).
  * cost_trace: iters+1 entries (initial cost first, FitReport::cost_trace);
  * wall_seconds: iters per-iteration device times (may be NULL);
- * stage_seconds[4] = {w_update, mm_update, eta, decorrelate} (may be NULL;
- * the fused kernels report the whole iteration under w_update).  Returns the number of IP
+ * stage_seconds[4] = {w_update, mm_update, eta, decorrelate} (may be NULL):
+ * device time per stage (engine.cpp:210-251).  The fused kernels overlap the
+ * reference's stages, so each launch's wall (first CTA start to last CTA
+ * end) is attributed: the bin kernel by its CTAs' phase times (Lambda update
+ * -> mm_update; eta/cost/Q_mu and the IP sweep -> w_update; P and the
+ * T-update weights -> decorrelate), the T and V updates -> mm_update, the
+ * V-update weights -> eta.  Returns the number of IP
  * pinv fallbacks (>= 0) or an error code.
  * With a communicator the cost entries are the GLOBAL cost (allreduced). */
 int dfm_fit(dfm_ctx* ctx, int iters, double* cost_trace, double* wall_seconds,

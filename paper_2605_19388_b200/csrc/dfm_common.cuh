@@ -17,6 +17,18 @@
 
 namespace dfm {
 
+// Acceptance of the fast IP paths (ip_sweep_quad / ip_sweep_fast /
+// ip_sweep_warp).  The reference decides LU-or-pinv per column on
+// ||S u_LU - e_mu|| <= 1e-6 (engine.cpp:47-49).  The fast paths solve the
+// same system in another form (Q_mu^-1 W^-H e_mu), whose residual can differ
+// from the LU one by a small factor near the threshold.  A fast sweep is
+// therefore kept only when every column's residual is below 1e-8, a guard
+// band two orders of magnitude under the reference's threshold; anything
+// above reruns the exact sweep, which applies the reference's own LU
+// predicate.  Well-conditioned systems sit at ~1e-15 and never reach the band.
+constexpr double kFastResid = 1e-8;
+constexpr double kFastResid2 = kFastResid * kFastResid;
+
 struct cd {
   double re, im;
 };
@@ -542,7 +554,7 @@ __device__ bool ip_sweep_warp(int mb, cd* W, const cd* qb, const cd* qi, double 
   if (act) {
     double r2 = 0.0;
     for (int a = 0; a < mb; ++a) r2 += res[lane * mb + a];
-    bad |= !(r2 <= 1e-12);
+    bad |= !(r2 <= kFastResid2);  // guard band under the reference's 1e-6 (see kFastResid)
   }
   if (__any_sync(0xffffffffu, bad)) {
     for (int i = lane; i < n2; i += 32) W[i] = s.S0[i];

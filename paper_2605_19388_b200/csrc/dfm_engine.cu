@@ -99,6 +99,7 @@ struct dfm_ctx {
   DBuf<double> Tf, V, lam, H, Aw, Bw, P, numden, cost_part, cost_sum, cost_step;
   DBuf<cd> Ginv;  // (W^H)^-1 per (bin, block) for the Wiener filter
   DBuf<int> fallbacks;
+  DBuf<StageClock> stage;  // device StageSeconds accumulator (dfm_em.cuh)
   int maxmb = 4;
   int kmaxmb = 4;  // MAXMB of the selected instantiations
   void (*kem)(EmArgs) = nullptr;
@@ -164,7 +165,15 @@ EmArgs make_args(dfm_ctx* c) {
   a.Bw = c->Bw.p;
   a.P = c->P.p;
   a.fallbacks = c->fallbacks.p;
+  a.sc = c->stage.p;
   return a;
+}
+
+void reset_stage_clock(dfm_ctx* c) {
+  StageClock h;
+  std::memset(&h, 0, sizeof(h));
+  for (auto& t : h.t0) t = ~0ull;
+  c->stage.upload(&h, 1, c->stream);
 }
 
 size_t em_smem(const EmArgs& a, int FT, int kmaxmb) {
@@ -302,7 +311,7 @@ void launch_tupd(dfm_ctx* c) {
   }
   // h' = T_new V fused into the T update
   kern<<<grid, 32 * kTupdWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->V.p, c->Aw.p, c->Bw.p, c->floor_,
-                                                nullptr, c->H.p, nullptr);
+                                                nullptr, c->H.p, nullptr, c->stage.p);
   DFM_CK_LAUNCH();
   c->launches++;
 }
@@ -315,6 +324,19 @@ void launch_pd(dfm_ctx* c) {
   c->kpdw<<<grid, c->TB, 0, c->stream>>>(a);
   DFM_CK_LAUNCH();
   c->launches++;
+}
+
+// The sharded path's second stream and fork/join events, and the NCCL entry
+// points: created before any stream capture (step_graph), so nothing that can
+// throw runs while the stream is capturing.
+void ensure_comm_resources(dfm_ctx* c) {
+  if (!collective(c)) return;
+  (void)nccl();
+  if (!c->comm_stream) {
+    DFM_CK(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    for (auto& e : c->ev_chunk) DFM_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    DFM_CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  }
 }
 
 void launch_vupd(dfm_ctx* c) {
@@ -330,7 +352,8 @@ void launch_vupd(dfm_ctx* c) {
   if (!sharded || c->host_exchange) {
     kern<<<grid, 32 * kVupdMWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->Aw.p, c->Bw.p, c->V.p,
                                                    sharded ? c->numden.p : nullptr, c->floor_, nullptr,
-                                                   sharded ? nullptr : c->H.p, nullptr, 0);  // H = T V_new fused
+                                                   sharded ? nullptr : c->H.p, nullptr, 0,
+                                                   c->stage.p);  // H = T V_new fused
     DFM_CK_LAUNCH();
     c->launches++;
     return;
@@ -344,16 +367,13 @@ void launch_vupd(dfm_ctx* c) {
     return e ? std::max(1, std::min(kVupdChunks, atoi(e))) : kVupdChunks;
   }();
   const int nch = std::min(env_ch, c->N);
-  if (!c->comm_stream) {
-    DFM_CK(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
-    for (auto& e : c->ev_chunk) DFM_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    DFM_CK(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
-  }
+  ensure_comm_resources(c);
   for (int j = 0; j < nch; ++j) {
     const int n0 = c->N * j / nch, n1 = c->N * (j + 1) / nch;
     const dim3 gj((c->T + 7) / 8, n1 - n0);
     kern<<<gj, 32 * kVupdMWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->Aw.p, c->Bw.p, c->V.p,
-                                                 c->numden.p, c->floor_, nullptr, nullptr, nullptr, n0);
+                                                 c->numden.p, c->floor_, nullptr, nullptr, nullptr, n0,
+                                                 c->stage.p);
     DFM_CK_LAUNCH();
     c->launches++;
     DFM_CK(cudaEventRecord(c->ev_chunk[j], c->stream));
@@ -402,16 +422,32 @@ bool step_graph(dfm_ctx* c) {
   if (!c->use_graph || c->host_exchange) return false;
   if (c->step_exec) return true;
   if (c->cost_step.n < (size_t)c->F) c->cost_step.alloc(c->F);
+  ensure_comm_resources(c);  // everything that can throw, before the capture
   cudaGraph_t g = nullptr;
   DFM_CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   const long long l0 = c->launches;
-  launch_em(c, 2, 1, 0, c->cost_step.p);
-  launch_rest(c, nullptr);
-  DFM_CK(cudaStreamEndCapture(c->stream, &g));
+  try {
+    launch_em(c, 2, 1, 0, c->cost_step.p);
+    launch_rest(c, nullptr);
+  } catch (...) {
+    // leave the stream usable: end the capture and drop the partial graph
+    cudaGraph_t partial = nullptr;
+    cudaStreamEndCapture(c->stream, &partial);
+    if (partial) cudaGraphDestroy(partial);
+    cudaGetLastError();
+    c->launches = l0;
+    throw;
+  }
+  const cudaError_t ec = cudaStreamEndCapture(c->stream, &g);
   c->graph_launches = c->launches - l0;
   c->launches = l0;  // capture does not launch
-  DFM_CK(cudaGraphInstantiate(&c->step_exec, g, 0));
+  if (ec != cudaSuccess) {
+    if (g) cudaGraphDestroy(g);
+    DFM_CK(ec);
+  }
+  const cudaError_t ei = cudaGraphInstantiate(&c->step_exec, g, 0);
   cudaGraphDestroy(g);
+  DFM_CK(ei);
   return true;
 }
 
@@ -514,6 +550,8 @@ dfm_ctx* dfm_create(int F, int T, int nblocks, const int* block_sizes, int N, in
     c->numden.alloc(2 * (size_t)N * K * T);
     c->fallbacks.alloc(1);
     DFM_CK(cudaMemset(c->fallbacks.p, 0, sizeof(int)));
+    c->stage.alloc(1);
+    reset_stage_clock(c);
     if (!choose_tiling(c)) throw CudaError{DFM_ERR_UNSUPPORTED};
     set_kernel_attrs(c);
     ensure_cost(c, 2);
@@ -703,6 +741,7 @@ void fit_begin(dfm_ctx* c, int iters) {
   DFM_CK(cudaSetDevice(c->device));
   ensure_cost(c, iters + 1);
   DFM_CK(cudaMemsetAsync(c->fallbacks.p, 0, sizeof(int), c->stream));
+  reset_stage_clock(c);
   while ((int)c->iter_ev.size() < iters + 2) {
     cudaEvent_t e;
     DFM_CK(cudaEventCreate(&e));
@@ -730,6 +769,8 @@ int fit_end(dfm_ctx* c, int iters, double* cost_trace, double* wall_seconds, dou
   c->cost_part.download(part.data(), part.size(), c->stream);
   int fb = 0;
   c->fallbacks.download(&fb, 1, c->stream);
+  StageClock sc;
+  c->stage.download(&sc, 1, c->stream);
   DFM_CK(cudaStreamSynchronize(c->stream));
   std::vector<double> cost(iters + 1, 0.0);
   for (int i = 0; i <= iters; ++i)
@@ -751,10 +792,11 @@ int fit_end(dfm_ctx* c, int iters, double* cost_trace, double* wall_seconds, dou
     if (wall_seconds) wall_seconds[i] = ms * 1e-3;
     total_ms += ms;
   }
-  if (stage_seconds) {
-    stage_seconds[0] = total_ms * 1e-3;
-    stage_seconds[1] = stage_seconds[2] = stage_seconds[3] = 0.0;
-  }
+  // per-stage device time (dfm_em.cuh StageClock): the launches' walls
+  // attributed to {w_update, mm_update, eta, decorrelate}
+  if (stage_seconds)
+    for (int k = 0; k < 4; ++k) stage_seconds[k] = sc.acc[k];
+  (void)total_ms;
   return fb;
 }
 }  // namespace

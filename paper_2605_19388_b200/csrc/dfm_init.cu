@@ -767,7 +767,7 @@ int is_nmf_dev(const double* h0_dev, int F, int T, int N, int K, int max_iters, 
     // rec = T_new V fused (skipped with the update for converged sources,
     // whose rec is unchanged)
     kern<<<dim3((F + 7) / 8, N), 32 * kTupdWarps, 0, s>>>(F, T, N, K, Tf.p, V.p, Aw.p, Bw.p, kEpsNmf, done.p,
-                                                          H.p, tgt.p);
+                                                          H.p, tgt.p, nullptr);
     DFM_CK_LAUNCH();
   };
   auto vupd = [&]() {
@@ -779,7 +779,7 @@ int is_nmf_dev(const double* h0_dev, int F, int T, int N, int K, int max_iters, 
       default: kern = k_vupd_mma<8>; break;
     }
     kern<<<dim3((T + 7) / 8, N), 32 * kVupdMWarps, 0, s>>>(F, T, N, K, Tf.p, Aw.p, Bw.p, V.p, nullptr, kEpsNmf,
-                                                         done.p, H.p, tgt.p, 0);
+                                                         done.p, H.p, tgt.p, 0, nullptr);
     DFM_CK_LAUNCH();
   };
   spec();
@@ -794,11 +794,20 @@ int is_nmf_dev(const double* h0_dev, int F, int T, int N, int K, int max_iters, 
     // the next iteration), so only the first iteration's come from k_is_weights
     weights();
     DFM_CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    tupd();  // -> weights of rec = T_new V
-    vupd();  // -> rec = T V_new and its weights
-    divergence(0);
+    try {
+      tupd();  // -> weights of rec = T_new V
+      vupd();  // -> rec = T V_new and its weights
+      divergence(0);
+    } catch (...) {  // end the capture so the stream stays usable
+      cudaStreamEndCapture(s, &g);
+      if (g) cudaGraphDestroy(g);
+      cudaGetLastError();
+      throw;
+    }
     DFM_CK(cudaStreamEndCapture(s, &g));
-    DFM_CK(cudaGraphInstantiate(&ge, g, 0));
+    const cudaError_t ei = cudaGraphInstantiate(&ge, g, 0);
+    if (ei != cudaSuccess) cudaGraphDestroy(g);
+    DFM_CK(ei);
   }
   std::vector<int> dn(N);
   int it = 0;

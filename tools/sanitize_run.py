@@ -39,3 +39,15 @@ with dfm.Engine(7, 100, l3, 5, 16) as e3:
     e3.set_model(i3.nmf, i3.w0, i3.lambda0)
     e3.fit(3)
     e3.wiener()
+# the 2 x 2-mic static shape (config 0: <2, 2, 3, 2>) and the 8 x 4-mic one
+# (config 3: <4, 8, 8, 4>, the instantiation whose frame-major tile trapped)
+for sizes_s, N_s, K_s, F_s, T_s in (([2, 2], 3, 4, 9, 70), ([4] * 8, 8, 32, 5, 300)):
+    l_s = dfm.BlockLayout(sizes_s)
+    x_s = dfm.generate_mixture(1, F_s, T_s, l_s.total, N_s, K_s, 10)
+    i_s = dfm.random_init(F_s, T_s, l_s, N_s, K_s, 11)
+    with dfm.Engine(F_s, T_s, l_s, N_s, K_s) as e_s:
+        e_s.set_obs(x_s)
+        e_s.set_model(i_s.nmf, i_s.w0, i_s.lambda0)
+        e_s.fit(3)
+        e_s.wiener()
+print("sanitize run ok (static shapes 2x2, 8x4, 1x12)")
