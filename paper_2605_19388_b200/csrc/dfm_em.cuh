@@ -20,21 +20,23 @@ namespace dfm {
 // ---------------------------------------------------------------------------
 // StageSeconds on the device (engine.cpp:210-251 fills {w_update, mm_update,
 // eta, decorrelate} per iteration).  The iteration's kernels overlap the
-// reference's stages, so each kernel launch is timed from its first CTA's
-// start to its last CTA's end (%globaltimer; the last CTA is found with a
-// ticket counter) and that wall time is attributed to stages: k_tupd and
-// k_vupd -> mm_update, k_pdw -> eta (eta' and the V-update weights), and
-// k_em_bin split by its CTAs' summed phase times: pass A (Lambda update) ->
+// reference's stages, so device time is attributed per launch: the first CTA
+// of every instrumented launch stamps %globaltimer on entry, and the time
+// from one launch's stamp to the next one's (the launch plus the gap after
+// it) goes to that launch's stage: k_tupd and k_vupd -> mm_update, k_pdw ->
+// eta (eta' and the V-update weights), k_em_bin split by its first CTA's
+// phase times (every bin does the same work): pass A (Lambda update) ->
 // mm_update, pass B (eta, cost, Q_mu) and the IP sweep -> w_update, pass C
-// (P = |W^H x|^2 and the T-update weights) -> decorrelate.  The accumulator
-// is read once per fit (dfm_fit).  Cost: a few atomics per CTA.
+// (P = |W^H x|^2 and the T-update weights) -> decorrelate.  One plain store
+// per launch, no atomics; k_stage_close ends the last launch of a fit.
 enum { kStW = 0, kStMM = 1, kStEta = 2, kStDec = 3 };
-enum { kScBin = 0, kScTupd = 1, kScPdw = 2, kScVupd = 3, kScKernels = 4 };
+enum { kScNone = -1, kScBin = 0, kScTupd = 1, kScPdw = 2, kScVupd = 3 };
 constexpr int kScPhases = 4;
 struct StageClock {
-  unsigned long long t0[kScKernels];  // earliest CTA start of the running launch (~0 when idle)
-  unsigned int done[kScKernels];      // CTAs finished in the running launch
-  unsigned long long ph[kScKernels][kScPhases];  // summed CTA time per phase (ns)
+  unsigned long long prev_t;          // entry stamp of the previous instrumented launch (0: none)
+  int prev_kind;                      // its kind (kSc*)
+  int pad;
+  unsigned long long em_ph[kScPhases];  // k_em_bin's first CTA: time per phase (ns)
   double acc[4];                      // seconds per stage since the last reset
 };
 
@@ -43,36 +45,28 @@ __device__ __forceinline__ unsigned long long gtimer() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-__device__ __forceinline__ void sc_begin(StageClock* sc, int k) {
-  if (sc && threadIdx.x == 0) atomicMin(&sc->t0[k], gtimer());
-}
-// Thread 0 of every CTA, once, after the CTA's work.  phase_ns: this CTA's
-// time per phase (nullptr: the whole launch goes to `stage`).
-__device__ inline void sc_end(StageClock* sc, int k, int stage, const unsigned long long* phase_ns = nullptr,
-                              const int* phase_stage = nullptr) {
-  if (!sc || threadIdx.x != 0) return;
-  if (phase_ns)
-    for (int p = 0; p < kScPhases; ++p)
-      if (phase_ns[p]) atomicAdd(&sc->ph[k][p], phase_ns[p]);
-  __threadfence();
-  const unsigned total = gridDim.x * gridDim.y * gridDim.z;
-  if (atomicAdd(&sc->done[k], 1u) != total - 1) return;
-  __threadfence();
-  const double wall = (double)(gtimer() - *(volatile unsigned long long*)&sc->t0[k]) * 1e-9;
-  if (phase_ns) {
-    double sum = 0.0;
-    for (int p = 0; p < kScPhases; ++p) sum += (double)*(volatile unsigned long long*)&sc->ph[k][p];
-    for (int p = 0; p < kScPhases; ++p) {
-      const double share = sum > 0.0 ? (double)*(volatile unsigned long long*)&sc->ph[k][p] / sum : 0.0;
-      sc->acc[phase_stage[p]] += wall * share;
-      sc->ph[k][p] = 0ull;
+// First CTA, thread 0: close the previous launch's interval, open this one's.
+__device__ inline void sc_tick(StageClock* sc, int kind) {
+  if (!sc || threadIdx.x != 0 || blockIdx.x != 0 || blockIdx.y != 0 || blockIdx.z != 0) return;
+  const unsigned long long now = gtimer();
+  if (sc->prev_t && now > sc->prev_t) {
+    const double dt = (double)(now - sc->prev_t) * 1e-9;
+    switch (sc->prev_kind) {
+      case kScBin: {
+        const int stage_of[kScPhases] = {kStMM, kStW, kStW, kStDec};
+        double sum = 0.0;
+        for (int p = 0; p < kScPhases; ++p) sum += (double)sc->em_ph[p];
+        for (int p = 0; p < kScPhases; ++p)
+          sc->acc[stage_of[p]] += sum > 0.0 ? dt * (double)sc->em_ph[p] / sum : (p == 1 ? dt : 0.0);
+        break;
+      }
+      case kScTupd: case kScVupd: sc->acc[kStMM] += dt; break;
+      case kScPdw: sc->acc[kStEta] += dt; break;
+      default: break;
     }
-  } else {
-    sc->acc[stage] += wall;
   }
-  sc->t0[k] = ~0ull;
-  __threadfence();
-  sc->done[k] = 0u;
+  sc->prev_t = kind == kScNone ? 0ull : now;
+  sc->prev_kind = kind;
 }
 
 struct EmArgs {
@@ -182,26 +176,21 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   const unsigned long long pol_keep = l2_evict_last(), pol_last = l2_evict_first();
   const double* Hf = a.H + (size_t)f * N * T;
   em_stamp(a, 0);
-  // StageSeconds: thread 0's phase boundaries (shared memory, not registers)
+  // StageSeconds: the first CTA's phase boundaries (thread 0, shared memory)
   __shared__ unsigned long long sc_ts[4];
+  const bool sc_on = a.sc && f == 0;
   auto sc_mark = [&](int i) {
-    if (a.sc && tid == 0) sc_ts[i] = gtimer();
+    if (sc_on && tid == 0) sc_ts[i] = gtimer();
   };
-  sc_begin(a.sc, kScBin);
+  sc_tick(a.sc, kScBin);
   sc_mark(0);
-  auto sc_finish = [&]() {  // thread 0; phases A, B, IP, C
-    if (!a.sc || tid != 0) return;
+  auto sc_finish = [&]() {  // thread 0 of bin 0: phases A, B, IP, C
+    if (!sc_on || tid != 0) return;
     const unsigned long long now = gtimer();
-    unsigned long long ph[kScPhases] = {sc_ts[1] - sc_ts[0], 0, 0, 0};
-    const int stage_of[kScPhases] = {kStMM, kStW, kStW, kStDec};
-    if (a.start) {
-      ph[1] = sc_ts[2] - sc_ts[1];
-      ph[2] = sc_ts[3] - sc_ts[2];
-      ph[3] = now - sc_ts[3];
-    } else {
-      ph[1] = now - sc_ts[1];
-    }
-    sc_end(a.sc, kScBin, kStW, ph, stage_of);
+    a.sc->em_ph[0] = sc_ts[1] - sc_ts[0];
+    a.sc->em_ph[1] = (a.start ? sc_ts[2] : now) - sc_ts[1];
+    a.sc->em_ph[2] = a.start ? sc_ts[3] - sc_ts[2] : 0ull;
+    a.sc->em_ph[3] = a.start ? now - sc_ts[3] : 0ull;
   };
 
   // Lambda of the bin, and its transpose [m][NP] for the per-frame products
@@ -916,7 +905,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
         }
   }
   em_stamp(a, 5);
-  if (a.sc) {
+  if (sc_on) {
     __syncthreads();
     sc_finish();
   }
@@ -1109,7 +1098,7 @@ __global__ void __launch_bounds__(32 * kTupdWarps, KT <= 2 ? 3 : 2) k_tupd_mma(i
                                                              const double* __restrict__ tgt = nullptr,
                                                              StageClock* sc = nullptr) {
   __shared__ double part[kTupdWarps / 2][2][KT][64];
-  sc_begin(sc, kScTupd);
+  sc_tick(sc, kScTupd);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
   const int n = blockIdx.y, f0 = blockIdx.x * 8;
@@ -1184,18 +1173,11 @@ __global__ void __launch_bounds__(32 * kTupdWarps, KT <= 2 ? 3 : 2) k_tupd_mma(i
           *tp = fmax(*tp * sqrt(nu / fmax(de, floor_)), floor_);
         }
   }
-  if (!Hout) {
-    sc_end(sc, kScTupd, kStMM);
-    return;
-  }
+  if (!Hout) return;
   __syncthreads();  // the CTA's new T rows are visible
   // h' = T_new V (IS-NMF: the weights of rec = T_new V instead)
   spec_rows<2 * KT>(F, T, N, K, n, f0, Tf, V, Hout, warp, kTupdWarps, lane, tgt, floor_, const_cast<double*>(Aw),
                     const_cast<double*>(Bw));
-  if (sc) {
-    __syncthreads();
-    sc_end(sc, kScTupd, kStMM);
-  }
 }
 
 // V update (engine.cpp:125-133): num[k][t] = sum_f T[f][n][k] A'[n][f][t].
@@ -1213,7 +1195,7 @@ __global__ void __launch_bounds__(32 * kVupdMWarps, KT <= 2 ? 3 : 2) k_vupd_mma(
                                                               const double* __restrict__ tgt = nullptr,
                                                               int n_base = 0, StageClock* sc = nullptr) {
   __shared__ double part[kVupdMWarps / 2][2][KT][64];
-  sc_begin(sc, kScVupd);
+  sc_tick(sc, kScVupd);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
   const int n = n_base + blockIdx.y, t0 = blockIdx.x * 8;  // n_base: source chunk (sharded overlap)
@@ -1291,18 +1273,11 @@ __global__ void __launch_bounds__(32 * kVupdMWarps, KT <= 2 ? 3 : 2) k_vupd_mma(
           }
         }
   }
-  if (!Hout || numden) {  // sharded: V is final only after the allreduce
-    sc_end(sc, kScVupd, kStMM);
-    return;
-  }
+  if (!Hout || numden) return;  // sharded: V is final only after the allreduce
   __syncthreads();  // the CTA's new V columns are visible
   // H = T V_new (IS-NMF: and the next iteration's weights)
   spec_cols<2 * KT>(F, T, N, K, n, t0, Tf, V, Hout, warp, kVupdMWarps, lane, tgt, floor_, const_cast<double*>(Aw),
                     const_cast<double*>(Bw));
-  if (sc) {
-    __syncthreads();
-    sc_end(sc, kScVupd, kStMM);
-  }
 }
 
 // Pass D as an elementwise kernel over (bin, frame): h' from H (= T_new V by
@@ -1319,7 +1294,7 @@ __global__ void __launch_bounds__(128, 6) k_pdw(const EmArgs a) {
   const int T = a.T;
   const int NP = (N + 1) & ~1;
   const int f = blockIdx.y, t = blockIdx.x * blockDim.x + threadIdx.x;
-  sc_begin(a.sc, kScPdw);
+  sc_tick(a.sc, kScPdw);
   const double* Lg = a.lam + (size_t)f * N * M;
   const bool smemL = M * NP <= kMaxN * 64;
   if (smemL)
@@ -1403,8 +1378,10 @@ __global__ void __launch_bounds__(128, 6) k_pdw(const EmArgs a) {
       a.Aw[o] = A[n];
       a.Bw[o] = B[n];
     }
-  sc_end(a.sc, kScPdw, kStEta);  // thread 0 (t < T always holds for it)
 }
+
+// Closes the last instrumented launch of a fit (StageClock).
+static __global__ void k_stage_close(StageClock* sc) { sc_tick(sc, kScNone); }
 
 }  // namespace dfm
 

@@ -172,7 +172,7 @@ EmArgs make_args(dfm_ctx* c) {
 void reset_stage_clock(dfm_ctx* c) {
   StageClock h;
   std::memset(&h, 0, sizeof(h));
-  for (auto& t : h.t0) t = ~0ull;
+  h.prev_kind = kScNone;
   c->stage.upload(&h, 1, c->stream);
 }
 
@@ -760,7 +760,11 @@ void fit_launch(dfm_ctx* c, int i, int iters) {
     DFM_CK(cudaMemcpyAsync(c->cost_part.p + (size_t)i * c->F, c->cost_step.p, sizeof(double) * c->F,
                            cudaMemcpyDeviceToDevice, c->stream));
   }
-  if (i == iters) DFM_CK(cudaEventRecord(c->iter_ev[iters + 1], c->stream));
+  if (i == iters) {
+    k_stage_close<<<1, 1, 0, c->stream>>>(c->stage.p);  // ends the last launch's StageClock interval
+    DFM_CK_LAUNCH();
+    DFM_CK(cudaEventRecord(c->iter_ev[iters + 1], c->stream));
+  }
 }
 
 int fit_end(dfm_ctx* c, int iters, double* cost_trace, double* wall_seconds, double* stage_seconds) {

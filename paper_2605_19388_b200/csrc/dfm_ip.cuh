@@ -122,20 +122,28 @@ __device__ int ip_solve_thread(cd* W, const cd* qb, double floor_, IpScratch<MB>
     cd qu[MB];
     double r2 = 0.0;
     if (fin) {
+      // the reference's residual ||S u - e_mu|| with S = W^H Q formed first
+      // (engine.cpp:46-49); S is re-formed entry by entry, bitwise the S
+      // that was factorised
+#pragma unroll
+      for (int a = 0; a < MB; ++a) {
+        cd r{0.0, 0.0};
+#pragma unroll
+        for (int c = 0; c < MB; ++c) {
+          cd sac{0.0, 0.0};
+#pragma unroll
+          for (int k = 0; k < MB; ++k) sac = sac + cmulc(W[a * MB + k], Q(k, c));
+          r = r + sac * u[c];
+        }
+        if (a == mu) r.re -= 1.0;
+        r2 += norm2(r);
+      }
 #pragma unroll
       for (int a = 0; a < MB; ++a) {
         cd s{0.0, 0.0};
 #pragma unroll
         for (int c = 0; c < MB; ++c) s = s + Q(a, c) * u[c];
         qu[a] = s;
-      }
-#pragma unroll
-      for (int a = 0; a < MB; ++a) {
-        cd s{0.0, 0.0};
-#pragma unroll
-        for (int k = 0; k < MB; ++k) s = s + cmulc(W[a * MB + k], qu[k]);
-        if (a == mu) s.re -= 1.0;
-        r2 += norm2(s);
       }
     }
     if (!fin || sqrt(r2) > 1e-6) {
