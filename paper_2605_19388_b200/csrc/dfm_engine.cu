@@ -311,7 +311,7 @@ void launch_tupd(dfm_ctx* c) {
   }
   // h' = T_new V fused into the T update
   kern<<<grid, 32 * kTupdWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->V.p, c->Aw.p, c->Bw.p, c->floor_,
-                                                nullptr, c->H.p, nullptr, c->stage.p);
+                                                nullptr, (c->dbg & 4) ? nullptr : c->H.p, nullptr, c->stage.p);
   DFM_CK_LAUNCH();
   c->launches++;
 }
@@ -352,7 +352,7 @@ void launch_vupd(dfm_ctx* c) {
   if (!sharded || c->host_exchange) {
     kern<<<grid, 32 * kVupdMWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->Aw.p, c->Bw.p, c->V.p,
                                                    sharded ? c->numden.p : nullptr, c->floor_, nullptr,
-                                                   sharded ? nullptr : c->H.p, nullptr, 0,
+                                                   (sharded || (c->dbg & 4)) ? nullptr : c->H.p, nullptr, 0,
                                                    c->stage.p);  // H = T V_new fused
     DFM_CK_LAUNCH();
     c->launches++;

@@ -653,3 +653,4 @@ def test_ip_branch_near_the_residual_threshold(dfm, oracle, sizes, N, K):
     for a, b in zip(fit.spatial.W, ref["w"]):
         for f in np.nonzero(stable)[0]:
             assert _rel(a[f], b[f]) < 1e-7, f"bin {f} (LU residual {res[f]:.1e})"
+
