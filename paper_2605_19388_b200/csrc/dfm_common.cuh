@@ -60,6 +60,19 @@ __host__ __device__ __forceinline__ cd cdiv(cd a, cd b) {
   return cd{(a.im * r + a.re) / d, (a.im - a.re * r) / d};
 }
 __host__ __device__ __forceinline__ bool cfinite(cd a) { return isfinite(a.re) && isfinite(a.im); }
+// Multiply-accumulate forms for the hot loops: four FMAs (two for a real
+// scale) instead of the separate products and sums of s + a * b (the
+// compiler cannot contract those without reassociating).  The rounding
+// differs from the reference's complex product only at the last bit.
+__host__ __device__ __forceinline__ cd cfma(cd s, cd a, cd b) {  // s + a b
+  return cd{fma(-a.im, b.im, fma(a.re, b.re, s.re)), fma(a.im, b.re, fma(a.re, b.im, s.im))};
+}
+__host__ __device__ __forceinline__ cd cfmac(cd s, cd a, cd b) {  // s + conj(a) b
+  return cd{fma(a.im, b.im, fma(a.re, b.re, s.re)), fma(-a.im, b.re, fma(a.re, b.im, s.im))};
+}
+__host__ __device__ __forceinline__ cd rfma(cd s, cd a, double r) {  // s + a r
+  return cd{fma(a.re, r, s.re), fma(a.im, r, s.im)};
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
       for (int mu = 0; mu < MB_; ++mu) {
         cd s{0.0, 0.0};
 #pragma unroll
-        for (int q = 0; q < MB_; ++q) s = s + cmulc(wb[mu * MB_ + q], xv[q]);
+        for (int q = 0; q < MB_; ++q) s = cfmac(s, wb[mu * MB_ + q], xv[q]);
         P[mu] = norm2(s);
       }
     } else {
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
         cd s{0.0, 0.0};
         for (int q = 0; q < mb; ++q) {
           const double2 v = __ldg(reinterpret_cast<const double2*>(xt + off + q));
-          s = s + cmulc(wb[mu * mb + q], cd{v.x, v.y});
+          s = cfmac(s, wb[mu * mb + q], cd{v.x, v.y});
           if (xout && mu == 0) xout[q * xstride] = cd{v.x, v.y};
         }
         P[mu] = norm2(s);
@@ -647,8 +647,8 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
 #pragma unroll
               for (int mu = 0; mu < MBI; mu += 2) {
                 const double2 e = *reinterpret_cast<const double2*>(ef + tt * ISP + mu);
-                qacc[mu] = qacc[mu] + pr * e.x;
-                qacc[mu + 1] = qacc[mu + 1] + pr * e.y;
+                qacc[mu] = rfma(qacc[mu], pr, e.x);
+                qacc[mu + 1] = rfma(qacc[mu + 1], pr, e.y);
               }
             }
           } else
@@ -661,7 +661,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
               pr = xr[tt] * conjg(xc[tt]);
 #pragma unroll
             for (int mu = 0; mu < MAXMB; ++mu)
-              if (mu < mb) qacc[mu] = qacc[mu] + pr * ew[mu * FTp + tt];
+              if (mu < mb) qacc[mu] = rfma(qacc[mu], pr, ew[mu * FTp + tt]);
           }
           cd* dst = qpart + u;
           const int NU = nitems * SQ;
@@ -858,7 +858,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
         for (int mu = 0; mu < MB_; ++mu) {
           cd s{0.0, 0.0};
 #pragma unroll
-          for (int q = 0; q < MB_; ++q) s = s + cmulc(wb[mu * MB_ + q], xv[q]);
+          for (int q = 0; q < MB_; ++q) s = cfmac(s, wb[mu * MB_ + q], xv[q]);
           P[mu] = norm2(s);
         }
       } else {
@@ -1500,6 +1500,43 @@ __device__ __forceinline__ void wh_inverse_regs(const cd* w, cd* g) {
   }
 }
 
+// Staged images leave through the TMA engine: each warp writes its 32
+// frames' rows for source n into a shared-memory stage laid out as 8 groups
+// of 4 frames (4 x M samples contiguous, as in global memory, groups 16 bytes
+// apart so the per-lane row writes hit every bank equally), and the first
+// lane of each group issues one bulk copy of the group (cp.async.bulk
+// shared -> global).  The stage is double-buffered per warp, so the copies of
+// source n drain while source n + 1 is computed.
+__host__ __device__ constexpr size_t wien_group_bytes(int M) { return (size_t)4 * M * 16 + 16; }
+__host__ __device__ constexpr size_t wien_stage_bytes(int M) {  // one warp, one buffer
+  return 8 * wien_group_bytes(M);
+}
+// stage buffers per warp: two (copies of source n drain during source n + 1)
+// up to 16 mics, one above (shared memory would cap the CTAs per SM)
+__host__ __device__ constexpr int wien_nbuf(int M) { return M <= 16 ? 2 : 1; }
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(ssrc));
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(s), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+// (W_b^H)^-1 of every (bin, block) with blocks of <= 4 mics, one thread per
+// system, in registers (wh_inverse_regs: bitwise the result of k_wh_inverse).
+static __global__ void k_wh_inverse_small(int F, Layout L, const cd* __restrict__ W, cd* __restrict__ G) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= F * L.nb) return;
+  const int b = idx % L.nb, f = idx / L.nb;
+  const cd* w = W + (size_t)f * L.wsz + L.woff[b];
+  cd* g = G + (size_t)f * L.wsz + L.woff[b];
+  switch (L.mb[b]) {
+    case 1: wh_inverse_regs<1>(w, g); break;
+    case 2: wh_inverse_regs<2>(w, g); break;
+    case 3: wh_inverse_regs<3>(w, g); break;
+    default: wh_inverse_regs<4>(w, g); break;
+  }
+}
+
 template <int MB_, int NB_, int NS_, int MAXMB>
 __global__ void __launch_bounds__(kWienFT, 4) k_wiener_ctx(const EmArgs a, const cd* __restrict__ G,
                                                         cd* __restrict__ images) {
@@ -1513,23 +1550,22 @@ __global__ void __launch_bounds__(kWienFT, 4) k_wiener_ctx(const EmArgs a, const
   auto MBof = [&](int b) { return SB ? MB_ : a.mb[b]; };
   auto OFF = [&](int b) { return SB ? b * MB_ : a.off[b]; };
   auto WOFF = [&](int b) { return SB ? b * MB_ * MB_ : a.woff[b]; };
-  const int Mp = M + 1;          // padded stage row: conflict-free 16-byte rows
-  cd* Ws = (cd*)swn;             // [wsz]
-  cd* Gs = Ws + wsz;             // [wsz]
-  cd* stage = Gs + wsz;          // [FT][M + 1]
-  double* Ls = (double*)(stage + (size_t)kWienFT * Mp);  // [N][M]
   const int f = blockIdx.y, t0 = blockIdx.x * kWienFT, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const size_t gbytes = wien_group_bytes(M), wbytes = wien_stage_bytes(M);
+  const int nbuf = wien_nbuf(M);
+  unsigned char* stage0 = swn;                                   // [warp][nbuf][8 groups]
+  cd* Ws = (cd*)(swn + (size_t)(kWienFT / 32) * nbuf * wbytes);  // [wsz]
+  cd* Gs = Ws + wsz;                                             // [wsz]
+  double* Ls = (double*)(Gs + wsz);                              // [N][M]
   const int tn = min(kWienFT, T - t0);
   for (int e = tid; e < wsz; e += kWienFT) Ws[e] = a.W[(size_t)f * wsz + e];
-  constexpr bool GREG = SB && MB_ <= 4;  // (W^H)^-1 per CTA in registers, else precomputed
-  if (!GREG)
-    for (int e = tid; e < wsz; e += kWienFT) Gs[e] = G[(size_t)f * wsz + e];
+  // (W_b^H)^-1, precomputed once per (bin, block) by launch_wh_inverse
+  // (every frame tile of a bin used to repeat the serial inverse while its
+  // other threads waited at the barrier)
+  for (int e = tid; e < wsz; e += kWienFT) Gs[e] = G[(size_t)f * wsz + e];
   for (int e = tid; e < N * M; e += kWienFT) Ls[e] = a.lam[(size_t)f * N * M + e];
   __syncthreads();
-  if constexpr (GREG) {  // (W_b^H)^-1 of this bin's blocks, one thread each (wiener.cpp:25)
-    if (tid < NB_) wh_inverse_regs<MB_ <= 4 ? MB_ : 1>(Ws + tid * MB_ * MB_, Gs + tid * MB_ * MB_);
-    __syncthreads();
-  }
   const int t = t0 + tid;
   const bool act = tid < tn;
   double h[kMaxN];
@@ -1553,7 +1589,7 @@ __global__ void __launch_bounds__(kWienFT, 4) k_wiener_ctx(const EmArgs a, const
         for (int mu = 0; mu < MB_; ++mu) {
           cd s{0.0, 0.0};
 #pragma unroll
-          for (int q = 0; q < MB_; ++q) s = s + cmulc(Ws[b * MB_ * MB_ + mu * MB_ + q], xv[b * MB_ + q]);
+          for (int q = 0; q < MB_; ++q) s = cfmac(s, Ws[b * MB_ * MB_ + mu * MB_ + q], xv[b * MB_ + q]);
           y[b * MB_ + mu] = s;
           double e = 0.0;
 #pragma unroll
@@ -1563,10 +1599,23 @@ __global__ void __launch_bounds__(kWienFT, 4) k_wiener_ctx(const EmArgs a, const
         }
     }
   }
-  // each warp stages and stores its own 32 frames: no CTA-wide barrier per source
-  const int lane = tid & 31, wbase = tid & ~31;
+  // this lane's row in the warp's stage: group lane / 4, row lane % 4
+  const int wbase = warp * 32;
   const int wn = max(0, min(32, tn - wbase));
+  const bool leader = (lane & 3) == 0 && lane < wn;
+  const unsigned gframes = (unsigned)max(0, min(4, wn - lane));
   for (int n = 0; n < N; ++n) {
+    unsigned char* st = stage0 + ((size_t)warp * nbuf + (n % nbuf)) * wbytes;
+    cd* row = (cd*)(st + (size_t)(lane >> 2) * gbytes + (size_t)(lane & 3) * M * 16);
+    if (n >= nbuf) {  // this buffer's copies (source n - nbuf) have read shared memory
+      if (leader) {
+        if (nbuf == 2)
+          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        else
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      }
+      __syncwarp();
+    }
     if (act) {
       if constexpr (SB) {
 #pragma unroll
@@ -1582,8 +1631,8 @@ __global__ void __launch_bounds__(kWienFT, 4) k_wiener_ctx(const EmArgs a, const
           for (int r = 0; r < MB_; ++r) {
             cd s{0.0, 0.0};
 #pragma unroll
-            for (int c = 0; c < MB_; ++c) s = s + gb[c * MB_ + r] * sc[c];
-            stage[tid * Mp + b * MB_ + r] = s;
+            for (int c = 0; c < MB_; ++c) s = cfma(s, gb[c * MB_ + r], sc[c]);
+            row[b * MB_ + r] = s;
           }
         }
       } else {
@@ -1599,28 +1648,26 @@ __global__ void __launch_bounds__(kWienFT, 4) k_wiener_ctx(const EmArgs a, const
               cd yc{0.0, 0.0};
               for (int q = 0; q < mb; ++q) {
                 const double2 v = __ldg(reinterpret_cast<const double2*>(xt + off + q));
-                yc = yc + cmulc(wb[c * mb + q], cd{v.x, v.y});
+                yc = cfmac(yc, wb[c * mb + q], cd{v.x, v.y});
               }
               double e = 0.0;
               for (int nn = 0; nn < N; ++nn) e += h[nn] * Ls[nn * M + off + c];
               const double gain = (h[n] * Ls[n * M + off + c]) / fmax(e, a.floor_);
-              s = s + gb[c * mb + r] * (yc * gain);
+              s = cfma(s, gb[c * mb + r], yc * gain);
             }
-            stage[tid * Mp + off + r] = s;
+            row[off + r] = s;
           }
         }
       }
     }
+    // the rows are written: generic-proxy stores visible to the bulk copies
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
-    // coalesced copy of the warp's rows (wn frames x M, contiguous in images)
-    cd* dst = images + (((size_t)n * a.F + f) * T + t0 + wbase) * M;
-    const cd* src = stage + (size_t)wbase * Mp;
-    for (int e = lane; e < wn * M; e += 32) {
-      const int row = e / M;
-      const cd v = src[e + row];  // row * (M + 1) + col
-      *reinterpret_cast<double2*>(dst + e) = make_double2(v.re, v.im);
+    if (leader) {
+      cd* dst = images + (((size_t)n * a.F + f) * T + t0 + wbase + lane) * M;
+      bulk_store(dst, st + (size_t)(lane >> 2) * gbytes, gframes * (unsigned)M * 16u);
     }
-    __syncwarp();
   }
+  if (leader) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // writes complete before exit
 }
 }  // namespace dfm

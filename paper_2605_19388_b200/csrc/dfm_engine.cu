@@ -128,6 +128,7 @@ struct dfm_ctx {
   int xs_iter = 0, xs_iters = 0;
   bool use_graph = true;
   bool has_obs = false, has_model = false;
+  bool h_valid = false;  // H == T V for the current T, V (kept by every iteration's last kernel)
   std::vector<cudaEvent_t> iter_ev;
 };
 
@@ -280,6 +281,7 @@ void launch_spec(dfm_ctx* c) {
   kern<<<grid, 32 * kSpecWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->V.p, c->H.p);
   DFM_CK_LAUNCH();
   c->launches++;
+  c->h_valid = true;
 }
 
 void launch_em(dfm_ctx* c, int finish, int start, int slot, double* cost_dst = nullptr) {
@@ -404,6 +406,7 @@ void launch_rest(dfm_ctx* c, cudaEvent_t* ev) {
   // allreduce (or the caller's exchange) when sharded
   const bool sharded = collective(c) || c->host_exchange;
   if (sharded && !c->host_exchange) launch_spec(c);
+  c->h_valid = !c->host_exchange && !(c->dbg & 4);  // k_vupd's epilogue (or launch_spec) wrote H = T V
 }
 
 void drop_graph(dfm_ctx* c) {
@@ -472,18 +475,25 @@ void run_step(dfm_ctx* c, bool split) {
 // [N][F][T][M]: (W^H)^-1 per (bin, block), H = T V, then k_wiener_ctx.
 void launch_wiener_ctx(dfm_ctx* c, cd* img) {
   if (c->Ginv.n < (size_t)c->F * c->L.wsz) c->Ginv.alloc((size_t)c->F * c->L.wsz);
-  // the static-shape kernels with blocks of <= 4 mics invert W^H per CTA in
-  // registers; larger blocks and the generic kernels read it precomputed
-  const bool ginv = !c->static_shapes || c->kmaxmb > 4;
-  if (ginv) launch_wh_inverse(c->F, c->L, c->W.p, c->L.wsz, c->Ginv.p, c->stream);
-  launch_spec(c);
-  const size_t smem = (size_t)(2 * c->L.wsz + kWienFT * (c->M + 1)) * sizeof(cd) + (size_t)c->N * c->M * 8;
+  // (W^H)^-1 once per (bin, block): in registers for blocks of <= 4 mics,
+  // else the warp Gauss-Jordan kernel
+  if (c->maxmb <= 4) {
+    const int ns = c->F * c->L.nb;
+    k_wh_inverse_small<<<(ns + 127) / 128, 128, 0, c->stream>>>(c->F, c->L, c->W.p, c->Ginv.p);
+    DFM_CK_LAUNCH();
+  } else {
+    launch_wh_inverse(c->F, c->L, c->W.p, c->L.wsz, c->Ginv.p, c->stream);
+  }
+  if (!c->h_valid) launch_spec(c);  // H = T V is current after a fit
+  const size_t smem = (size_t)(kWienFT / 32) * wien_nbuf(c->M) * wien_stage_bytes(c->M) +
+                      (size_t)2 * c->L.wsz * sizeof(cd) +
+                      (size_t)c->N * c->M * 8;
   DFM_CK(cudaFuncSetAttribute(c->kwien, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const EmArgs a = make_args(c);
   const dim3 grid((c->T + kWienFT - 1) / kWienFT, c->F);
   c->kwien<<<grid, kWienFT, smem, c->stream>>>(a, c->Ginv.p, img);
   DFM_CK_LAUNCH();
-  c->launches += ginv ? 3 : 2;
+  c->launches += 2;
 }
 
 }  // namespace
@@ -625,6 +635,7 @@ int dfm_set_model(dfm_ctx* c, const double* Tm, const double* V, const double* l
   c->W.upload(wb.data(), wb.size(), c->stream);
   DFM_CK(cudaStreamSynchronize(c->stream));
   c->has_model = true;
+  c->h_valid = false;
   return DFM_OK;
   DFM_API_END
 }
@@ -679,6 +690,7 @@ int dfm_set_model_native(dfm_ctx* c, const double* Tf, const double* V, const do
   c->W.upload((const cd*)w, c->W.n, c->stream);
   DFM_CK(cudaStreamSynchronize(c->stream));
   c->has_model = true;
+  c->h_valid = false;
   return DFM_OK;
   DFM_API_END
 }
