@@ -285,10 +285,16 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   // lines), with the mic index XOR-swizzled per slot: xsw(slot, m) spreads a
   // warp's per-thread reads of its own frame (pass C) over all banks, and
   // the Q loop's reads of one frame stay within one row.
-  // (Frames of more than 16 mics keep the mic-major [m][FT + 1] layout: the
-  // frame-major one hit an illegal-instruction trap in the 8 x 4-mic
-  // instantiation, cause not isolated.)
-  constexpr bool XFM = SB && MS <= 16;
+  //
+  // The copy loop of 32-mic frames is unrolled by 4, not fully: fully
+  // unrolled, ptxas addressed some of its cp.async (LDGSTS with the L2
+  // cache-hint operand) as [Rn + URm] shared memory, and that form raises
+  // "an illegal instruction was encountered" on sm_100a (driver 580.159,
+  // CUDA 12.9); tools/ldgsts_probe.cu isolates it: exactly the variants whose
+  // LDGSTS use the uniform-register shared address fault, the [Rn + imm]
+  // ones do not.  tests/test_sass.py keeps that form out of the library.
+  constexpr bool XFM = SB && MS <= 32;
+  constexpr int XCU = MS > 16 ? 4 : MS;  // copy-loop unroll
   auto xsw = [&](int slot, int m) -> int {
     if constexpr (XFM) {
       // even keys keep each 32-byte pair of samples whole (copies stay in
@@ -304,7 +310,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     const int nf = min(32, T - fr0);
     if (nf <= 0) return;
     const cd* src = xf + (size_t)fr0 * MS;
-#pragma unroll
+#pragma unroll XCU
     for (int j = 0; j < MS; ++j) {
       const int c = lane + 32 * j;  // frame c / MS, mic c % MS
       const int fl = c / MS, m = c - fl * MS;
