@@ -1434,78 +1434,6 @@ __global__ void __launch_bounds__(128) k_power(const EmArgs a) {
 // staged in shared memory and written with coalesced 16-byte stores.
 constexpr int kWienFT = 128;
 
-// (W_b^H)^-1 of one block in registers (compile-time size): the algorithm of
-// k_wh_inverse (partial-pivot LU of W^H, then one solve per column), whose
-// result it reproduces; w and g are col-major MB x MB
-template <int MB>
-__device__ __forceinline__ void wh_inverse_regs(const cd* w, cd* g) {
-  cd lu[MB * MB];
-  int perm[MB];
-#pragma unroll
-  for (int c = 0; c < MB; ++c)
-#pragma unroll
-    for (int r = 0; r < MB; ++r) lu[c * MB + r] = conjg(w[r * MB + c]);
-#pragma unroll
-  for (int k = 0; k < MB; ++k) {
-    int piv = k;
-    double best = hypot(lu[k * MB + k].re, lu[k * MB + k].im);
-#pragma unroll
-    for (int r = k + 1; r < MB; ++r) {
-      const double v = hypot(lu[k * MB + r].re, lu[k * MB + r].im);
-      if (v > best) {
-        best = v;
-        piv = r;
-      }
-    }
-    perm[k] = piv;
-    if (best != 0.0) {
-#pragma unroll
-      for (int r = k + 1; r < MB; ++r)
-        if (piv == r)
-#pragma unroll
-          for (int c = 0; c < MB; ++c) {
-            const cd t = lu[c * MB + k];
-            lu[c * MB + k] = lu[c * MB + r];
-            lu[c * MB + r] = t;
-          }
-      const cd d = lu[k * MB + k];
-#pragma unroll
-      for (int r = k + 1; r < MB; ++r) lu[k * MB + r] = cdiv(lu[k * MB + r], d);
-    }
-#pragma unroll
-    for (int c = k + 1; c < MB; ++c)
-#pragma unroll
-      for (int r = k + 1; r < MB; ++r) lu[c * MB + r] = lu[c * MB + r] - lu[k * MB + r] * lu[c * MB + k];
-  }
-#pragma unroll
-  for (int col = 0; col < MB; ++col) {
-    cd v[MB];
-#pragma unroll
-    for (int r = 0; r < MB; ++r) v[r] = cd{r == col ? 1.0 : 0.0, 0.0};
-#pragma unroll
-    for (int k = 0; k < MB; ++k)
-#pragma unroll
-      for (int r = k + 1; r < MB; ++r)
-        if (perm[k] == r) {
-          const cd t = v[k];
-          v[k] = v[r];
-          v[r] = t;
-        }
-#pragma unroll
-    for (int r = 1; r < MB; ++r)
-#pragma unroll
-      for (int c = 0; c < r; ++c) v[r] = v[r] - lu[c * MB + r] * v[c];
-#pragma unroll
-    for (int r = MB - 1; r >= 0; --r) {
-#pragma unroll
-      for (int c = r + 1; c < MB; ++c) v[r] = v[r] - lu[c * MB + r] * v[c];
-      v[r] = cdiv(v[r], lu[r * MB + r]);
-    }
-#pragma unroll
-    for (int r = 0; r < MB; ++r) g[col * MB + r] = v[r];
-  }
-}
-
 // Staged images leave through the TMA engine: each warp writes its 32
 // frames' rows for source n into a shared-memory stage laid out as 8 groups
 // of 4 frames (4 x M samples contiguous, as in global memory, groups 16 bytes
@@ -1525,22 +1453,6 @@ __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigne
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(s), "r"(bytes)
                : "memory");
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-
-// (W_b^H)^-1 of every (bin, block) with blocks of <= 4 mics, one thread per
-// system, in registers (wh_inverse_regs: bitwise the result of k_wh_inverse).
-static __global__ void k_wh_inverse_small(int F, Layout L, const cd* __restrict__ W, cd* __restrict__ G) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= F * L.nb) return;
-  const int b = idx % L.nb, f = idx / L.nb;
-  const cd* w = W + (size_t)f * L.wsz + L.woff[b];
-  cd* g = G + (size_t)f * L.wsz + L.woff[b];
-  switch (L.mb[b]) {
-    case 1: wh_inverse_regs<1>(w, g); break;
-    case 2: wh_inverse_regs<2>(w, g); break;
-    case 3: wh_inverse_regs<3>(w, g); break;
-    default: wh_inverse_regs<4>(w, g); break;
-  }
 }
 
 template <int MB_, int NB_, int NS_, int MAXMB>

@@ -110,6 +110,7 @@ struct dfm_ctx {
   bool force_generic = false;
   int FT = 128, TB = 128, smem_em = 0;
   int req_FT = 0, req_TB = 0;
+  int pref_FT = 0;  // measured best frame tile of a static shape (0: the tiler decides)
   DBuf<unsigned long long> trace;
   bool tracing = false;
   ncclComm_t comm = nullptr;
@@ -193,12 +194,16 @@ void select_kernels(dfm_ctx* c) {
   for (int b = 1; b < c->L.nb; ++b) uniform = uniform && c->L.mb[b] == c->L.mb[0];
   const int mb = c->L.mb[0], nb = c->L.nb, N = c->N, K = c->K;
   c->kem = nullptr;
+  c->pref_FT = 0;
   if (uniform && !c->force_generic) {
     if (mb == 4 && nb == 3 && N == 5 && K == 16) {
       c->kem = k_em_bin<4, 3, 5, 4>; c->kpdw = k_pdw<4, 3, 5, 4>; c->kpow = k_power<4, 3, 5, 4>; c->kwien = k_wiener_ctx<4, 3, 5, 4>; c->kmaxmb = 4;
     } else if (mb == 2 && nb == 2 && N == 3 && K == 4) {
       c->kem = k_em_bin<2, 2, 3, 2>; c->kpdw = k_pdw<2, 2, 3, 2>; c->kpow = k_power<2, 2, 3, 2>; c->kwien = k_wiener_ctx<2, 2, 3, 2>; c->kmaxmb = 2;
     } else if (mb == 4 && nb == 8 && N == 8 && K == 32) {
+      // measured: 96-frame tiles (2 CTAs per SM) 2.73 ms per launch against
+      // 2.81 for the tiler's 192 (1 CTA per SM, 7 waves) and 3.47 for 128
+      c->pref_FT = 96;
       c->kem = k_em_bin<4, 8, 8, 4>; c->kpdw = k_pdw<4, 8, 8, 4>; c->kpow = k_power<4, 8, 8, 4>; c->kwien = k_wiener_ctx<4, 8, 8, 4>; c->kmaxmb = 4;
     } else if (mb == 12 && nb == 1 && N == 5 && K == 16) {
       c->kem = k_em_bin<12, 1, 5, 12>; c->kpdw = k_pdw<12, 1, 5, 12>; c->kpow = k_power<12, 1, 5, 12>; c->kwien = k_wiener_ctx<12, 1, 5, 12>; c->kmaxmb = 12;
@@ -226,7 +231,11 @@ bool choose_tiling(dfm_ctx* c) {
   // (non-power-of-two tiles fill the SM when shared memory, not registers,
   // bounds the CTAs per SM: a 12-mic block runs 4 x 96-thread CTAs per SM)
   std::vector<int> cands = {512, 384, 256, 192, 160, 128, 96, 64, 32};
-  if (c->req_FT) cands = {c->req_FT};
+  if (c->req_FT) {
+    cands = {c->req_FT};
+  } else if (c->pref_FT && c->F >= 2 * sms) {  // full-size (unsharded) problems
+    cands = {c->pref_FT};
+  }
   for (int FT : cands) {
     const size_t sm = em_smem(a, FT, c->kmaxmb);
     if (sm > 227 * 1024) continue;
@@ -475,15 +484,8 @@ void run_step(dfm_ctx* c, bool split) {
 // [N][F][T][M]: (W^H)^-1 per (bin, block), H = T V, then k_wiener_ctx.
 void launch_wiener_ctx(dfm_ctx* c, cd* img) {
   if (c->Ginv.n < (size_t)c->F * c->L.wsz) c->Ginv.alloc((size_t)c->F * c->L.wsz);
-  // (W^H)^-1 once per (bin, block): in registers for blocks of <= 4 mics,
-  // else the warp Gauss-Jordan kernel
-  if (c->maxmb <= 4) {
-    const int ns = c->F * c->L.nb;
-    k_wh_inverse_small<<<(ns + 127) / 128, 128, 0, c->stream>>>(c->F, c->L, c->W.p, c->Ginv.p);
-    DFM_CK_LAUNCH();
-  } else {
-    launch_wh_inverse(c->F, c->L, c->W.p, c->L.wsz, c->Ginv.p, c->stream);
-  }
+  // (W^H)^-1 once per (bin, block), one warp per system (Gauss-Jordan)
+  launch_wh_inverse(c->F, c->L, c->W.p, c->L.wsz, c->Ginv.p, c->stream);
   if (!c->h_valid) launch_spec(c);  // H = T V is current after a fit
   const size_t smem = (size_t)(kWienFT / 32) * wien_nbuf(c->M) * wien_stage_bytes(c->M) +
                       (size_t)2 * c->L.wsz * sizeof(cd) +
