@@ -184,6 +184,11 @@ int dfm_set_tiling(dfm_ctx* ctx, int frame_tile, int pd_frames);
  * per-bin kernel (16 slots per CTA).  dfm_set_trace returns the buffer length. */
 int dfm_set_trace(dfm_ctx* ctx, int on);
 int dfm_get_trace(dfm_ctx* ctx, unsigned long long* out, int n);
+/* Profiling aid: per-CTA {entry, exit, SM id} %globaltimer stamps of one
+ * kernel kind (0 k_tupd, 1 k_pdw (entry and end of setup), 2 k_vupd,
+ * 3 k_em_bin).  out == NULL arms the trace for n CTAs (n = 0 disarms);
+ * otherwise synchronises and copies up to n records, returning the count. */
+int dfm_cta_trace(dfm_ctx* ctx, int kind, int n, unsigned long long* out);
 /* Timing experiments only (results become wrong): bit0 skips the Lambda
  * frame reduction, bit1 the Q accumulation of the per-bin kernel. */
 int dfm_debug_bits(dfm_ctx* ctx, int bits);

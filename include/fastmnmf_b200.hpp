@@ -1035,4 +1035,45 @@ inline void write_trace_csv(const std::string& path, const FitReport& report) {
     f << i << ',' << report.cost_trace[i] << ',' << (i == 0 ? 0.0 : report.wall_seconds.at(i - 1)) << '\n';
 }
 
+// ------------------------------------------------------------ sdr.hpp:50-65
+// The tracing harness of the reference's evaluation code (the SDR scorer
+// itself stays out of scope): any score of a FitSnapshot can be
+// traced.
+struct TraceRow {
+  int iteration = 0;
+  double seconds = 0;  // cumulative estimation time, evaluation excluded
+  double cost = 0;
+  double mean_sdr_improvement = 0;
+};
+
+struct TraceResult {
+  FitReport report;
+  std::vector<TraceRow> rows;
+};
+
+/// sdr.cpp:158-177: runs an estimator with periodic snapshot scoring.  The
+/// snapshots are taken between graph-replayed chunks of eval_every
+/// iterations, so the device clock behind `seconds` is stopped while `score`
+/// runs (the reference pauses its estimator clock).
+inline TraceResult trace_run(const std::function<FitReport(const FitOptions&)>& run_fit,
+                             const std::function<double(const FitSnapshot&)>& score, int eval_every,
+                             double floor_ = kFloor) {
+  TraceResult out;
+  FitOptions options;
+  options.floor = floor_;
+  options.eval_every = eval_every;
+  if (eval_every > 0 && score) {
+    options.on_eval = [&](const FitSnapshot& snap) {
+      TraceRow row;
+      row.iteration = snap.iteration;
+      row.seconds = snap.elapsed_seconds;
+      row.cost = snap.cost;
+      row.mean_sdr_improvement = score(snap);
+      out.rows.push_back(row);
+    };
+  }
+  out.report = run_fit(options);
+  return out;
+}
+
 }  // namespace fastmnmf

@@ -7,7 +7,8 @@ from .fastmnmf import (  # noqa: F401
     SourceImages, SpatialModel, build_spectrogram, compute_eta, cost_dist, cost_full, decorrelate,
     decorrelate_blocks, extract_block, fit_distributed, fit_full, fit_single, generate_mixture,
     ip_update_block, ip_update_w, kFloor, mm_update_lambda, mm_update_t, mm_update_v, power_of,
-    fit_many, random_init, random_observations, slice_init, wiener_block, wiener_full)
+    fit_many, random_init, random_observations, slice_init, trace_run, TraceResult, TraceRow, wiener_block,
+    wiener_full)
 
 from . import container, init, stft  # noqa: F401,E402
 from ._capi import SignalTooShortError  # noqa: F401,E402

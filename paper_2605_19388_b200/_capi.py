@@ -82,6 +82,7 @@ _SIGS = {
     "dfm_get_tiling": (_i, [_vp, _ip, _ip, _ip, _ip, _ip]),
     "dfm_force_generic": (_i, [_vp, _i]),
     "dfm_debug_bits": (_i, [_vp, _i]),
+    "dfm_cta_trace": (_i, [_vp, _i, _i, _vp]),
     "dfm_set_trace": (_i, [_vp, _i]),
     "dfm_get_trace": (_i, [_vp, _vp, _i]),
     "dfm_wiener": (_i, [_vp, _vp]),

@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libdfm_b200.so")
-SOURCES = ["dfm_steps.cu", "dfm_engine.cu", "dfm_host.cpp", "dfm_io.cpp", "dfm_stft.cu", "dfm_init.cu",
+SOURCES = ["dfm_steps.cu", "dfm_engine.cu", "dfm_tv.cu", "dfm_host.cpp", "dfm_io.cpp", "dfm_stft.cu", "dfm_init.cu",
            "dfm_align.cpp"]
 HEADERS = ["dfm_common.cuh", "dfm_internal.cuh", "dfm_ip.cuh", "dfm_em.cuh", "dfm_rng.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

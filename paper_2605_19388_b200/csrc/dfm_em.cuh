@@ -30,13 +30,14 @@ namespace dfm {
 // (P = |W^H x|^2 and the T-update weights) -> decorrelate.  One plain store
 // per launch, no atomics; k_stage_close ends the last launch of a fit.
 enum { kStW = 0, kStMM = 1, kStEta = 2, kStDec = 3 };
-enum { kScNone = -1, kScBin = 0, kScTupd = 1, kScPdw = 2, kScVupd = 3 };
+enum { kScNone = -1, kScBin = 0, kScTupd = 1, kScPdw = 2, kScVupd = 3, kScTpd = 4 };
 constexpr int kScPhases = 4;
 struct StageClock {
   unsigned long long prev_t;          // entry stamp of the previous instrumented launch (0: none)
   int prev_kind;                      // its kind (kSc*)
   int pad;
   unsigned long long em_ph[kScPhases];  // k_em_bin's first CTA: time per phase (ns)
+  unsigned long long tpd_ph[2];         // k_tpd's first CTA: T update, pass D (ns)
   double acc[4];                      // seconds per stage since the last reset
 };
 
@@ -62,11 +63,36 @@ __device__ inline void sc_tick(StageClock* sc, int kind) {
       }
       case kScTupd: case kScVupd: sc->acc[kStMM] += dt; break;
       case kScPdw: sc->acc[kStEta] += dt; break;
+      case kScTpd: {  // fused T update (mm_update) + pass D (eta), split by the first CTA's phases
+        const double s0 = (double)sc->tpd_ph[0], s1 = (double)sc->tpd_ph[1];
+        const double fr = s0 + s1 > 0.0 ? s0 / (s0 + s1) : 1.0;
+        sc->acc[kStMM] += dt * fr;
+        sc->acc[kStEta] += dt * (1.0 - fr);
+        break;
+      }
       default: break;
     }
   }
   sc->prev_t = kind == kScNone ? 0ull : now;
   sc->prev_kind = kind;
+}
+
+// Profiling aid (dfm_cta_trace): per-CTA {entry, exit, SM} stamps of the
+// update kernels, one buffer per kind (0 k_tupd, 1 k_pdw, 2 k_vupd, 3 k_em_bin);
+// null = off.  Thread 0 stamps entry and, after the CTA's last barrier, exit.
+static __device__ unsigned long long* g_ctatr[4];
+__device__ __forceinline__ unsigned long long ctatr_begin(int kind) {
+  return (g_ctatr[kind] && threadIdx.x == 0) ? gtimer() : 0ull;
+}
+__device__ __forceinline__ void ctatr_end(int kind, unsigned long long t0) {
+  unsigned long long* b = g_ctatr[kind];
+  if (!b || threadIdx.x != 0) return;
+  unsigned sm;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+  const size_t i = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  b[3 * i] = t0;
+  b[3 * i + 1] = gtimer();
+  b[3 * i + 2] = sm;
 }
 
 struct EmArgs {
@@ -176,6 +202,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   const unsigned long long pol_keep = l2_evict_last(), pol_last = l2_evict_first();
   const double* Hf = a.H + (size_t)f * N * T;
   em_stamp(a, 0);
+  const unsigned long long tr0 = ctatr_begin(3);
   // StageSeconds: the first CTA's phase boundaries (thread 0, shared memory)
   __shared__ unsigned long long sc_ts[4];
   const bool sc_on = a.sc && f == 0;
@@ -915,6 +942,10 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     __syncthreads();
     sc_finish();
   }
+  if (g_ctatr[3]) {
+    __syncthreads();
+    ctatr_end(3, tr0);
+  }
 }
 
 static __global__ void k_vapply(size_t nkt, const double* __restrict__ numden, double* __restrict__ V,
@@ -1013,6 +1044,10 @@ __device__ __forceinline__ void is_weights2(int F, int T, int N, int n, int f, i
   }
 }
 
+// the tile loops run in batches of kSpecBatch tiles: every operand load of a
+// batch is issued before its DMMAs (one L2 round trip per batch, not per tile)
+template <int KS>
+__host__ __device__ constexpr int spec_batch() { return KS <= 8 ? 4 : (KS <= 16 ? 2 : 1); }
 template <int KS>
 __device__ __forceinline__ void spec_rows(int F, int T, int N, int K, int n, int f0, const double* __restrict__ Tf,
                                           const double* __restrict__ V, double* __restrict__ H, int warp, int nwarps,
@@ -1025,29 +1060,39 @@ __device__ __forceinline__ void spec_rows(int F, int T, int N, int K, int n, int
     const int k = 4 * s + q;
     a[s] = (f < F && k < K) ? Tf[((size_t)f * N + n) * K + k] : 0.0;
   }
-  for (int tile = warp; tile * 8 < T; tile += nwarps) {
-    const int tl = tile * 8 + g;
-    double b[KS];
+  constexpr int kSpecBatch = spec_batch<KS>();
+  const int ntile = (T + 7) / 8;
+  for (int tb = warp; tb < ntile; tb += kSpecBatch * nwarps) {
+    double b[kSpecBatch][KS];
 #pragma unroll
-    for (int s = 0; s < KS; ++s) {
-      const int k = 4 * s + q;
-      b[s] = (k < K && tl < T) ? __ldg(V + ((size_t)n * K + k) * T + tl) : 0.0;
-    }
-    double c0 = 0.0, c1 = 0.0;
+    for (int u = 0; u < kSpecBatch; ++u) {
+      const int tl = (tb + u * nwarps) * 8 + g;
 #pragma unroll
-    for (int s = 0; s < KS; ++s) dmma(c0, c1, a[s], b[s]);
-    const int t = tile * 8 + 2 * q;
-    if (tgt) {
-      if (f < F) is_weights2(F, T, N, n, f, t, c0, c1, tgt, eps, Aw, Bw);
-      continue;
+      for (int s = 0; s < KS; ++s) {
+        const int k = 4 * s + q;
+        b[u][s] = (k < K && tl < T) ? __ldg(V + ((size_t)n * K + k) * T + tl) : 0.0;
+      }
     }
-    if (f < F) {
-      double* hp = H + ((size_t)f * N + n) * T;
-      if (!(T & 1) && t + 1 < T) {
-        *reinterpret_cast<double2*>(hp + t) = make_double2(c0, c1);
-      } else {
-        if (t < T) hp[t] = c0;
-        if (t + 1 < T) hp[t + 1] = c1;
+#pragma unroll
+    for (int u = 0; u < kSpecBatch; ++u) {
+      const int tile = tb + u * nwarps;
+      if (tile >= ntile) break;
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int s = 0; s < KS; ++s) dmma(c0, c1, a[s], b[u][s]);
+      const int t = tile * 8 + 2 * q;
+      if (tgt) {
+        if (f < F) is_weights2(F, T, N, n, f, t, c0, c1, tgt, eps, Aw, Bw);
+        continue;
+      }
+      if (f < F) {
+        double* hp = H + ((size_t)f * N + n) * T;
+        if (!(T & 1) && t + 1 < T) {
+          *reinterpret_cast<double2*>(hp + t) = make_double2(c0, c1);
+        } else {
+          if (t < T) hp[t] = c0;
+          if (t + 1 < T) hp[t + 1] = c1;
+        }
       }
     }
   }
@@ -1066,25 +1111,36 @@ __device__ __forceinline__ void spec_cols(int F, int T, int N, int K, int n, int
     b[s] = (k < K && tl < T) ? V[((size_t)n * K + k) * T + tl] : 0.0;
   }
   const int t = t0 + 2 * q;
-  for (int tile = warp; tile * 8 < F; tile += nwarps) {
-    const int f = tile * 8 + g;
-    double a[KS];
+  constexpr int kSpecBatch = spec_batch<KS>();
+  const int ntile = (F + 7) / 8;
+  for (int tb = warp; tb < ntile; tb += kSpecBatch * nwarps) {
+    double a[kSpecBatch][KS];
 #pragma unroll
-    for (int s = 0; s < KS; ++s) {
-      const int k = 4 * s + q;
-      a[s] = (f < F && k < K) ? __ldg(Tf + ((size_t)f * N + n) * K + k) : 0.0;
+    for (int u = 0; u < kSpecBatch; ++u) {
+      const int f = (tb + u * nwarps) * 8 + g;
+#pragma unroll
+      for (int s = 0; s < KS; ++s) {
+        const int k = 4 * s + q;
+        a[u][s] = (f < F && k < K) ? __ldg(Tf + ((size_t)f * N + n) * K + k) : 0.0;
+      }
     }
-    double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-    for (int s = 0; s < KS; ++s) dmma(c0, c1, a[s], b[s]);
-    if (tgt && f < F) is_weights2(F, T, N, n, f, t, c0, c1, tgt, eps, Aw, Bw);  // rec is stored too (divergence)
-    if (f < F) {
-      double* hp = H + ((size_t)f * N + n) * T;
-      if (!(T & 1) && t + 1 < T) {
-        *reinterpret_cast<double2*>(hp + t) = make_double2(c0, c1);
-      } else {
-        if (t < T) hp[t] = c0;
-        if (t + 1 < T) hp[t + 1] = c1;
+    for (int u = 0; u < kSpecBatch; ++u) {
+      const int tile = tb + u * nwarps;
+      if (tile >= ntile) break;
+      const int f = tile * 8 + g;
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int s = 0; s < KS; ++s) dmma(c0, c1, a[u][s], b[s]);
+      if (tgt && f < F) is_weights2(F, T, N, n, f, t, c0, c1, tgt, eps, Aw, Bw);  // rec is stored too (divergence)
+      if (f < F) {
+        double* hp = H + ((size_t)f * N + n) * T;
+        if (!(T & 1) && t + 1 < T) {
+          *reinterpret_cast<double2*>(hp + t) = make_double2(c0, c1);
+        } else {
+          if (t < T) hp[t] = c0;
+          if (t + 1 < T) hp[t + 1] = c1;
+        }
       }
     }
   }
@@ -1104,6 +1160,7 @@ __global__ void __launch_bounds__(32 * kTupdWarps, KT <= 2 ? 3 : 2) k_tupd_mma(i
                                                              const double* __restrict__ tgt = nullptr,
                                                              StageClock* sc = nullptr) {
   __shared__ double part[kTupdWarps / 2][2][KT][64];
+  const unsigned long long tr0 = ctatr_begin(0);
   sc_tick(sc, kScTupd);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
@@ -1113,7 +1170,7 @@ __global__ void __launch_bounds__(32 * kTupdWarps, KT <= 2 ? 3 : 2) k_tupd_mma(i
   const int steps = (T + 3) / 4;
   const int per = (steps + kTupdWarps - 1) / kTupdWarps;
   const int s0 = warp * per, s1 = min(steps, s0 + per);
-  constexpr int U = 4;  // k-steps whose operands are loaded before their DMMAs
+  constexpr int U = KT <= 1 ? 8 : 4;  // k-steps whose operands are loaded before their DMMAs
   double num[KT][2], den[KT][2];
 #pragma unroll
   for (int j = 0; j < KT; ++j) num[j][0] = num[j][1] = den[j][0] = den[j][1] = 0.0;
@@ -1184,6 +1241,10 @@ __global__ void __launch_bounds__(32 * kTupdWarps, KT <= 2 ? 3 : 2) k_tupd_mma(i
   // h' = T_new V (IS-NMF: the weights of rec = T_new V instead)
   spec_rows<2 * KT>(F, T, N, K, n, f0, Tf, V, Hout, warp, kTupdWarps, lane, tgt, floor_, const_cast<double*>(Aw),
                     const_cast<double*>(Bw));
+  if (g_ctatr[0]) {
+    __syncthreads();
+    ctatr_end(0, tr0);
+  }
 }
 
 // V update (engine.cpp:125-133): num[k][t] = sum_f T[f][n][k] A'[n][f][t].
@@ -1201,6 +1262,7 @@ __global__ void __launch_bounds__(32 * kVupdMWarps, KT <= 2 ? 3 : 2) k_vupd_mma(
                                                               const double* __restrict__ tgt = nullptr,
                                                               int n_base = 0, StageClock* sc = nullptr) {
   __shared__ double part[kVupdMWarps / 2][2][KT][64];
+  const unsigned long long tr0 = ctatr_begin(2);
   sc_tick(sc, kScVupd);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
@@ -1210,7 +1272,7 @@ __global__ void __launch_bounds__(32 * kVupdMWarps, KT <= 2 ? 3 : 2) k_vupd_mma(
   const int steps = (F + 3) / 4;
   const int per = (steps + kVupdMWarps - 1) / kVupdMWarps;
   const int s0 = warp * per, s1 = min(steps, s0 + per);
-  constexpr int U = 4;  // k-steps whose operands are loaded before their DMMAs
+  constexpr int U = KT <= 1 ? 8 : 4;  // k-steps whose operands are loaded before their DMMAs
   double num[KT][2], den[KT][2];
 #pragma unroll
   for (int j = 0; j < KT; ++j) num[j][0] = num[j][1] = den[j][0] = den[j][1] = 0.0;
@@ -1284,6 +1346,10 @@ __global__ void __launch_bounds__(32 * kVupdMWarps, KT <= 2 ? 3 : 2) k_vupd_mma(
   // H = T V_new (IS-NMF: and the next iteration's weights)
   spec_cols<2 * KT>(F, T, N, K, n, t0, Tf, V, Hout, warp, kVupdMWarps, lane, tgt, floor_, const_cast<double*>(Aw),
                     const_cast<double*>(Bw));
+  if (g_ctatr[2]) {
+    __syncthreads();
+    ctatr_end(2, tr0);
+  }
 }
 
 // Pass D as an elementwise kernel over (bin, frame): h' from H (= T_new V by
@@ -1300,6 +1366,7 @@ __global__ void __launch_bounds__(128, 6) k_pdw(const EmArgs a) {
   const int T = a.T;
   const int NP = (N + 1) & ~1;
   const int f = blockIdx.y, t = blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned long long tr0 = ctatr_begin(1);
   sc_tick(a.sc, kScPdw);
   const double* Lg = a.lam + (size_t)f * N * M;
   const bool smemL = M * NP <= kMaxN * 64;
@@ -1313,6 +1380,7 @@ __global__ void __launch_bounds__(128, 6) k_pdw(const EmArgs a) {
   if constexpr (IL)
     for (int e = threadIdx.x; e < N * MS; e += blockDim.x) Lr[e] = Lg[e];
   __syncthreads();
+  if (g_ctatr[1] && threadIdx.x == 0) ctatr_end(1, tr0);
   if (t >= T) return;
   auto load_lam = [&](int m, double* lv) {
     if (smemL) {

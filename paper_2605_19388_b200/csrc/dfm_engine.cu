@@ -107,6 +107,7 @@ struct dfm_ctx {
   void (*kpow)(EmArgs) = nullptr;
   void (*kwien)(EmArgs, const cd*, cd*) = nullptr;
   bool static_shapes = false;  // compile-time-shape instantiations selected
+  bool use_tpd = false;        // fused T update + pass D (k_tpd) instead of k_tupd + k_pdw
   bool force_generic = false;
   int FT = 128, TB = 128, smem_em = 0;
   int req_FT = 0, req_TB = 0;
@@ -210,6 +211,8 @@ void select_kernels(dfm_ctx* c) {
     }
   }
   c->static_shapes = c->kem != nullptr;
+  static const bool want_tpd = getenv("DFM_TPD") != nullptr;  // the fused cluster kernel (measured slower)
+  c->use_tpd = c->static_shapes && want_tpd && tpd_supported(c->L.M, N, K, c->T);
   if (!c->kem) {
     if (c->maxmb <= 4) {
       c->kem = k_em_bin<0, 0, 0, 4>; c->kpdw = k_pdw<0, 0, 0, 4>; c->kpow = k_power<0, 0, 0, 4>; c->kwien = k_wiener_ctx<0, 0, 0, 4>; c->kmaxmb = 4;
@@ -405,10 +408,18 @@ void launch_vupd(dfm_ctx* c) {
 // The "start" half of an iteration after k_em_bin: T update, V-update
 // weights, V update, and the spectrogram for the next k_em_bin.
 void launch_rest(dfm_ctx* c, cudaEvent_t* ev) {
-  launch_tupd(c);
-  if (ev) DFM_CK(cudaEventRecord(ev[2], c->stream));
-  launch_pd(c);
-  if (ev) DFM_CK(cudaEventRecord(ev[3], c->stream));
+  if (c->use_tpd) {  // T update + pass D in one cluster kernel (dfm_tv.cu)
+    launch_tpd(c->F, c->T, c->M, c->N, c->K, c->floor_, c->Tf.p, c->V.p, c->lam.p, c->P.p, c->Aw.p, c->Bw.p,
+               c->stage.p, c->stream);
+    c->launches++;
+    if (ev) DFM_CK(cudaEventRecord(ev[2], c->stream));
+    if (ev) DFM_CK(cudaEventRecord(ev[3], c->stream));
+  } else {
+    launch_tupd(c);
+    if (ev) DFM_CK(cudaEventRecord(ev[2], c->stream));
+    launch_pd(c);
+    if (ev) DFM_CK(cudaEventRecord(ev[3], c->stream));
+  }
   launch_vupd(c);
   if (ev) DFM_CK(cudaEventRecord(ev[4], c->stream));
   // H for the next k_em_bin: fused into k_vupd on one GPU; after the
@@ -1071,6 +1082,26 @@ int dfm_get_trace(dfm_ctx* c, unsigned long long* out, int n) {
   c->trace.download(out, m, c->stream);
   DFM_CK(cudaStreamSynchronize(c->stream));
   return (int)m;
+  DFM_API_END
+}
+
+int dfm_cta_trace(dfm_ctx* c, int kind, int n, unsigned long long* out) {
+  if (!c || kind < 0 || kind > 3 || n < 0) return DFM_ERR_ARG;
+  DFM_API_BEGIN
+  static DBuf<unsigned long long> bufs[4];
+  drop_graph(c);  // the symbol is read at launch; a captured graph would keep the old value
+  if (!out) {  // (re)arm: n CTAs (0 = off)
+    bufs[kind].alloc((size_t)3 * n);
+    if (n) DFM_CK(cudaMemset(bufs[kind].p, 0, sizeof(unsigned long long) * 3 * n));
+    unsigned long long* ptr = n ? bufs[kind].p : nullptr;
+    DFM_CK(cudaMemcpyToSymbol(g_ctatr, &ptr, sizeof(ptr), sizeof(ptr) * kind));
+    if (kind == 0) tpd_cta_trace(ptr);  // the fused k_tpd reports as kind 0 too
+    return DFM_OK;
+  }
+  DFM_CK(cudaDeviceSynchronize());
+  const size_t m = std::min<size_t>((size_t)3 * n, bufs[kind].n);
+  if (m) DFM_CK(cudaMemcpy(out, bufs[kind].p, sizeof(unsigned long long) * m, cudaMemcpyDeviceToHost));
+  return (int)(m / 3);
   DFM_API_END
 }
 

@@ -89,6 +89,14 @@ void launch_wiener(const Layout& L, int F, int T, int N, int K, const cd* x, con
                    const cd* W, long long wstride, double floor_, cd* images, cudaStream_t s,
                    long long* launches, cd* G = nullptr);
 
+// The fused T update + pass D (dfm_tv.cu): k_tpd replaces k_tupd_mma + k_pdw
+// for the shapes tpd_supported() accepts.
+struct StageClock;
+bool tpd_supported(int M, int N, int K, int T);
+void tpd_cta_trace(unsigned long long* buf);  // dfm_cta_trace kind 0 in dfm_tv.cu's module
+void launch_tpd(int F, int T, int M, int N, int K, double floor_, double* Tf, const double* V, const double* lam,
+                const double* P, double* Aw, double* Bw, StageClock* sc, cudaStream_t s);
+
 // (W_b^H)^-1 per (bin, block) into G [F][wsz] (wiener.cpp:25).
 void launch_wh_inverse(int F, const Layout& L, const cd* W, long long wstride, cd* G, cudaStream_t s);
 

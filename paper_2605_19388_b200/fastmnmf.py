@@ -702,3 +702,41 @@ def wiener_block(x, models, spatial: BlockSpatialModel, floor: float = kFloor) -
         out[:, :, :, o:o + mb] = _wiener(extract_block(x, spatial.layout, l), BlockLayout.full(mb),
                                          models[l], [sub.W], sub.Lambda, floor)
     return SourceImages(out)
+
+
+# ------------------------------------------------------------ tracing harness
+@dataclass
+class TraceRow:
+    """sdr.hpp:50-55: one periodic evaluation of a running fit."""
+    iteration: int = 0
+    seconds: float = 0.0  # cumulative estimation time, evaluation excluded
+    cost: float = 0.0
+    mean_sdr_improvement: float = 0.0
+
+
+@dataclass
+class TraceResult:
+    """sdr.hpp:57-60."""
+    report: FitReport
+    rows: List[TraceRow] = field(default_factory=list)
+
+
+def trace_run(run_fit: Callable[[FitOptions], FitReport], score: Optional[Callable[[FitSnapshot], float]],
+              eval_every: int, floor: float = kFloor) -> TraceResult:
+    """sdr.cpp:158-177: runs an estimator with periodic snapshot scoring.
+
+    ``run_fit`` maps FitOptions to a FitReport (e.g. ``lambda o:
+    fit_distributed(x, layout, init, iters, options=o).report``); ``score`` maps
+    a FitSnapshot to a number (the reference's SDR improvement, or any other
+    figure of merit).  The snapshots are taken between graph-replayed chunks of
+    ``eval_every`` iterations, so the device clock that fills ``seconds`` never
+    runs while ``score`` does (the reference pauses its estimator clock).
+    """
+    out = TraceResult(report=FitReport(np.zeros(0), np.zeros(0)))
+    options = FitOptions(floor=floor, eval_every=eval_every)
+    if eval_every > 0 and score is not None:
+        def on_eval(snap: FitSnapshot) -> None:
+            out.rows.append(TraceRow(snap.iteration, snap.elapsed_seconds, snap.cost, float(score(snap))))
+        options.on_eval = on_eval
+    out.report = run_fit(options)
+    return out

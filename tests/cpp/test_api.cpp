@@ -4,6 +4,8 @@
 // oracle (oracle/, test infrastructure only) as the checker on the same
 // seeded inputs.  Built by __graft_entry__.build(); run on a GPU by
 // tests/test_cpp_api.py.  Prints "ALL PASSED" and exits 0 on success.
+#include <chrono>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -330,6 +332,34 @@ void test_eval_callback() {
   expect(a.report.cost_trace == b.report.cost_trace, "callbacks do not change the trajectory");
 }
 
+// trace_run (sdr.cpp:158-177), after test_sdr.cpp:146-197: the scorer's time
+// is excluded from the traced seconds and the rows carry the recorded cost
+void test_trace_run() {
+  const BlockLayout layout({4});
+  std::vector<cplx> xf;
+  const ObsTensor x = mixture(24, 64, 4, 2, 4, 70, xf);
+  const InitBundle init = random_init(24, 64, layout, 2, 4, 70);
+  auto runner = [&](const FitOptions& o) { return fit_full(x, init, 20, o).report; };
+  const TraceResult plain = trace_run(runner, nullptr, 0);
+  expect(plain.rows.empty(), "trace_run: no rows without a scorer");
+  auto sleepy = [](const FitSnapshot&) {
+    std::this_thread::sleep_for(std::chrono::milliseconds(25));
+    return 1.0;
+  };
+  const TraceResult traced = trace_run(runner, sleepy, 5);
+  expect(traced.rows.size() == 4, "trace_run: one row per eval_every iterations");
+  bool sorted = true;
+  for (size_t r = 1; r < traced.rows.size(); ++r) sorted = sorted && traced.rows[r].seconds >= traced.rows[r - 1].seconds;
+  expect(sorted, "trace_run: cumulative seconds non-decreasing");
+  expect(traced.report.cost_trace == plain.report.cost_trace, "trace_run: deterministic costs");
+  const double tp = plain.report.total_seconds(), tt = traced.report.total_seconds();
+  expect(tt < 0.100 + tp, "trace_run: the scorer's sleeps are not in the estimation time");
+  const TraceResult zero = trace_run(runner, [](const FitSnapshot&) { return 0.0; }, 2);
+  bool same = zero.rows.size() == 10;
+  for (const auto& row : zero.rows) same = same && row.cost == zero.report.cost_trace[row.iteration];
+  expect(same, "trace_run: traced rows carry the recorded cost");
+}
+
 }  // namespace
 
 int main() {
@@ -345,6 +375,7 @@ int main() {
     test_container();
     test_per_update_monotone();
     test_eval_callback();
+    test_trace_run();
   } catch (const std::exception& e) {
     std::printf("FAIL: uncaught exception: %s\n", e.what());
     return 2;
