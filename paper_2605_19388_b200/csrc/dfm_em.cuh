@@ -114,6 +114,7 @@ struct EmArgs {
   int start;   // 1 = Q, IP, T-update weights
   unsigned long long* trace;  // optional [bin][16] phase stamps
   StageClock* sc;             // optional per-stage device time (StageSeconds)
+  cd* Gout;                   // optional [F][wsz]: (W^H)^-1 per block for the Wiener filter (finish-only launch)
   int dbg;                    // timing experiments only: bit0 no Lambda reduction, bit1 no Q accumulation,
 };
 
@@ -337,6 +338,25 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     const int nf = min(32, T - fr0);
     if (nf <= 0) return;
     const cd* src = xf + (size_t)fr0 * MS;
+    if constexpr (XFM && MS % 8 == 4) {
+      // 4- and 12-mic frames: the lane pattern of c = lane + 32 j repeats
+      // every P = MS / 4 rows 8 frames further on, and the slot key (bit 2 of
+      // the slot) is the same 8 frames on, so each lane forms P address pairs
+      // and every other copy is the same pair plus a constant offset
+      constexpr int P = MS / 4;
+#pragma unroll
+      for (int r = 0; r < P; ++r) {
+        const int c = lane + 32 * r;
+        const int fl = c / MS, m = c - fl * MS;
+        const int k = ((slot0 + fl) >> 1) & 2;
+        cd* d = dst + (slot0 + fl) * MS + m;
+        const cd* s = src + fl * MS + (m ^ k);
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+          if (fl + 8 * p < nf) cp_async16_hint(d + 8 * p * MS, s + 8 * p * MS, pol);
+      }
+      return;
+    }
 #pragma unroll XCU
     for (int j = 0; j < MS; ++j) {
       const int c = lane + 32 * j;  // frame c / MS, mic c % MS
@@ -554,6 +574,13 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
 #pragma unroll
         for (int e = 0; e < MB_ * MB_; ++e) w.Wold[e] = wb[e];
         ldet[b] = logdet2_inverse_thread<MB_>(wb, w.Winv);
+        if (a.Gout) {  // the fit's final demixers: G = (W^-1)^H for the separation (col-major)
+          cd* g = a.Gout + (size_t)f * wsz + b * MB_ * MB_;
+#pragma unroll
+          for (int c = 0; c < MB_; ++c)
+#pragma unroll
+            for (int r = 0; r < MB_; ++r) g[c * MB_ + r] = conjg(w.Winv[r * MB_ + c]);
+        }
       } else {
         cd* scr = (cd*)(smem + sp.ipscr + b * ipscr_bytes<MAXMB>());
         ldet[b] = 2.0 * log_abs_det_serial(MBof(b), Wsm + WOFF(b), scr);
@@ -1523,8 +1550,8 @@ __device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigne
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
-template <int MB_, int NB_, int NS_, int MAXMB>
-__global__ void __launch_bounds__(kWienFT, 4) k_wiener_ctx(const EmArgs a, const cd* __restrict__ G,
+template <int MB_, int NB_, int NS_, int MAXMB, int kWienFT = dfm::kWienFT>
+__global__ void __launch_bounds__(kWienFT, 512 / kWienFT) k_wiener_ctx(const EmArgs a, const cd* __restrict__ G,
                                                         cd* __restrict__ images) {
   constexpr bool SB = MB_ > 0 && NB_ > 0;
   extern __shared__ __align__(16) unsigned char swn[];

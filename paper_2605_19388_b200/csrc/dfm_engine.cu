@@ -106,6 +106,7 @@ struct dfm_ctx {
   void (*kpdw)(EmArgs) = nullptr;
   void (*kpow)(EmArgs) = nullptr;
   void (*kwien)(EmArgs, const cd*, cd*) = nullptr;
+  int wien_ft = kWienFT;  // frames per CTA of k_wiener_ctx (its template tile)
   bool static_shapes = false;  // compile-time-shape instantiations selected
   bool use_tpd = false;        // fused T update + pass D (k_tpd) instead of k_tupd + k_pdw
   bool force_generic = false;
@@ -131,6 +132,7 @@ struct dfm_ctx {
   bool use_graph = true;
   bool has_obs = false, has_model = false;
   bool h_valid = false;  // H == T V for the current T, V (kept by every iteration's last kernel)
+  bool g_valid = false;  // Ginv == (W^H)^-1 of the current W (written by a fit's finish-only launch)
   std::vector<cudaEvent_t> iter_ev;
 };
 
@@ -188,6 +190,20 @@ size_t em_smem(const EmArgs& a, int FT, int kmaxmb) {
   }
 }
 
+// Wiener tile per static shape (frames per CTA; measured, profiles/r02b):
+// config 1 160 (90 us against 100 for 128 and 192), config 2 192 (179 us
+// against 202), config 3 192 (2.93 ms against 3.12); config 0 is the same at
+// 128 and 160.  DFM_WIEN_FT overrides (128, 160, 192) for tile experiments.
+template <int MB_, int NB_, int NS_, int MAXMB>
+void set_wiener(dfm_ctx* c) {
+  static const int env = getenv("DFM_WIEN_FT") ? atoi(getenv("DFM_WIEN_FT")) : 0;
+  int ft = env ? env : ((NB_ == 8 || MB_ > 4) ? 192 : 160);
+  if (ft != 128 && ft != 160 && ft != 192) ft = 128;
+  c->wien_ft = ft;
+  c->kwien = ft == 128 ? k_wiener_ctx<MB_, NB_, NS_, MAXMB, 128>
+                       : (ft == 160 ? k_wiener_ctx<MB_, NB_, NS_, MAXMB, 160> : k_wiener_ctx<MB_, NB_, NS_, MAXMB, 192>);
+}
+
 // Kernel selection: compile-time-shape instantiations for uniform layouts of
 // the BASELINE configurations (0-3), else the generic kernels.
 void select_kernels(dfm_ctx* c) {
@@ -196,18 +212,19 @@ void select_kernels(dfm_ctx* c) {
   const int mb = c->L.mb[0], nb = c->L.nb, N = c->N, K = c->K;
   c->kem = nullptr;
   c->pref_FT = 0;
+  c->wien_ft = kWienFT;
   if (uniform && !c->force_generic) {
     if (mb == 4 && nb == 3 && N == 5 && K == 16) {
-      c->kem = k_em_bin<4, 3, 5, 4>; c->kpdw = k_pdw<4, 3, 5, 4>; c->kpow = k_power<4, 3, 5, 4>; c->kwien = k_wiener_ctx<4, 3, 5, 4>; c->kmaxmb = 4;
+      c->kem = k_em_bin<4, 3, 5, 4>; c->kpdw = k_pdw<4, 3, 5, 4>; c->kpow = k_power<4, 3, 5, 4>; set_wiener<4, 3, 5, 4>(c); c->kmaxmb = 4;
     } else if (mb == 2 && nb == 2 && N == 3 && K == 4) {
-      c->kem = k_em_bin<2, 2, 3, 2>; c->kpdw = k_pdw<2, 2, 3, 2>; c->kpow = k_power<2, 2, 3, 2>; c->kwien = k_wiener_ctx<2, 2, 3, 2>; c->kmaxmb = 2;
+      c->kem = k_em_bin<2, 2, 3, 2>; c->kpdw = k_pdw<2, 2, 3, 2>; c->kpow = k_power<2, 2, 3, 2>; set_wiener<2, 2, 3, 2>(c); c->kmaxmb = 2;
     } else if (mb == 4 && nb == 8 && N == 8 && K == 32) {
       // measured: 96-frame tiles (2 CTAs per SM) 2.73 ms per launch against
       // 2.81 for the tiler's 192 (1 CTA per SM, 7 waves) and 3.47 for 128
       c->pref_FT = 96;
-      c->kem = k_em_bin<4, 8, 8, 4>; c->kpdw = k_pdw<4, 8, 8, 4>; c->kpow = k_power<4, 8, 8, 4>; c->kwien = k_wiener_ctx<4, 8, 8, 4>; c->kmaxmb = 4;
+      c->kem = k_em_bin<4, 8, 8, 4>; c->kpdw = k_pdw<4, 8, 8, 4>; c->kpow = k_power<4, 8, 8, 4>; set_wiener<4, 8, 8, 4>(c); c->kmaxmb = 4;
     } else if (mb == 12 && nb == 1 && N == 5 && K == 16) {
-      c->kem = k_em_bin<12, 1, 5, 12>; c->kpdw = k_pdw<12, 1, 5, 12>; c->kpow = k_power<12, 1, 5, 12>; c->kwien = k_wiener_ctx<12, 1, 5, 12>; c->kmaxmb = 12;
+      c->kem = k_em_bin<12, 1, 5, 12>; c->kpdw = k_pdw<12, 1, 5, 12>; c->kpow = k_power<12, 1, 5, 12>; set_wiener<12, 1, 5, 12>(c); c->kmaxmb = 12;
     }
   }
   c->static_shapes = c->kem != nullptr;
@@ -306,12 +323,19 @@ void launch_em(dfm_ctx* c, int finish, int start, int slot, double* cost_dst = n
   }
   a.finish = finish;
   a.start = start;
+  // a launch that leaves W unchanged (the last of a fit) also writes the
+  // Wiener filter's (W_b^H)^-1 from the W^-1 its log-det pass forms anyway
+  // (static shapes, blocks of <= 4 mics); the separation then skips k_wh_inverse
+  const bool gfuse = !start && c->static_shapes && c->kmaxmb <= 4;
+  if (gfuse && c->Ginv.n < (size_t)c->F * c->L.wsz) c->Ginv.alloc((size_t)c->F * c->L.wsz);
+  a.Gout = gfuse ? c->Ginv.p : nullptr;
   a.cost_out = cost_dst ? cost_dst : c->cost_part.p + (size_t)slot * c->F;
   a.trace = c->tracing ? c->trace.p : nullptr;
   a.dbg = c->dbg;
   c->kem<<<c->F, c->FT, c->smem_em, c->stream>>>(a);
   DFM_CK_LAUNCH();
   c->launches++;
+  c->g_valid = gfuse;
 }
 
 void launch_tupd(dfm_ctx* c) {
@@ -496,17 +520,20 @@ void run_step(dfm_ctx* c, bool split) {
 void launch_wiener_ctx(dfm_ctx* c, cd* img) {
   if (c->Ginv.n < (size_t)c->F * c->L.wsz) c->Ginv.alloc((size_t)c->F * c->L.wsz);
   // (W^H)^-1 once per (bin, block), one warp per system (Gauss-Jordan)
-  launch_wh_inverse(c->F, c->L, c->W.p, c->L.wsz, c->Ginv.p, c->stream);
+  if (!c->g_valid) {
+    launch_wh_inverse(c->F, c->L, c->W.p, c->L.wsz, c->Ginv.p, c->stream);
+    c->launches++;
+  }
   if (!c->h_valid) launch_spec(c);  // H = T V is current after a fit
-  const size_t smem = (size_t)(kWienFT / 32) * wien_nbuf(c->M) * wien_stage_bytes(c->M) +
+  const size_t smem = (size_t)(c->wien_ft / 32) * wien_nbuf(c->M) * wien_stage_bytes(c->M) +
                       (size_t)2 * c->L.wsz * sizeof(cd) +
                       (size_t)c->N * c->M * 8;
   DFM_CK(cudaFuncSetAttribute(c->kwien, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const EmArgs a = make_args(c);
-  const dim3 grid((c->T + kWienFT - 1) / kWienFT, c->F);
-  c->kwien<<<grid, kWienFT, smem, c->stream>>>(a, c->Ginv.p, img);
+  const dim3 grid((c->T + c->wien_ft - 1) / c->wien_ft, c->F);
+  c->kwien<<<grid, c->wien_ft, smem, c->stream>>>(a, c->Ginv.p, img);
   DFM_CK_LAUNCH();
-  c->launches += 2;
+  c->launches++;
 }
 
 }  // namespace
@@ -646,6 +673,7 @@ int dfm_set_model(dfm_ctx* c, const double* Tm, const double* V, const double* l
   c->V.upload(v.data(), v.size(), c->stream);
   c->lam.upload(l.data(), l.size(), c->stream);
   c->W.upload(wb.data(), wb.size(), c->stream);
+  c->g_valid = false;
   DFM_CK(cudaStreamSynchronize(c->stream));
   c->has_model = true;
   c->h_valid = false;
@@ -701,6 +729,7 @@ int dfm_set_model_native(dfm_ctx* c, const double* Tf, const double* V, const do
   c->V.upload(V, c->V.n, c->stream);
   c->lam.upload(lam, c->lam.n, c->stream);
   c->W.upload((const cd*)w, c->W.n, c->stream);
+  c->g_valid = false;
   DFM_CK(cudaStreamSynchronize(c->stream));
   c->has_model = true;
   c->h_valid = false;
