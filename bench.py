@@ -638,7 +638,9 @@ def main():
                           "peak_source": "measured in this run (DFMA microbenchmark, dfm_probe_fp64_tflops)"},
         "iteration_roofline": {"alg_bytes_per_iter": alg_bytes(c), "hbm_frac": alg_bytes(c) / (ms_step * 1e-3) / 1e9 / pk["hbm_gbs"]},
         "kernel_split_ms": {n: float(v) for n, v in zip(names, split_avg)},
-        "wiener": {"ms": w_ms, "alg_bytes": w_bytes, "achieved_gbs": w_bytes / (w_ms * 1e-3) / 1e9,
+        "wiener": {"step": "separation of the fitted model (after the e2e fit): k_wiener_ctx, its (W_b^H)^-1 "
+                           "written by the fit's last bin launch (blocks <= 4 mics; else k_wh_inverse first)",
+                   "ms": w_ms, "alg_bytes": w_bytes, "achieved_gbs": w_bytes / (w_ms * 1e-3) / 1e9,
                    "frac_hbm": w_bytes / (w_ms * 1e-3) / 1e9 / pk["hbm_gbs"]},
         "dominant_kernel": names[dom],
         "stft": stft,

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--workload", default="config1")
     ap.add_argument("--dbg", type=int, default=0)
     ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--tiling", default="", help="FT,TB (dfm_set_tiling)")
     args = ap.parse_args()
     import bench
     import paper_2605_19388_b200 as dfm
@@ -34,6 +35,9 @@ def main():
     eng = dfm.Engine(c["F"], c["T"], layout, c["N"], c["K"])
     eng.set_obs(x)
     eng.set_model(init.nmf, init.w0, init.lambda0)
+    if args.tiling:
+        ft, tb = (int(v) for v in args.tiling.split(","))
+        dfm._capi.check(lib.dfm_set_tiling(eng.ctx, ft, tb))
     dfm._capi.check(lib.dfm_prime(eng.ctx))
     if args.dbg:
         dfm._capi.check(lib.dfm_debug_bits(eng.ctx, args.dbg))
