@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdfm_b200.so")
+# DFM_LIB: another build of the library (A/B timing experiments in tools/)
+LIB_PATH = os.environ.get("DFM_LIB") or os.path.join(_HERE, "libdfm_b200.so")
 
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int)

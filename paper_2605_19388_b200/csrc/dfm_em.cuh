@@ -1384,7 +1384,7 @@ __global__ void __launch_bounds__(32 * kVupdMWarps, KT <= 2 ? 3 : 2) k_vupd_mma(
 // and the V-update weights A'_n = sum_m Lambda z, B'_n = sum_m Lambda / eta'
 // (engine.cpp:231-237).
 template <int MB_, int NB_, int NS_, int MAXMB>
-__global__ void __launch_bounds__(128, 6) k_pdw(const EmArgs a) {
+__global__ void __launch_bounds__(128, (MB_ * NB_ > 16) ? 4 : 6) k_pdw(const EmArgs a) {
   constexpr bool SB = MB_ > 0 && NB_ > 0;
   __shared__ __align__(16) double Ls[kMaxN * 64];  // Lambda^T [m][NP] (one 16-byte load per source pair)
   __shared__ __align__(16) double Lr[kMaxN * 16];  // Lambda [n][M] rows (static shapes with M <= 16)
