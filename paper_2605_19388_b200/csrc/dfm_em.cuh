@@ -890,6 +890,11 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   // P = |W_new^H x|^2 and the T-update weights with the pre-update eta
   // (engine.cpp:100-109), written per (source, bin, frame) for k_tupd
   // uniform trip count over the frame tiles (the warp copies need every lane)
+  // h of the next tile is in flight while this one is computed (as in passes
+  // A, B; measured: config 1 -1 us, config 3 (32 mics) +70 us, so <= 16 mics)
+  constexpr bool PFC = PF;
+  double hnc[kMaxN];
+  if (PFC && tid < T) load_h(tid, hnc);
   for (int t0 = 0; t0 < T; t0 += FT) {
     const int t = t0 + tid;
     const bool act = t < T;
@@ -900,9 +905,15 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     double A[kMaxN], B[kMaxN];
 #pragma unroll
     for (int n = 0; n < kMaxN; ++n) A[n] = B[n] = 0.0;
-    if (act) {
     double h[kMaxN];
-    load_h(t, h);
+    if constexpr (PFC) {
+#pragma unroll
+      for (int n = 0; n < kMaxN; ++n) h[n] = hnc[n];
+      if (t + FT < T) load_h(t + FT, hnc);
+    } else if (act) {
+      load_h(t, h);
+    }
+    if (act) {
     const cd* xt = xf + (size_t)t * M;
     double rawc[MI];
     if constexpr (IL) eta_raw(h, rawc);
