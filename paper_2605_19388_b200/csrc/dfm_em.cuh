@@ -15,6 +15,8 @@
 // Every reduction has a fixed order; there are no floating-point atomics.
 #pragma once
 
+#include <cooperative_groups.h>
+
 namespace dfm {
 
 // ---------------------------------------------------------------------------
@@ -115,6 +117,7 @@ struct EmArgs {
   unsigned long long* trace;  // optional [bin][16] phase stamps
   StageClock* sc;             // optional per-stage device time (StageSeconds)
   cd* Gout;                   // optional [F][wsz]: (W^H)^-1 per block for the Wiener filter (finish-only launch)
+  int cs;     // CTAs per bin of this launch (the kernel's CS; 0 = 1)
   int dbg;                    // timing experiments only: bit0 no Lambda reduction, bit1 no Q accumulation,
 };
 
@@ -161,22 +164,37 @@ __host__ __device__ inline EmPlan plan_em(const EmArgs& a, int FT) {
   return p;
 }
 
+__device__ __forceinline__ int em_cs(const EmArgs& a) { return a.cs > 1 ? a.cs : 1; }
 __device__ __forceinline__ void em_stamp(const EmArgs& a, int phase) {
-  if (a.trace && threadIdx.x == 0) {
+  if (a.trace && threadIdx.x == 0 && (int)blockIdx.x % em_cs(a) == 0) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    a.trace[blockIdx.x * 16 + phase] = t;
+    a.trace[(int)blockIdx.x / em_cs(a) * 16 + phase] = t;
   }
 }
+// the shared memory of CTA `r` of this bin's cluster (CS > 1 only)
+template <class P>
+__device__ __forceinline__ P* cl_peer(P* p, int r) {
+  return cooperative_groups::this_cluster().map_shared_rank(p, (unsigned)r);
+}
+__device__ __forceinline__ void cl_sync() { cooperative_groups::this_cluster().sync(); }
 
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b);
 
-template <int MB_, int NB_, int NS_, int MAXMB>
+template <int MB_, int NB_, int NS_, int MAXMB, int CS_ = 1>
 __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 registers
   constexpr bool SB = MB_ > 0 && NB_ > 0;
   extern __shared__ __align__(16) unsigned char smem[];
-  const int f = blockIdx.x;
+  // CS_ CTAs per bin (a thread-block cluster; frequency shards with fewer
+  // bins than SMs) split its frames into warp-aligned chunks; their Lambda,
+  // cost and Q partial sums are combined through distributed shared memory
+  // in rank order (the same sums in every CTA of the cluster), the IP sweep
+  // runs redundantly in each, and the lead CTA writes the per-bin outputs.
+  // CS_ == 1 is the one-CTA-per-bin kernel.
+  constexpr int cs = CS_;
+  const int f = cs > 1 ? (int)blockIdx.x / cs : (int)blockIdx.x;
+  const bool lead = cs == 1 || (int)blockIdx.x % cs == 0;
   const int tid = threadIdx.x, FT = blockDim.x;
   const int M = SB ? MB_ * NB_ : a.M;
   const int nb = SB ? NB_ : a.nb;
@@ -195,7 +213,11 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   double* ldet = (double*)(smem + sp.ldet);
   double* tile = (double*)(smem + sp.tile);
   const double floor_ = a.floor_;
-  const int ntiles = (T + FT - 1) / FT;
+  const int tchunk = cs > 1 ? (((T + cs - 1) / cs + 31) & ~31) : T;
+  const int tbeg = cs > 1 ? min(T, ((int)blockIdx.x % cs) * tchunk) : 0;
+  const int tend = cs > 1 ? min(T, tbeg + tchunk) : T;
+  const int Tl = tend - tbeg;  // this CTA's frames [tbeg, tend)
+  const int ntiles = (Tl + FT - 1) / FT;
   const cd* xf = a.x + (size_t)f * T * M;
   double* Pf = a.P + (size_t)f * M * T;
   // X is read by pass B and again by pass C after the IP sweep: pass B's
@@ -206,7 +228,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   const unsigned long long tr0 = ctatr_begin(3);
   // StageSeconds: the first CTA's phase boundaries (thread 0, shared memory)
   __shared__ unsigned long long sc_ts[4];
-  const bool sc_on = a.sc && f == 0;
+  const bool sc_on = a.sc && f == 0 && lead;
   auto sc_mark = [&](int i) {
     if (sc_on && tid == 0) sc_ts[i] = gtimer();
   };
@@ -335,7 +357,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   };
   auto warp_copy_x = [&](cd* dst, int slot0, int fr0, unsigned long long pol) {
     const int lane = tid & 31;
-    const int nf = min(32, T - fr0);
+    const int nf = min(32, tend - fr0);
     if (nf <= 0) return;
     const cd* src = xf + (size_t)fr0 * MS;
     if constexpr (XFM && MS % 8 == 4) {
@@ -415,13 +437,13 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     // software pipeline: the next tile's h and P are in flight while this
     // tile is computed and reduced
     double hn[kMaxN], pn[MP];
-    if (tid < T) {
-      load_h(tid, hn);
-      if constexpr (PF) load_power(tid, pn, pol_keep);
+    if (tid < Tl) {
+      load_h(tbeg + tid, hn);
+      if constexpr (PF) load_power(tbeg + tid, pn, pol_keep);
     }
     for (int tl = 0; tl < ntiles; ++tl) {
-      const int t = tl * FT + tid;
-      const int tn = min(FT, T - tl * FT);
+      const int t = tbeg + tl * FT + tid;
+      const int tn = min(FT, Tl - tl * FT);
       double h[kMaxN], pv[MS];
 #pragma unroll
       for (int n = 0; n < kMaxN; ++n) h[n] = hn[n];
@@ -429,7 +451,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
 #pragma unroll
         for (int m = 0; m < MS; ++m) pv[m] = pn[m];
       }
-      if (t + FT < T) {
+      if (t + FT < tend) {
         load_h(t + FT, hn);
         if constexpr (PF) load_power(t + FT, pn, pol_keep);
       }
@@ -536,16 +558,21 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
       }
       __syncthreads();
     }
+    if constexpr (cs > 1) cl_sync();  // every CTA's frame partials are in its red[]
     for (int q = tid; q < NM; q += FT) {
       double nu = 0.0, de = 0.0;
-      for (int s = 0; s < SL; ++s) {
-        nu += red[2 * (s * NM + q)];
-        de += red[2 * (s * NM + q) + 1];
+      for (int r = 0; r < cs; ++r) {
+        const double* rr = cs > 1 ? cl_peer(red, r) : red;
+        for (int s = 0; s < SL; ++s) {
+          nu += rr[2 * (s * NM + q)];
+          de += rr[2 * (s * NM + q) + 1];
+        }
       }
       double& l = Lsm[q];
       l = fmax(l * sqrt(nu / fmax(de, floor_)), floor_);
-      a.lam[(size_t)f * N * M + q] = l;
+      if (lead) a.lam[(size_t)f * N * M + q] = l;
     }
+    if constexpr (cs > 1) cl_sync();  // the peers have read red[] (pass B reuses it)
     __syncthreads();
     build_lst();
     __syncthreads();
@@ -574,7 +601,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
 #pragma unroll
         for (int e = 0; e < MB_ * MB_; ++e) w.Wold[e] = wb[e];
         ldet[b] = logdet2_inverse_thread<MB_>(wb, w.Winv);
-        if (a.Gout) {  // the fit's final demixers: G = (W^-1)^H for the separation (col-major)
+        if (a.Gout && lead) {  // the fit's final demixers: G = (W^-1)^H for the separation (col-major)
           cd* g = a.Gout + (size_t)f * wsz + b * MB_ * MB_;
 #pragma unroll
           for (int c = 0; c < MB_; ++c)
@@ -603,18 +630,18 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     constexpr bool IFM = SB && IL && (MB_ % 2 == 0);
     constexpr int ISP = MS + 2;
     double hn[kMaxN], pn[MP];
-    if (tid < T) {
-      load_h(tid, hn);
-      if constexpr (PF) load_power(tid, pn, pol_last);
+    if (tid < Tl) {
+      load_h(tbeg + tid, hn);
+      if constexpr (PF) load_power(tbeg + tid, pn, pol_last);
     }
     for (int tl = 0; tl < ntiles; ++tl) {
-      const int t = tl * FT + tid;
-      const int tn = min(FT, T - tl * FT);
+      const int t = tbeg + tl * FT + tid;
+      const int tn = min(FT, Tl - tl * FT);
       const cd* xt = xf + (size_t)t * M;
       // the frame's samples for the Q tile: asynchronous copies that land
       // while the per-frame terms below are computed
       if constexpr (SB) {
-        if (a.start) warp_copy_x(xsm, tid & ~31, tl * FT + (tid & ~31), pol_keep);
+        if (a.start) warp_copy_x(xsm, tid & ~31, tbeg + tl * FT + (tid & ~31), pol_keep);
       }
       if (a.start && tid < tn) {
         if constexpr (SB) {
@@ -632,7 +659,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
 #pragma unroll
         for (int m = 0; m < MS; ++m) pv[m] = pn[m];
       }
-      if (t + FT < T) {
+      if (t + FT < tend) {
         load_h(t + FT, hn);
         if constexpr (PF) load_power(t + FT, pn, pol_last);
       }
@@ -740,14 +767,19 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   cost = warp_sum(cost);
   if ((tid & 31) == 0) wsum[tid >> 5] = cost;
   __syncthreads();
-  if (tid == 0) {
+  if constexpr (cs > 1) cl_sync();  // the peers' cost and Q partials are complete
+  if (tid == 0 && lead) {
     double c = 0.0;
-    for (int w = 0; w < sp.nwarps; ++w) c += wsum[w];
+    for (int r = 0; r < cs; ++r) {
+      const double* ws = cs > 1 ? cl_peer(wsum, r) : wsum;
+      for (int w = 0; w < sp.nwarps; ++w) c += ws[w];
+    }
     double d = 0.0;
     for (int b = 0; b < nb; ++b) d += ldet[b];
     a.cost_out[f] = c - (double)T * d;
   }
   if (!a.start) {
+    if constexpr (cs > 1) cl_sync();  // the lead has read the peers' wsum
     sc_finish();
     return;
   }
@@ -759,7 +791,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   const bool pf_early = (size_t)M * FTpc * sizeof(cd) <= sp.qsum - sp.tile;
   __syncthreads();  // the Q tile reads of pass B are done (Qsum overwrites the tile end)
   if constexpr (SB) {
-    if (pf_early) warp_copy_x(xst, tid & ~31, tid & ~31, pol_last);
+    if (pf_early) warp_copy_x(xst, tid & ~31, tbeg + (tid & ~31), pol_last);
   }
   for (int idx = tid; idx < nitems * MAXMB; idx += FT) {
     const int it = idx / MAXMB, mu = idx - it * MAXMB;
@@ -775,11 +807,15 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     const int mb = MBof(b);
     if (mu >= mb) continue;
     cd sum{0.0, 0.0};
-    for (int s = 0; s < SQ; ++s) sum = sum + qpart[mu * (SQ * nitems) + s * nitems + it];
+    for (int r = 0; r < cs; ++r) {
+      const cd* qp = cs > 1 ? cl_peer(qpart, r) : qpart;
+      for (int s = 0; s < SQ; ++s) sum = sum + qp[mu * (SQ * nitems) + s * nitems + it];
+    }
     const int E = mb * (mb + 1) / 2;
     Qsum[a.qofs[b] + mu * E + rem] = cd{sum.re / (double)T, sum.im / (double)T};
   }
   __syncthreads();
+  if constexpr (cs > 1) cl_sync();  // the peers have read this CTA's Q partials (red[] is reused below)
   em_stamp(a, 3);
 
   // ============================================================ IP sweep
@@ -808,14 +844,14 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
         const cd* qb = Qsum + a.qofs[b];
         const long long c0 = clock64();
         const bool ok = ip_sweep_quad<MB_>(wb, w, qb, floor_, l, qmask);
-        if (a.trace && b == 0 && l == 0) a.trace[blockIdx.x * 16 + 8] = (unsigned long long)(clock64() - c0);
-        if (!ok && l == 0 && a.trace) atomicAdd(a.trace + blockIdx.x * 16 + 7, 1ull);
+        if (a.trace && lead && b == 0 && l == 0) a.trace[f * 16 + 8] = (unsigned long long)(clock64() - c0);
+        if (!ok && l == 0 && a.trace && lead) atomicAdd(a.trace + f * 16 + 7, 1ull);
         if (!ok && l == 0) {
           // exact path (engine.cpp:47-49: LU, residual test, pinv) from W_old
 #pragma unroll
           for (int e = 0; e < MB_ * MB_; ++e) wb[e] = w.Wold[e];
           const int fb = ip_solve_thread<MB_>(wb, qb, floor_, w.slow);
-          if (fb) atomicAdd(a.fallbacks, fb);
+          if (fb && lead) atomicAdd(a.fallbacks, fb);
         }
         __syncwarp(qmask);
       };
@@ -863,8 +899,8 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
         fbs = 0;
         const long long c0 = clock64();
         const bool ok = ip_sweep_warp<MAXMB>(mb, wb, Qsum + a.qofs[b], Qinv + a.qofs[b], floor_, sc);
-        if (a.trace && b == 0 && lane == 0) a.trace[blockIdx.x * 16 + 8] = (unsigned long long)(clock64() - c0);
-        if (!ok && lane == 0 && a.trace) atomicAdd(a.trace + blockIdx.x * 16 + 7, 1ull);
+        if (a.trace && lead && b == 0 && lane == 0) a.trace[f * 16 + 8] = (unsigned long long)(clock64() - c0);
+        if (!ok && lane == 0 && a.trace && lead) atomicAdd(a.trace + f * 16 + 7, 1ull);
         // exact path (engine.cpp:47-49: LU, residual test, pinv), W restored
         if (!ok)
           for (int mu = 0; mu < mb; ++mu) {
@@ -874,15 +910,16 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
             };
             fbs += ip_column_warp<MAXMB>(mb, wb, mu, qget, floor_, sc);
           }
-        if (lane == 0 && fbs) atomicAdd(a.fallbacks, fbs);
+        if (lane == 0 && fbs && lead) atomicAdd(a.fallbacks, fbs);
       }
     }
   }
   __syncthreads();
   if constexpr (SB) {  // Q_mu is dead: pass C's first frame into the tile start
-    if (!pf_early) warp_copy_x(xst, tid & ~31, tid & ~31, pol_last);
+    if (!pf_early) warp_copy_x(xst, tid & ~31, tbeg + (tid & ~31), pol_last);
   }
-  for (int e = tid; e < wsz; e += FT) a.W[(size_t)f * wsz + e] = Wsm[e];
+  if (lead)
+    for (int e = tid; e < wsz; e += FT) a.W[(size_t)f * wsz + e] = Wsm[e];
   em_stamp(a, 4);
   sc_mark(3);
 
@@ -894,10 +931,10 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   // A, B; measured: config 1 -1 us, config 3 (32 mics) +70 us, so <= 16 mics)
   constexpr bool PFC = PF;
   double hnc[kMaxN];
-  if (PFC && tid < T) load_h(tid, hnc);
-  for (int t0 = 0; t0 < T; t0 += FT) {
+  if (PFC && tid < Tl) load_h(tbeg + tid, hnc);
+  for (int t0 = tbeg; t0 < tend; t0 += FT) {
     const int t = t0 + tid;
-    const bool act = t < T;
+    const bool act = t < tend;
     if constexpr (SB) {
       cp_async_wait_all();
       __syncwarp();  // the warp's copies of this tile's frames have landed
@@ -909,7 +946,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     if constexpr (PFC) {
 #pragma unroll
       for (int n = 0; n < kMaxN; ++n) h[n] = hnc[n];
-      if (t + FT < T) load_h(t + FT, hnc);
+      if (t + FT < tend) load_h(t + FT, hnc);
     } else if (act) {
       load_h(t, h);
     }
@@ -964,7 +1001,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     }  // act
     if constexpr (SB) {
       __syncwarp();  // every lane has read its slot: the warp's next frames
-      if (t0 + FT < T) warp_copy_x(xst, tid & ~31, t0 + FT + (tid & ~31), pol_last);
+      if (t0 + FT < tend) warp_copy_x(xst, tid & ~31, t0 + FT + (tid & ~31), pol_last);
     }
     if (act)
 #pragma unroll
@@ -1189,15 +1226,17 @@ __device__ __forceinline__ void spec_cols(int F, int T, int N, int K, int n, int
 // partials are added in warp order, then the multiplicative update.
 constexpr int kTupdWarps = 8;
 constexpr int kMaxKt = kMaxK / 8;
-template <int KT>
-__global__ void __launch_bounds__(32 * kTupdWarps, KT <= 2 ? 3 : 2) k_tupd_mma(int F, int T, int N, int K, double* __restrict__ Tf,
+// WARPS: 8, or 16 when the grid has fewer CTAs than SMs (frequency shards:
+// a warp's share of the frames, and so its chain of load round trips, halves)
+template <int KT, int WARPS = kTupdWarps>
+__global__ void __launch_bounds__(32 * WARPS, WARPS > 8 ? 1 : (KT <= 2 ? 3 : 2)) k_tupd_mma(int F, int T, int N, int K, double* __restrict__ Tf,
                                                              const double* __restrict__ V,
                                                              const double* __restrict__ Aw,
                                                              const double* __restrict__ Bw, double floor_,
                                                              const int* __restrict__ skip, double* __restrict__ Hout,
                                                              const double* __restrict__ tgt = nullptr,
                                                              StageClock* sc = nullptr) {
-  __shared__ double part[kTupdWarps / 2][2][KT][64];
+  __shared__ double part[WARPS / 2][2][KT][64];
   const unsigned long long tr0 = ctatr_begin(0);
   sc_tick(sc, kScTupd);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1206,7 +1245,7 @@ __global__ void __launch_bounds__(32 * kTupdWarps, KT <= 2 ? 3 : 2) k_tupd_mma(i
   if (skip && skip[n]) return;  // IS-NMF: this source has converged
   constexpr int kt = KT;
   const int steps = (T + 3) / 4;
-  const int per = (steps + kTupdWarps - 1) / kTupdWarps;
+  const int per = (steps + WARPS - 1) / WARPS;
   const int s0 = warp * per, s1 = min(steps, s0 + per);
   constexpr int U = KT <= 1 ? 8 : 4;  // k-steps whose operands are loaded before their DMMAs
   double num[KT][2], den[KT][2];
@@ -1240,7 +1279,7 @@ __global__ void __launch_bounds__(32 * kTupdWarps, KT <= 2 ? 3 : 2) k_tupd_mma(i
   }
   // fixed-order tree over the warps: w += w + h for h = W/2, W/4, ..., 1
 #pragma unroll
-  for (int h = kTupdWarps / 2; h >= 1; h >>= 1) {
+  for (int h = WARPS / 2; h >= 1; h >>= 1) {
     if (warp >= h && warp < 2 * h)
 #pragma unroll
       for (int j = 0; j < KT; ++j) {
@@ -1277,7 +1316,7 @@ __global__ void __launch_bounds__(32 * kTupdWarps, KT <= 2 ? 3 : 2) k_tupd_mma(i
   if (!Hout) return;
   __syncthreads();  // the CTA's new T rows are visible
   // h' = T_new V (IS-NMF: the weights of rec = T_new V instead)
-  spec_rows<2 * KT>(F, T, N, K, n, f0, Tf, V, Hout, warp, kTupdWarps, lane, tgt, floor_, const_cast<double*>(Aw),
+  spec_rows<2 * KT>(F, T, N, K, n, f0, Tf, V, Hout, warp, WARPS, lane, tgt, floor_, const_cast<double*>(Aw),
                     const_cast<double*>(Bw));
   if (g_ctatr[0]) {
     __syncthreads();

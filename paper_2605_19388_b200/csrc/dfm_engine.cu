@@ -103,6 +103,8 @@ struct dfm_ctx {
   int maxmb = 4;
   int kmaxmb = 4;  // MAXMB of the selected instantiations
   void (*kem)(EmArgs) = nullptr;
+  void (*kem2)(EmArgs) = nullptr;  // the same shape with a 2-CTA cluster per bin (few-bin shards)
+  int cs_em = 1;                   // CTAs per bin of the selected bin kernel
   void (*kpdw)(EmArgs) = nullptr;
   void (*kpow)(EmArgs) = nullptr;
   void (*kwien)(EmArgs, const cd*, cd*) = nullptr;
@@ -211,10 +213,12 @@ void select_kernels(dfm_ctx* c) {
   for (int b = 1; b < c->L.nb; ++b) uniform = uniform && c->L.mb[b] == c->L.mb[0];
   const int mb = c->L.mb[0], nb = c->L.nb, N = c->N, K = c->K;
   c->kem = nullptr;
+  c->kem2 = nullptr;
   c->pref_FT = 0;
   c->wien_ft = kWienFT;
   if (uniform && !c->force_generic) {
     if (mb == 4 && nb == 3 && N == 5 && K == 16) {
+      c->kem2 = k_em_bin<4, 3, 5, 4, 2>;
       c->kem = k_em_bin<4, 3, 5, 4>; c->kpdw = k_pdw<4, 3, 5, 4>; c->kpow = k_power<4, 3, 5, 4>; set_wiener<4, 3, 5, 4>(c); c->kmaxmb = 4;
     } else if (mb == 2 && nb == 2 && N == 3 && K == 4) {
       c->kem = k_em_bin<2, 2, 3, 2>; c->kpdw = k_pdw<2, 2, 3, 2>; c->kpow = k_power<2, 2, 3, 2>; set_wiener<2, 2, 3, 2>(c); c->kmaxmb = 2;
@@ -222,6 +226,7 @@ void select_kernels(dfm_ctx* c) {
       // measured: 96-frame tiles (2 CTAs per SM) 2.73 ms per launch against
       // 2.81 for the tiler's 192 (1 CTA per SM, 7 waves) and 3.47 for 128
       c->pref_FT = 96;
+      c->kem2 = k_em_bin<4, 8, 8, 4, 2>;
       c->kem = k_em_bin<4, 8, 8, 4>; c->kpdw = k_pdw<4, 8, 8, 4>; c->kpow = k_power<4, 8, 8, 4>; set_wiener<4, 8, 8, 4>(c); c->kmaxmb = 4;
     } else if (mb == 12 && nb == 1 && N == 5 && K == 16) {
       c->kem = k_em_bin<12, 1, 5, 12>; c->kpdw = k_pdw<12, 1, 5, 12>; c->kpow = k_power<12, 1, 5, 12>; set_wiener<12, 1, 5, 12>(c); c->kmaxmb = 12;
@@ -274,6 +279,30 @@ bool choose_tiling(dfm_ctx* c) {
     return false;
   }
   c->FT = bestFT;
+  c->cs_em = 1;
+  // a frequency shard with at most half as many bins as SMs: each bin's
+  // frames split over a 2-CTA cluster (measured on config 1's 8-way shard:
+  // k_em_bin 48.3 -> 43.3 us), the tile chosen for the half frames
+  static const int env_cs = getenv("DFM_EM_CS") ? atoi(getenv("DFM_EM_CS")) : 0;  // 1: never split
+  if (c->kem2 && !c->req_FT && env_cs != 1 && 2 * c->F <= sms) {
+    const int half = ((c->T + 1) / 2 + 31) & ~31;
+    double best2 = 1e30;
+    int ft2 = 0;
+    for (int FT : cands) {
+      const size_t sm = em_smem(a, FT, c->kmaxmb);
+      if (sm > 227 * 1024) continue;
+      const int per_sm = std::max(1, std::min({(int)((228 * 1024) / (sm + 1024)), 65536 / (FT * 128), 2048 / FT, 32}));
+      const double score = std::ceil(2.0 * c->F / (sms * per_sm)) * std::ceil((double)half / FT) + 0.01 * FT / 256.0;
+      if (score < best2) {
+        best2 = score;
+        ft2 = FT;
+      }
+    }
+    if (ft2) {
+      c->FT = ft2;
+      c->cs_em = 2;
+    }
+  }
   c->smem_em = (int)em_smem(a, c->FT, c->kmaxmb);
   c->TB = c->req_TB ? c->req_TB : 128;  // frames per CTA of the elementwise pass D
   return true;
@@ -281,6 +310,7 @@ bool choose_tiling(dfm_ctx* c) {
 
 void set_kernel_attrs(dfm_ctx* c) {
   DFM_CK(cudaFuncSetAttribute(c->kem, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_em));
+  if (c->kem2) DFM_CK(cudaFuncSetAttribute(c->kem2, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_em));
 
 }
 
@@ -332,7 +362,24 @@ void launch_em(dfm_ctx* c, int finish, int start, int slot, double* cost_dst = n
   a.cost_out = cost_dst ? cost_dst : c->cost_part.p + (size_t)slot * c->F;
   a.trace = c->tracing ? c->trace.p : nullptr;
   a.dbg = c->dbg;
-  c->kem<<<c->F, c->FT, c->smem_em, c->stream>>>(a);
+  if (c->cs_em > 1) {  // a cluster of cs_em CTAs per bin
+    a.cs = c->cs_em;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(c->F * c->cs_em));
+    cfg.blockDim = dim3(c->FT);
+    cfg.dynamicSmemBytes = c->smem_em;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = c->cs_em;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    DFM_CK(cudaLaunchKernelEx(&cfg, c->kem2, a));
+  } else {
+    c->kem<<<c->F, c->FT, c->smem_em, c->stream>>>(a);
+  }
   DFM_CK_LAUNCH();
   c->launches++;
   c->g_valid = gfuse;
@@ -341,14 +388,20 @@ void launch_em(dfm_ctx* c, int finish, int start, int slot, double* cost_dst = n
 void launch_tupd(dfm_ctx* c) {
   const dim3 grid((c->F + 7) / 8, c->N);
   auto kern = k_tupd_mma<8>;
+  int warps = kTupdWarps;
+  static int sms = 0;
+  if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  static const bool no_wide = getenv("DFM_TUPD_WIDE") && atoi(getenv("DFM_TUPD_WIDE")) == 0;
+  const bool wide = !no_wide && (int)(grid.x * grid.y) < sms;  // fewer CTAs than SMs (shards): 16 warps each
   switch ((c->K + 7) / 8) {
     case 1: kern = k_tupd_mma<1>; break;
-    case 2: kern = k_tupd_mma<2>; break;
-    case 3: case 4: kern = k_tupd_mma<4>; break;
+    case 2: kern = wide ? k_tupd_mma<2, 16> : k_tupd_mma<2>; break;
+    case 3: case 4: kern = wide ? k_tupd_mma<4, 16> : k_tupd_mma<4>; break;
     default: kern = k_tupd_mma<8>; break;
   }
+  if (wide && (c->K + 7) / 8 >= 2 && (c->K + 7) / 8 <= 4) warps = 16;
   // h' = T_new V fused into the T update
-  kern<<<grid, 32 * kTupdWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->V.p, c->Aw.p, c->Bw.p, c->floor_,
+  kern<<<grid, 32 * warps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->V.p, c->Aw.p, c->Bw.p, c->floor_,
                                                 nullptr, (c->dbg & 4) ? nullptr : c->H.p, nullptr, c->stage.p);
   DFM_CK_LAUNCH();
   c->launches++;
