@@ -1220,7 +1220,7 @@ int dfm_get_tiling(const dfm_ctx* c, int* frame_tile, int* pd_frames, int* ctas,
   if (!c) return DFM_ERR_ARG;
   if (frame_tile) *frame_tile = c->FT;
   if (pd_frames) *pd_frames = c->TB;
-  if (ctas) *ctas = c->F;
+  if (ctas) *ctas = c->F * c->cs_em;  // 2 per bin when the bins run as 2-CTA clusters
   if (threads) *threads = c->FT;
   if (smem) *smem = c->smem_em;
   return DFM_OK;

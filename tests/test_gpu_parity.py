@@ -654,3 +654,30 @@ def test_ip_branch_near_the_residual_threshold(dfm, oracle, sizes, N, K):
         for f in np.nonzero(stable)[0]:
             assert _rel(a[f], b[f]) < 1e-7, f"bin {f} (LU residual {res[f]:.1e})"
 
+
+
+def test_two_cta_cluster_bins_match_oracle(dfm, oracle):
+    """A shard with at most half as many bins as SMs runs every bin as a 2-CTA
+    cluster (k_em_bin<..., CS=2>: half the frames each, partial sums through
+    distributed shared memory).  The fit meets the north_star bar against the
+    oracle: trajectory 1e-8 over 20 iterations, non-increasing cost, separated
+    STFTs 1e-6; and the full-size context keeps one CTA per bin."""
+    F, T, sizes, N, K, iters = 40, 160, [4, 4, 4], 5, 16, 20
+    layout = dfm.BlockLayout(sizes)
+    x = dfm.generate_mixture(1, F, T, layout.total, N, K, 31)
+    init = dfm.random_init(F, T, layout, N, K, 32)
+    e = dfm.Engine(F, T, layout, N, K)
+    assert e.tiling()["ctas"] == 2 * F
+    e.close()
+    big = dfm.Engine(513, 626, layout, N, K)
+    assert big.tiling()["ctas"] == 513
+    big.close()
+    fit = dfm.fit_distributed(x, layout, init, iters, True)
+    ref = oracle.run_engine(x, sizes, _init_dict(init), iters)
+    cost = fit.report.cost_trace
+    assert np.max(np.abs(cost - ref["cost_trace"]) / np.abs(ref["cost_trace"])) < TRAJ_RTOL
+    assert np.all(cost[1:] <= cost[:-1] + 1e-9 * np.abs(cost[:-1]))
+    assert fit.report.fallbacks == ref["fallbacks"]
+    img = dfm.wiener_block(x, fit.models, fit.spatial).images
+    ref_img = oracle.wiener_block(x, sizes, ref)
+    assert _rel(img, ref_img) < 1e-6
