@@ -952,9 +952,14 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     }
     if (act) {
     const cd* xt = xf + (size_t)t * M;
-    double rawc[MI];
-    if constexpr (IL) eta_raw(h, rawc);
-#pragma unroll
+    // blocks in a rolled loop (one block's code instead of NB_ copies: the
+    // kernel's hot instruction footprint); eta per mic from the block's
+    // Lambda column, the same FMA chain over n as eta_raw, so bitwise equal
+    constexpr bool ROLLC = true;
+    constexpr bool ILC = IL && !ROLLC;
+    double rawc[ILC ? MI : 1];
+    if constexpr (ILC) eta_raw(h, rawc);
+#pragma unroll 1
     for (int b = 0; b < nb; ++b) {
       double P[MAXMB];
       if constexpr (SB) {  // the block's samples from the thread's slot
@@ -980,8 +985,8 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
           double lv[kMaxN];
           load_lam(m, lv);
           double raw = 0.0;
-          if constexpr (IL) {
-            raw = rawc[IL ? m : 0];
+          if constexpr (ILC) {
+            raw = rawc[ILC ? m : 0];
           } else {
 #pragma unroll
             for (int n = 0; n < kMaxN; ++n)
