@@ -249,18 +249,16 @@ __device__ double logdet2_inverse_thread(const cd* W, cd* Winv) {
   }
 #pragma unroll 1
   for (int col = 0; col < MB; ++col) {
+    // the row swaps applied to e_col leave a unit vector: follow its 1
+    int pos = col;
+#pragma unroll
+    for (int k = 0; k < MB; ++k) {
+      if (pos == k) pos = perm[k];
+      else if (pos == perm[k]) pos = k;
+    }
     cd v[MB];
 #pragma unroll
-    for (int r = 0; r < MB; ++r) v[r] = cd{r == col ? 1.0 : 0.0, 0.0};
-#pragma unroll
-    for (int k = 0; k < MB; ++k)
-#pragma unroll
-      for (int r = k + 1; r < MB; ++r)
-        if (perm[k] == r) {
-          const cd t = v[k];
-          v[k] = v[r];
-          v[r] = t;
-        }
+    for (int r = 0; r < MB; ++r) v[r] = cd{r == pos ? 1.0 : 0.0, 0.0};
 #pragma unroll
     for (int r = 1; r < MB; ++r)
 #pragma unroll
@@ -275,6 +273,10 @@ __device__ double logdet2_inverse_thread(const cd* W, cd* Winv) {
     for (int r = 0; r < MB; ++r) Winv[col * MB + r] = v[r];
   }
   return sing ? -INFINITY : 2.0 * acc;
+}
+
+__device__ __forceinline__ cd shfl4(unsigned mask, cd v, int src) {
+  return cd{__shfl_sync(mask, v.re, src, 4), __shfl_sync(mask, v.im, src, 4)};
 }
 
 // Cholesky Q_mu = L L^H of one weighted covariance (Hermitian, packed upper
@@ -400,9 +402,6 @@ __device__ bool ip_sweep_fast(cd* W, IpWork<MB>& f, const cd* qb, double floor_)
 // residual and of the Sherman-Morrison update, exchanging values with
 // width-4 shuffles.  Same algebra and the same reference residual test as
 // ip_sweep_fast; every early exit is uniform across the quad.
-__device__ __forceinline__ cd shfl4(unsigned mask, cd v, int src) {
-  return cd{__shfl_sync(mask, v.re, src, 4), __shfl_sync(mask, v.im, src, 4)};
-}
 
 template <int MB>
 __device__ bool ip_sweep_quad(cd* W, IpWork<MB>& f, const cd* qb, double floor_, int l, unsigned mask) {
