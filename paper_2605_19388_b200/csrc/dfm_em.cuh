@@ -118,6 +118,8 @@ struct EmArgs {
   StageClock* sc;             // optional per-stage device time (StageSeconds)
   cd* Gout;                   // optional [F][wsz]: (W^H)^-1 per block for the Wiener filter (finish-only launch)
   int cs;     // CTAs per bin of this launch (the kernel's CS; 0 = 1)
+  const double* ld_in;  // optional [F][nb]: 2 ln|det W_b| of the current W (k_logdet)
+  const cd* winv_in;    // optional [F][wsz]: W_b^-1 of the current W (k_logdet)
   int dbg;                    // timing experiments only: bit0 no Lambda reduction, bit1 no Q accumulation,
 };
 
@@ -600,7 +602,14 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
         const cd* wb = Wsm + b * MB_ * MB_;
 #pragma unroll
         for (int e = 0; e < MB_ * MB_; ++e) w.Wold[e] = wb[e];
-        ldet[b] = logdet2_inverse_thread<MB_>(wb, w.Winv);
+        if (a.ld_in) {  // formed by k_logdet while the previous iteration's update kernels ran
+          ldet[b] = a.ld_in[(size_t)f * nb + b];
+          const cd* gi = a.winv_in + (size_t)f * wsz + b * MB_ * MB_;
+#pragma unroll
+          for (int e = 0; e < MB_ * MB_; ++e) w.Winv[e] = gi[e];
+        } else {
+          ldet[b] = logdet2_inverse_thread<MB_>(wb, w.Winv);
+        }
         if (a.Gout && lead) {  // the fit's final demixers: G = (W^-1)^H for the separation (col-major)
           cd* g = a.Gout + (size_t)f * wsz + b * MB_ * MB_;
 #pragma unroll
@@ -1233,20 +1242,42 @@ constexpr int kTupdWarps = 8;
 constexpr int kMaxKt = kMaxK / 8;
 // WARPS: 8, or 16 when the grid has fewer CTAs than SMs (frequency shards:
 // a warp's share of the frames, and so its chain of load round trips, halves)
-template <int KT, int WARPS = kTupdWarps>
+// LDMB > 0: the grid's leading ld.rows rows of CTAs instead form 2 ln|det W_b|
+// and W_b^-1 of the new demixers (blocks of LDMB <= 4 mics, one thread per
+// (bin, block)) for the next k_em_bin: they start first, on the SMs the T
+// update leaves free, and finish well inside it; the bin kernel then only
+// loads them (a single thread's factorisation held one warp about 6 us)
+struct LdArgs {
+  const cd* W;
+  int nb, wsz, rows;
+  double* ld;
+  cd* winv;
+};
+template <int KT, int WARPS = kTupdWarps, int LDMB = 0>
 __global__ void __launch_bounds__(32 * WARPS, WARPS > 8 ? 1 : (KT <= 2 ? 3 : 2)) k_tupd_mma(int F, int T, int N, int K, double* __restrict__ Tf,
                                                              const double* __restrict__ V,
                                                              const double* __restrict__ Aw,
                                                              const double* __restrict__ Bw, double floor_,
                                                              const int* __restrict__ skip, double* __restrict__ Hout,
                                                              const double* __restrict__ tgt = nullptr,
-                                                             StageClock* sc = nullptr) {
+                                                             StageClock* sc = nullptr, LdArgs lda = LdArgs{}) {
   __shared__ double part[WARPS / 2][2][KT][64];
   const unsigned long long tr0 = ctatr_begin(0);
   sc_tick(sc, kScTupd);
+  if constexpr (LDMB > 0) {
+    if ((int)blockIdx.y < lda.rows) {
+      const int i = ((int)blockIdx.y * (int)gridDim.x + (int)blockIdx.x) * (int)blockDim.x + (int)threadIdx.x;
+      if (i < F * lda.nb) {
+        const int f = i / lda.nb, b = i - f * lda.nb;
+        const size_t o = (size_t)f * lda.wsz + (size_t)b * LDMB * LDMB;
+        lda.ld[i] = logdet2_inverse_thread<LDMB>(lda.W + o, lda.winv + o);
+      }
+      return;
+    }
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
-  const int n = blockIdx.y, f0 = blockIdx.x * 8;
+  const int n = (int)blockIdx.y - (LDMB > 0 ? lda.rows : 0), f0 = blockIdx.x * 8;
   if (skip && skip[n]) return;  // IS-NMF: this source has converged
   constexpr int kt = KT;
   const int steps = (T + 3) / 4;
@@ -1534,6 +1565,21 @@ __global__ void __launch_bounds__(128, (MB_ * NB_ > 16) ? 4 : 6) k_pdw(const EmA
       a.Aw[o] = A[n];
       a.Bw[o] = B[n];
     }
+}
+
+// 2 ln|det W_b| and W_b^-1 of every (bin, block) of the current demixers
+// (blocks <= 4 mics), one thread per system, written for the next k_em_bin.
+// The engine runs it on a second stream beside the T / V updates, which do
+// not touch W: the bin kernel then only loads the results, where a serial
+// factorisation on one warp held its first pass-B tile for about 6 us.
+template <int MB>
+__global__ void k_logdet(int F, int nb, int wsz, const cd* __restrict__ W, double* __restrict__ ld,
+                         cd* __restrict__ winv) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= F * nb) return;
+  const int f = i / nb, b = i - f * nb;
+  const size_t o = (size_t)f * wsz + (size_t)b * MB * MB;
+  ld[i] = logdet2_inverse_thread<MB>(W + o, winv + o);
 }
 
 // Closes the last instrumented launch of a fit (StageClock).

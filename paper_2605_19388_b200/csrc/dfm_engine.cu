@@ -104,6 +104,12 @@ struct dfm_ctx {
   int kmaxmb = 4;  // MAXMB of the selected instantiations
   void (*kem)(EmArgs) = nullptr;
   void (*kem2)(EmArgs) = nullptr;  // the same shape with a 2-CTA cluster per bin (few-bin shards)
+  // log-det + W^-1 of the current demixers by k_logdet (static shapes, blocks <= 4)
+  void (*kld)(int, int, int, const cd*, double*, cd*) = nullptr;
+  DBuf<double> ldg;
+  DBuf<cd> winvg;
+  bool ld_valid = false;  // ldg / winvg hold the current W's values
+
   int cs_em = 1;                   // CTAs per bin of the selected bin kernel
   void (*kpdw)(EmArgs) = nullptr;
   void (*kpow)(EmArgs) = nullptr;
@@ -214,6 +220,7 @@ void select_kernels(dfm_ctx* c) {
   const int mb = c->L.mb[0], nb = c->L.nb, N = c->N, K = c->K;
   c->kem = nullptr;
   c->kem2 = nullptr;
+  c->kld = nullptr;
   c->pref_FT = 0;
   c->wien_ft = kWienFT;
   if (uniform && !c->force_generic) {
@@ -227,6 +234,11 @@ void select_kernels(dfm_ctx* c) {
       // 2.81 for the tiler's 192 (1 CTA per SM, 7 waves) and 3.47 for 128
       c->pref_FT = 96;
       c->kem2 = k_em_bin<4, 8, 8, 4, 2>;
+      // config 3's eight blocks: the log-dets move into the T update's leading
+      // CTA rows (A/B: step 3336 -> 3260 us); with config 1's three blocks the
+      // in-kernel factorisation is cheaper than the rows (k_tupd +6 us at 80
+      // registers against k_em_bin -2 us), so it stays there
+      c->kld = k_logdet<4>;
       c->kem = k_em_bin<4, 8, 8, 4>; c->kpdw = k_pdw<4, 8, 8, 4>; c->kpow = k_power<4, 8, 8, 4>; set_wiener<4, 8, 8, 4>(c); c->kmaxmb = 4;
     } else if (mb == 12 && nb == 1 && N == 5 && K == 16) {
       c->kem = k_em_bin<12, 1, 5, 12>; c->kpdw = k_pdw<12, 1, 5, 12>; c->kpow = k_power<12, 1, 5, 12>; set_wiener<12, 1, 5, 12>(c); c->kmaxmb = 12;
@@ -311,6 +323,10 @@ bool choose_tiling(dfm_ctx* c) {
 void set_kernel_attrs(dfm_ctx* c) {
   DFM_CK(cudaFuncSetAttribute(c->kem, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_em));
   if (c->kem2) DFM_CK(cudaFuncSetAttribute(c->kem2, cudaFuncAttributeMaxDynamicSharedMemorySize, c->smem_em));
+  if (c->kld && !c->ldg.p) {  // allocated before any stream capture
+    c->ldg.alloc((size_t)c->F * c->L.nb);
+    c->winvg.alloc((size_t)c->F * c->L.wsz);
+  }
 
 }
 
@@ -343,6 +359,14 @@ void launch_spec(dfm_ctx* c) {
   c->h_valid = true;
 }
 
+// k_logdet on stream s for the current W (see dfm_em.cuh)
+void launch_logdet(dfm_ctx* c, cudaStream_t s) {
+  const int n = c->F * c->L.nb;
+  c->kld<<<(n + 127) / 128, 128, 0, s>>>(c->F, c->L.nb, c->L.wsz, c->W.p, c->ldg.p, c->winvg.p);
+  DFM_CK_LAUNCH();
+  c->launches++;
+}
+
 void launch_em(dfm_ctx* c, int finish, int start, int slot, double* cost_dst = nullptr) {
   EmArgs a = make_args(c);
   if (finish == 1) {  // first launch of a fit: P of the initial demixers
@@ -353,6 +377,14 @@ void launch_em(dfm_ctx* c, int finish, int start, int slot, double* cost_dst = n
   }
   a.finish = finish;
   a.start = start;
+  if (c->kld) {  // the log-dets and inverses of the current W come precomputed
+    if (!c->ld_valid) {
+      launch_logdet(c, c->stream);
+      c->ld_valid = true;
+    }
+    a.ld_in = c->ldg.p;
+    a.winv_in = c->winvg.p;
+  }
   // a launch that leaves W unchanged (the last of a fit) also writes the
   // Wiener filter's (W_b^H)^-1 from the W^-1 its log-det pass forms anyway
   // (static shapes, blocks of <= 4 mics); the separation then skips k_wh_inverse
@@ -383,28 +415,43 @@ void launch_em(dfm_ctx* c, int finish, int start, int slot, double* cost_dst = n
   DFM_CK_LAUNCH();
   c->launches++;
   c->g_valid = gfuse;
+  if (start) c->ld_valid = false;  // the sweep changes W (launch_rest forms the new values)
 }
 
 void launch_tupd(dfm_ctx* c) {
-  const dim3 grid((c->F + 7) / 8, c->N);
+  dim3 grid((c->F + 7) / 8, c->N);
   auto kern = k_tupd_mma<8>;
   int warps = kTupdWarps;
   static int sms = 0;
   if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   static const bool no_wide = getenv("DFM_TUPD_WIDE") && atoi(getenv("DFM_TUPD_WIDE")) == 0;
   const bool wide = !no_wide && (int)(grid.x * grid.y) < sms;  // fewer CTAs than SMs (shards): 16 warps each
+  // leading CTA rows form the new W's log-dets and inverses for the next
+  // k_em_bin (static shapes with blocks of <= 4 mics; dfm_em.cuh LdArgs)
+  const bool ld = c->kld && !c->ld_valid;
+  const int mb = c->L.mb[0];
+  LdArgs lda{};
   switch ((c->K + 7) / 8) {
     case 1: kern = k_tupd_mma<1>; break;
     case 2: kern = wide ? k_tupd_mma<2, 16> : k_tupd_mma<2>; break;
-    case 3: case 4: kern = wide ? k_tupd_mma<4, 16> : k_tupd_mma<4>; break;
+    case 3: case 4:
+      kern = wide ? (ld ? k_tupd_mma<4, 16, 4> : k_tupd_mma<4, 16>) : (ld ? k_tupd_mma<4, 8, 4> : k_tupd_mma<4>);
+      break;
     default: kern = k_tupd_mma<8>; break;
   }
   if (wide && (c->K + 7) / 8 >= 2 && (c->K + 7) / 8 <= 4) warps = 16;
+  const bool ld_fused = ld && (c->K + 7) / 8 >= 3 && (c->K + 7) / 8 <= 4 && mb == 4;
+  if (ld_fused) {
+    const int per_row = (int)grid.x * 32 * warps;
+    lda = LdArgs{c->W.p, c->L.nb, c->L.wsz, (c->F * c->L.nb + per_row - 1) / per_row, c->ldg.p, c->winvg.p};
+    grid.y += lda.rows;
+  }
   // h' = T_new V fused into the T update
   kern<<<grid, 32 * warps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->V.p, c->Aw.p, c->Bw.p, c->floor_,
-                                                nullptr, (c->dbg & 4) ? nullptr : c->H.p, nullptr, c->stage.p);
+                                           nullptr, (c->dbg & 4) ? nullptr : c->H.p, nullptr, c->stage.p, lda);
   DFM_CK_LAUNCH();
   c->launches++;
+  if (ld_fused) c->ld_valid = true;
 }
 
 // pass D: the elementwise V-update weights from h' (= T_new V, written by the
@@ -677,6 +724,8 @@ void dfm_destroy(dfm_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+
+
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -727,6 +776,7 @@ int dfm_set_model(dfm_ctx* c, const double* Tm, const double* V, const double* l
   c->lam.upload(l.data(), l.size(), c->stream);
   c->W.upload(wb.data(), wb.size(), c->stream);
   c->g_valid = false;
+  c->ld_valid = false;
   DFM_CK(cudaStreamSynchronize(c->stream));
   c->has_model = true;
   c->h_valid = false;
@@ -783,6 +833,7 @@ int dfm_set_model_native(dfm_ctx* c, const double* Tf, const double* V, const do
   c->lam.upload(lam, c->lam.n, c->stream);
   c->W.upload((const cd*)w, c->W.n, c->stream);
   c->g_valid = false;
+  c->ld_valid = false;
   DFM_CK(cudaStreamSynchronize(c->stream));
   c->has_model = true;
   c->h_valid = false;

@@ -767,7 +767,7 @@ int is_nmf_dev(const double* h0_dev, int F, int T, int N, int K, int max_iters, 
     // rec = T_new V fused (skipped with the update for converged sources,
     // whose rec is unchanged)
     kern<<<dim3((F + 7) / 8, N), 32 * kTupdWarps, 0, s>>>(F, T, N, K, Tf.p, V.p, Aw.p, Bw.p, kEpsNmf, done.p,
-                                                          H.p, tgt.p, nullptr);
+                                                          H.p, tgt.p, nullptr, LdArgs{});
     DFM_CK_LAUNCH();
   };
   auto vupd = [&]() {
