@@ -138,6 +138,9 @@ __host__ __device__ inline EmPlan plan_em(const EmArgs& a, int FT) {
   p.SL = FT / NM > 1 ? FT / NM : 1;
   p.nitems = a.etot;
   p.SQ = FT / a.etot > 1 ? FT / a.etot : 1;
+  // layouts with at most 32 Q items: slices are (warp, sub-slice within the
+  // warp's 32 frames), so a static kernel's Q loop can be warp-local (WLQ)
+  if (a.etot <= 32) p.SQ = p.nwarps * (32 / a.etot);
   size_t o = 0;
   p.lsm = o; o += al(N * M * sizeof(double));
   p.lst = o; o += al(M * (size_t)((N + 1) & ~1) * sizeof(double));  // Lambda^T [m][N rounded to even]
@@ -501,15 +504,16 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
           zs[m * FTp + tid] = p * ie * ie;
         }
       }
-      __syncthreads();
+      // fsj: warp w reduces the 32 frames it wrote itself, so the tile loop
+      // needs no CTA barrier and the warps stream their frames independently
+      if (FSJ && fsj) __syncwarp(); else __syncthreads();
       // Lambda numerator / denominator (engine.cpp:139-145) as the products
       // (N x frames) (frames x M) on the FP64 tensor cores: warp job = (column
       // tile of 8 mics, num|den), accumulated over k-steps of 4 frames and over
       // tiles in registers.  Fallback: SIMT (n, m) units.
       if (a.dbg & 1) {
       } else if (FSJ && fsj) {
-        const int chunk = (((tn + 3) >> 2) + nwarps - 1) / nwarps * 4;  // frames per warp (k-steps of 4)
-        const int s0 = warp * chunk, s1 = min(tn, s0 + chunk);
+        const int s0 = warp * 32, s1 = min(tn, s0 + 32);  // the warp's own frames
         // two independent accumulator chains per job (even / odd k-steps)
         double e0[FSJ ? NJ : 1], e1[FSJ ? NJ : 1], o0[FSJ ? NJ : 1], o1[FSJ ? NJ : 1];
 #pragma unroll
@@ -583,7 +587,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
         red[2 * u] += num;
         red[2 * u + 1] += den;
       }
-      __syncthreads();
+      if (FSJ && fsj) __syncwarp(); else __syncthreads();
     }
     if (FSJ && fsj) {
       __syncthreads();
@@ -646,8 +650,10 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   LogAcc lacc;
   const int nitems = sp.nitems, SQ = sp.SQ;
   cd* qpart = (cd*)red;  // [MAXMB][SQ * nitems] running sums over tiles (item-slices contiguous)
-  if (a.start)
+  if (a.start) {
     for (int e = tid; e < SQ * nitems * MAXMB; e += FT) qpart[e] = cd{0.0, 0.0};
+    __syncthreads();  // the warp-local Q loop has no CTA barrier before its first sums
+  }
   // log-det (+ W^-1 for the fast IP path) of the pre-IP demixers: threads
   // with no Q item take one (bin, block) system each
   {
@@ -695,6 +701,9 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     // weights with two broadcast 16-byte loads instead of four 8-byte ones
     constexpr bool IFM = SB && IL && (MB_ % 2 == 0);
     constexpr int ISP = MS + 2;
+    // static layouts with at most 32 (block, entry) items: warp-local Q loop
+    constexpr int NIT = SB ? NB_ * MB_ * (MB_ + 1) / 2 : 64;
+    constexpr bool WLQ = IFM && NIT <= 32;
     double hn[kMaxN], pn[MP];
     if (tid < Tl) {
       load_h(tbeg + tid, hn);
@@ -768,6 +777,45 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
         }
         lacc.renorm();
       }
+      if constexpr (WLQ) {
+        // warp-local Q accumulation: lane (item, sub-slice) sums its item over
+        // the warp's own 32 frames of the tile (the samples its warp copied,
+        // the 1/eta its lanes wrote), so the tile loop has no CTA barrier
+        if (a.start) {
+          cp_async_wait_all();
+          __syncwarp();
+          constexpr int SW = 32 / NIT;
+          constexpr int E = MB_ * (MB_ + 1) / 2;
+          const int lane = tid & 31, wq = tid >> 5;
+          if (lane < NIT * SW && !(a.dbg & 2)) {
+            const int qitem = lane % NIT, sub = lane / NIT;
+            const int qb_ = qitem / E;
+            int qr, qc;
+            decode_entry(qitem - qb_ * E, qr, qc);
+            const int off = qb_ * MB_;
+            const double* ef = is + off;
+            cd qacc[MB_];
+#pragma unroll
+            for (int mu = 0; mu < MB_; ++mu) qacc[mu] = cd{0.0, 0.0};
+            const int te = min(tn, 32 * wq + 32);
+#pragma unroll 4
+            for (int tt = 32 * wq + sub; tt < te; tt += SW) {
+              const cd pr = xsm[xsw(tt, off + qr)] * conjg(xsm[xsw(tt, off + qc)]);
+#pragma unroll
+              for (int mu = 0; mu < MB_; mu += 2) {
+                const double2 e = *reinterpret_cast<const double2*>(ef + tt * ISP + mu);
+                qacc[mu] = rfma(qacc[mu], pr, e.x);
+                qacc[mu + 1] = rfma(qacc[mu + 1], pr, e.y);
+              }
+            }
+            const int NU = nitems * SQ;
+            cd* dst = qpart + (wq * SW + sub) * nitems + qitem;
+#pragma unroll
+            for (int mu = 0; mu < MB_; ++mu) dst[mu * NU] = dst[mu * NU] + qacc[mu];
+          }
+          __syncwarp();  // the warp's reads are done before its next copies land
+        }
+      } else
       if (a.start) {
         if constexpr (SB) cp_async_wait_all();
         __syncthreads();
