@@ -798,8 +798,33 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
 #pragma unroll
             for (int mu = 0; mu < MB_; ++mu) qacc[mu] = cd{0.0, 0.0};
             const int te = min(tn, 32 * wq + 32);
+            int tt = 32 * wq + sub;
+            if constexpr (SW == 1) {
+              // whole key periods of frames: the slot's swizzle key is a
+              // compile-time constant of the unrolled position, so a sample
+              // address is the group's base plus an immediate (the rolled
+              // form spent ~11 integer instructions per frame on xsw)
+              constexpr int KP = (MS % 4 == 0) ? 8 : 4;  // the key's period in slots
+              const int mr = off + qr, mc = off + qc;
+              for (; tt + KP <= te; tt += KP) {
+                const cd* xg = xsm + tt * MS;
+                const double* eg = ef + tt * ISP;
+#pragma unroll
+                for (int j = 0; j < KP; ++j) {
+                  constexpr int dummy = 0;
+                  const int key = (MS % 8 == 0) ? j : ((MS % 4 == 0) ? ((j >> 1) & 2) : dummy);
+                  const cd pr = xg[j * MS + (mr ^ key)] * conjg(xg[j * MS + (mc ^ key)]);
+#pragma unroll
+                  for (int mu = 0; mu < MB_; mu += 2) {
+                    const double2 e = *reinterpret_cast<const double2*>(eg + j * ISP + mu);
+                    qacc[mu] = rfma(qacc[mu], pr, e.x);
+                    qacc[mu + 1] = rfma(qacc[mu + 1], pr, e.y);
+                  }
+                }
+              }
+            }
 #pragma unroll 4
-            for (int tt = 32 * wq + sub; tt < te; tt += SW) {
+            for (; tt < te; tt += SW) {
               const cd pr = xsm[xsw(tt, off + qr)] * conjg(xsm[xsw(tt, off + qc)]);
 #pragma unroll
               for (int mu = 0; mu < MB_; mu += 2) {
