@@ -1420,6 +1420,55 @@ __global__ void __launch_bounds__(32 * WARPS, WARPS > 8 ? 1 : (KT <= 2 ? 3 : 2))
   const int f = f0 + g;
   const double* ar = Aw + ((size_t)n * F + (f < F ? f : 0)) * T;
   const double* br = Bw + ((size_t)n * F + (f < F ? f : 0)) * T;
+  if (!(T & 1)) {
+    // even T (every row 16-byte aligned): a lane loads 4 consecutive frames
+    // of its row as two 16-byte loads, and k-step u of a 16-frame group
+    // takes frame 4 q + u from lane (g, q) -- the DMMA sums over the frames,
+    // so any grouping into k-steps is the same sum.  The four lanes of a row
+    // cover one 128-byte line per pair of loads: half the L1 wavefronts of
+    // the 8-byte loads below (8 rows x 32 bytes per instruction), which is
+    // what bounds this kernel (L1tex ~2 cycles per line touched).
+    const int groups = (T + 15) / 16;
+    const int gper = (groups + WARPS - 1) / WARPS;
+    const int g0 = warp * gper, g1 = min(groups, g0 + gper);
+    auto ld2 = [](const double* p, bool ok) {
+      return ok ? __ldg(reinterpret_cast<const double2*>(p)) : make_double2(0.0, 0.0);
+    };
+    for (int gb = g0; gb < g1; ++gb) {
+      const int t = 16 * gb + 4 * q;
+      const bool ok0 = t < T, ok1 = t + 2 < T;
+      const double2 a0 = ld2(ar + t, ok0 && f < F), a1 = ld2(ar + t + 2, ok1 && f < F);
+      const double2 b0 = ld2(br + t, ok0 && f < F), b1 = ld2(br + t + 2, ok1 && f < F);
+      double2 v0[KT], v1[KT];
+#pragma unroll
+      for (int j = 0; j < KT; ++j) {
+        const int k = 8 * j + g;
+        const double* vr = V + ((size_t)n * K + (k < K ? k : 0)) * T + t;
+        v0[j] = ld2(vr, ok0 && k < K);
+        v1[j] = ld2(vr + 2, ok1 && k < K);
+      }
+#pragma unroll
+      for (int j = 0; j < KT; ++j) {
+        dmma(num[j][0], num[j][1], a0.x, v0[j].x);
+        dmma(den[j][0], den[j][1], b0.x, v0[j].x);
+      }
+#pragma unroll
+      for (int j = 0; j < KT; ++j) {
+        dmma(num[j][0], num[j][1], a0.y, v0[j].y);
+        dmma(den[j][0], den[j][1], b0.y, v0[j].y);
+      }
+#pragma unroll
+      for (int j = 0; j < KT; ++j) {
+        dmma(num[j][0], num[j][1], a1.x, v1[j].x);
+        dmma(den[j][0], den[j][1], b1.x, v1[j].x);
+      }
+#pragma unroll
+      for (int j = 0; j < KT; ++j) {
+        dmma(num[j][0], num[j][1], a1.y, v1[j].y);
+        dmma(den[j][0], den[j][1], b1.y, v1[j].y);
+      }
+    }
+  } else
   for (int sb = s0; sb < s1; sb += U) {
     double av[U], bv[U], vb[U][KT];
 #pragma unroll
