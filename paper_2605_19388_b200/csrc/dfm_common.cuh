@@ -17,8 +17,8 @@
 
 namespace dfm {
 
-// Acceptance of the fast IP paths (ip_sweep_quad / ip_sweep_fast /
-// ip_sweep_warp).  The reference decides LU-or-pinv per column on
+// Acceptance of the fast IP paths (ip_sweep_quad / ip_sweep_warp).  The
+// reference decides LU-or-pinv per column on
 // ||S u_LU - e_mu|| <= 1e-6 (engine.cpp:47-49).  The fast paths solve the
 // same system in another form (Q_mu^-1 W^-H e_mu), whose residual can differ
 // from the LU one by a small factor near the threshold.  A fast sweep is

@@ -342,9 +342,10 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   // warp's per-thread reads of its own frame (pass C) over all banks, and
   // the Q loop's reads of one frame stay within one row.
   //
-  // The copy loop of 32-mic frames is unrolled by 4, not fully: fully
-  // unrolled, ptxas addressed some of its cp.async (LDGSTS with the L2
-  // cache-hint operand) as [Rn + URm] shared memory, and that form raises
+  // The copy loop of 32-mic frames: when ptxas is free to, it addresses some
+  // of the cp.async (LDGSTS with the L2 cache-hint operand) as [Rn + URm]
+  // shared memory (fully unrolled it did; unrolled by 4 it did or did not
+  // with the register allocation of the rest of the kernel), and that form raises
   // "an illegal instruction was encountered" on sm_100a (driver 580.159,
   // CUDA 12.9); tools/ldgsts_probe.cu isolates it: exactly the variants whose
   // LDGSTS use the uniform-register shared address fault, the [Rn + imm]
@@ -385,17 +386,30 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
       }
       return;
     }
+    if constexpr (XFM) {
+      // lane order = destination order: copy j of a lane lands at the lane's
+      // first 16 bytes + 512 j, and fetches the sample whose swizzled
+      // position that is (XOR is an involution; the source stays within the
+      // same 64-byte group).  The shared address of each batch of XCU copies
+      // is a shuffled (opaque) register plus immediates, so ptxas cannot
+      // form the faulting [Rn + URm] address (above).
+      const unsigned sb = (unsigned)__cvta_generic_to_shared(dst + slot0 * MS + lane);
+#pragma unroll 1
+      for (int j0 = 0; j0 < MS; j0 += XCU) {
+        const unsigned sj = opaque_u32(sb + 512u * (unsigned)j0);
+#pragma unroll
+        for (int i = 0; i < XCU; ++i) {
+          const int c = lane + 32 * (j0 + i);  // frame c / MS, mic c % MS
+          const int fl = c / MS, m = c - fl * MS;
+          const int k = xsw(slot0 + fl, 0) - (slot0 + fl) * MS;  // the slot's XOR key
+          if (fl < nf) cp_async16_hint_s(sj + 512u * (unsigned)i, src + fl * MS + (m ^ k), pol);
+        }
+      }
+    } else {
 #pragma unroll XCU
-    for (int j = 0; j < MS; ++j) {
-      const int c = lane + 32 * j;  // frame c / MS, mic c % MS
-      const int fl = c / MS, m = c - fl * MS;
-      if constexpr (XFM) {
-        // lane order = destination order: the lane writing (slot, m) fetches
-        // the sample whose swizzled position that is (XOR is an involution;
-        // the source stays within the same 64-byte group)
-        const int k = xsw(slot0 + fl, 0) - (slot0 + fl) * MS;  // the slot's XOR key
-        if (fl < nf) cp_async16_hint(dst + (slot0 + fl) * MS + m, src + fl * MS + (m ^ k), pol);
-      } else {
+      for (int j = 0; j < MS; ++j) {
+        const int c = lane + 32 * j;  // frame c / MS, mic c % MS
+        const int fl = c / MS, m = c - fl * MS;
         if (fl < nf) cp_async16_hint(dst + xsw(slot0 + fl, m), src + c, pol);
       }
     }
@@ -969,7 +983,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
       for (int b = (il >> 2) * nw + iw; b < nb; b += 8 * nw)
         if (l < MB_) {
           IpWork<MB_>& w = *(IpWork<MB_>*)(smem + sp.ipscr + b * ipscr_bytes<MAXMB>());
-          w.ok[l] = chol_thread<MB_>(Qsum + a.qofs[b] + l * E, w.L[l], w.dinv[l]) ? 1 : 0;
+          w.ok[l] = herm_inverse_thread<MB_>(Qsum + a.qofs[b] + l * E, w.Qi[l]) ? 1 : 0;
         }
       __syncthreads();
       em_stamp(a, 6);

@@ -190,8 +190,7 @@ struct IpWork {
   IpScratch<MB> slow;            // exact LU + pinv path (fallback)
   cd Winv[MB * MB];              // W^-1, col-major
   cd Wold[MB * MB];              // W before the sweep (restored on fallback)
-  cd L[MB][MB * (MB + 1) / 2];   // Cholesky factor of each Q_mu, packed lower
-  double dinv[MB][MB];           // 1 / L(c, c)
+  cd Qi[MB][MB * (MB + 1) / 2];  // Q_mu^-1 of each mu, packed upper triangle (herm_inverse_thread)
   int ok[MB];
 };
 
@@ -279,130 +278,75 @@ __device__ __forceinline__ cd shfl4(unsigned mask, cd v, int src) {
   return cd{__shfl_sync(mask, v.re, src, 4), __shfl_sync(mask, v.im, src, 4)};
 }
 
-// Cholesky Q_mu = L L^H of one weighted covariance (Hermitian, packed upper
-// triangle qp), one thread; false when Q_mu is not numerically positive
-// definite (the exact fallback then decides, as the reference's LU would).
+// Q_mu^-1 of one weighted covariance (Hermitian, packed upper triangle qp)
+// through its Cholesky factor: Q = L L^H, Q^-1 = L^-H L^-1, packed upper
+// into qi.  One thread; false when Q_mu is not numerically positive definite
+// (the exact fallback then decides, as the reference's LU would).  It runs
+// for every mu at once before the sweep, so the sweep's dependent chain per
+// column is products with Q_mu^-1 instead of two triangular solves.
 template <int MB>
-__device__ bool chol_thread(const cd* qp, cd* L, double* dinv) {
+__device__ bool herm_inverse_thread(const cd* qp, cd* qi) {
   auto Q = [&](int r, int c) -> cd { return r <= c ? qp[c * (c + 1) / 2 + r] : conjg(qp[r * (r + 1) / 2 + c]); };
-  auto Li = [](int r, int c) { return r * (r + 1) / 2 + c; };
+  cd L[MB][MB], Li[MB][MB];  // lower triangles (registers; the loops are unrolled)
+  double dinv[MB];
 #pragma unroll
   for (int c = 0; c < MB; ++c) {
     double d = Q(c, c).re;
 #pragma unroll
-    for (int k = 0; k < c; ++k) d -= norm2(L[Li(c, k)]);
+    for (int k = 0; k < c; ++k) d -= norm2(L[c][k]);
     if (!(d > 0.0) || !isfinite(d)) return false;
-    const double il = rsqrt_pos(d);  // 1 / sqrt(d) without the IEEE sqrt + divide chain
-    dinv[c] = il;
-    L[Li(c, c)] = cd{d * il, 0.0};
+    dinv[c] = rsqrt_pos(d);  // 1 / sqrt(d) without the IEEE sqrt + divide chain
 #pragma unroll
     for (int r = c + 1; r < MB; ++r) {
       cd s = Q(r, c);
 #pragma unroll
-      for (int k = 0; k < c; ++k) s = s - L[Li(r, k)] * conjg(L[Li(c, k)]);
-      L[Li(r, c)] = s * dinv[c];
+      for (int k = 0; k < c; ++k) s = s - L[r][k] * conjg(L[c][k]);
+      L[r][c] = s * dinv[c];
     }
   }
+  // L^-1 column by column: Li(c, c) = 1 / L(c, c), Li(r, c) = -(sum_k L(r, k) Li(k, c)) / L(r, r)
+#pragma unroll
+  for (int c = 0; c < MB; ++c) {
+    Li[c][c] = cd{dinv[c], 0.0};
+#pragma unroll
+    for (int r = c + 1; r < MB; ++r) {
+      cd s = L[r][c] * dinv[c];
+#pragma unroll
+      for (int k = c + 1; k < r; ++k) s = cfma(s, L[r][k], Li[k][c]);
+      Li[r][c] = cd{-s.re * dinv[r], -s.im * dinv[r]};
+    }
+  }
+  // Q^-1(i, j) = sum_{k >= j} conj(Li(k, i)) Li(k, j), i <= j
+#pragma unroll
+  for (int j = 0; j < MB; ++j)
+#pragma unroll
+    for (int i = 0; i <= j; ++i) {
+      cd s{0.0, 0.0};
+#pragma unroll
+      for (int k = j; k < MB; ++k) s = cfmac(s, Li[k][i], Li[k][j]);
+      if (i == j) s.im = 0.0;
+      qi[j * (j + 1) / 2 + i] = s;
+    }
   return true;
 }
 
-// Fast IP sweep of one system (engine.cpp:40-51 for mu = 0..MB-1):
-//   u = (W^H Q_mu)^-1 e_mu = Q_mu^-1 W^-H e_mu  (two triangular solves),
-//   u /= sqrt(max(Re(u^H Q u), floor)),  W[:, mu] = u,
-//   W^-1 refreshed by Sherman-Morrison for the replaced column.
-// Every column still passes the reference's test ||W^H Q u - e_mu|| <= 1e-6
-// (with the current W, as engine.cpp:47-49); any failure returns false and
-// the caller reruns the exact LU + pinv sweep from W_old.
-template <int MB>
-__device__ bool ip_sweep_fast(cd* W, IpWork<MB>& f, const cd* qb, double floor_) {
-  constexpr int E = MB * (MB + 1) / 2;
-#pragma unroll
-  for (int mu = 0; mu < MB; ++mu)
-    if (!f.ok[mu]) return false;
-  auto Li = [](int r, int c) { return r * (r + 1) / 2 + c; };
-#pragma unroll 1
-  for (int mu = 0; mu < MB; ++mu) {
-    const cd* qp = qb + mu * E;
-    auto Q = [&](int r, int c) -> cd { return r <= c ? qp[c * (c + 1) / 2 + r] : conjg(qp[r * (r + 1) / 2 + c]); };
-    const cd* L = f.L[mu];
-    const double* di = f.dinv[mu];
-    cd u[MB];
-    // L y = W^-H e_mu  (b_k = conj(Winv(mu, k)))
-#pragma unroll
-    for (int r = 0; r < MB; ++r) {
-      cd s = conjg(f.Winv[r * MB + mu]);
-#pragma unroll
-      for (int c = 0; c < r; ++c) s = s - L[Li(r, c)] * u[c];
-      u[r] = s * di[r];
-    }
-    // L^H u = y
-#pragma unroll
-    for (int r = MB - 1; r >= 0; --r) {
-      cd s = u[r];
-#pragma unroll
-      for (int c = r + 1; c < MB; ++c) s = s - cmulc(L[Li(c, r)], u[c]);
-      u[r] = s * di[r];
-    }
-    cd qu[MB];
-    bool fin = true;
-#pragma unroll
-    for (int a = 0; a < MB; ++a) {
-      fin = fin && cfinite(u[a]);
-      cd s{0.0, 0.0};
-#pragma unroll
-      for (int c = 0; c < MB; ++c) s = s + Q(a, c) * u[c];
-      qu[a] = s;
-    }
-    double r2 = 0.0, nq = 0.0;
-#pragma unroll
-    for (int a = 0; a < MB; ++a) {
-      cd s{0.0, 0.0};
-#pragma unroll
-      for (int k = 0; k < MB; ++k) s = s + cmulc(W[a * MB + k], qu[k]);
-      if (a == mu) s.re -= 1.0;
-      r2 += norm2(s);
-      nq += cmulc(u[a], qu[a]).re;
-    }
-    if (!fin || !(r2 <= kFastResid2)) return false;  // guard band (kFastResid)
-    const double sc = sqrt(fmax(nq, floor_));
-    cd d[MB];
-#pragma unroll
-    for (int a = 0; a < MB; ++a) {
-      u[a] = cdivr(u[a], sc);
-      d[a] = u[a] - W[mu * MB + a];
-    }
-    // Sherman-Morrison: (W + d e_mu^T)^-1 = W^-1 - z (e_mu^T W^-1) / (1 + z_mu), z = W^-1 d
-    cd z[MB];
-#pragma unroll
-    for (int r = 0; r < MB; ++r) {
-      cd s{0.0, 0.0};
-#pragma unroll
-      for (int c = 0; c < MB; ++c) s = s + f.Winv[c * MB + r] * d[c];
-      z[r] = s;
-    }
-    const cd den = cd{1.0 + z[mu].re, z[mu].im};
-    const double dn = norm2(den);
-    if (!(dn > 0.0)) return false;
-    const cd iden{den.re / dn, -den.im / dn};
-    cd row[MB];
-#pragma unroll
-    for (int c = 0; c < MB; ++c) row[c] = f.Winv[c * MB + mu] * iden;
-#pragma unroll
-    for (int c = 0; c < MB; ++c)
-#pragma unroll
-      for (int r = 0; r < MB; ++r) f.Winv[c * MB + r] = f.Winv[c * MB + r] - z[r] * row[c];
-#pragma unroll
-    for (int a = 0; a < MB; ++a) W[mu * MB + a] = u[a];
-  }
-  return true;
-}
-
-// Quad-cooperative version of ip_sweep_fast: the MB (<= 4) lanes of one
-// 4-lane segment own rows l of the triangular solves, of Q u, of the
-// residual and of the Sherman-Morrison update, exchanging values with
-// width-4 shuffles.  Same algebra and the same reference residual test as
-// ip_sweep_fast; every early exit is uniform across the quad.
-
+// Fast IP sweep of one (bin, block) system with MB <= 4 by the MB lanes of a
+// 4-lane segment (engine.cpp:40-51 for mu = 0..MB-1), lane l owning row l:
+//   v = W^-H e_mu (row mu of W^-1, conjugated),  u = Q_mu^-1 v
+//     (= (W^H Q_mu)^-1 e_mu),
+//   u /= sqrt(max(Re(u^H Q u), floor)) with u^H Q u = Re(v^H u),
+//   W[:, mu] = u, and W^-1 refreshed by Sherman-Morrison for the replaced
+//   column: z = W^-1 (u - w_mu), W^-1 -= z (e_mu^T W^-1) / (1 + z_mu).
+// The dependent chain of a column is: the row of W^-1 (shared memory), one
+// matrix-vector product, the normaliser's reciprocal square root, the
+// reciprocal of 1 + z_mu, one update.  Everything else hangs off the chain:
+// W^-1 u and W^-1 w_mu run beside the normaliser (z = W^-1 u / sqrt(.) -
+// W^-1 w_mu), and the reference's test ||W^H Q u - e_mu|| (with the current
+// W, as engine.cpp:47-49) and the finiteness checks are recorded per column
+// and evaluated once after the sweep.  Every column must pass the test
+// within the guard band (kFastResid); any failure returns false and the
+// caller reruns the exact LU + pinv sweep from W_old, so deferring the test
+// changes no result.  The flags are uniform across the quad.
 template <int MB>
 __device__ bool ip_sweep_quad(cd* W, IpWork<MB>& f, const cd* qb, double floor_, int l, unsigned mask) {
   constexpr int E = MB * (MB + 1) / 2;
@@ -410,91 +354,85 @@ __device__ bool ip_sweep_quad(cd* W, IpWork<MB>& f, const cd* qb, double floor_,
 #pragma unroll
   for (int mu = 0; mu < MB; ++mu) okall = okall && f.ok[mu];
   if (!okall) return false;
-  auto Li = [](int r, int c) { return r * (r + 1) / 2 + c; };
   const bool act = l < MB;
   const int la = act ? l : 0;
+  bool bad = false;
 #pragma unroll 1
   for (int mu = 0; mu < MB; ++mu) {
-    const cd* L = f.L[mu];
-    const double* di = f.dinv[mu];
     const cd* qp = qb + mu * E;
+    const cd* qi = f.Qi[mu];
     auto Q = [&](int r, int c) -> cd { return r <= c ? qp[c * (c + 1) / 2 + r] : conjg(qp[r * (r + 1) / 2 + c]); };
-    // forward: L y = b, b_l = conj(Winv(mu, l))
-    cd acc = act ? conjg(f.Winv[la * MB + mu]) : cd{0.0, 0.0};
-    cd y{0.0, 0.0};
+    auto QI = [&](int r, int c) -> cd { return r <= c ? qi[c * (c + 1) / 2 + r] : conjg(qi[r * (r + 1) / 2 + c]); };
+    cd v[MB], wi[MB];  // v = conj(row mu of W^-1); wi = row la of W^-1
 #pragma unroll
     for (int c = 0; c < MB; ++c) {
-      if (l == c) y = acc * di[c];
-      const cd yc = shfl4(mask, y, c);
-      if (act && l > c) acc = acc - L[Li(la, c)] * yc;
+      v[c] = conjg(f.Winv[c * MB + mu]);
+      wi[c] = f.Winv[c * MB + la];
     }
-    // backward: L^H u = y
-    acc = y;
-    cd u{0.0, 0.0};
+    // u_l = sum_c Q^-1(l, c) v_c on two accumulators
+    cd u0{0.0, 0.0}, u1{0.0, 0.0};
 #pragma unroll
-    for (int c = MB - 1; c >= 0; --c) {
-      if (l == c) u = acc * di[c];
-      const cd uc = shfl4(mask, u, c);
-      if (act && l < c) acc = acc - cmulc(L[Li(c, la)], uc);
+    for (int c = 0; c < MB; c += 2) {
+      u0 = cfma(u0, QI(la, c), v[c]);
+      if (c + 1 < MB) u1 = cfma(u1, QI(la, c + 1), v[c + 1]);
     }
+    const cd u = u0 + u1;
     cd uv[MB];
-    bool fin = true;
 #pragma unroll
-    for (int c = 0; c < MB; ++c) {
-      uv[c] = shfl4(mask, u, c);
-      fin = fin && cfinite(uv[c]);
+    for (int c = 0; c < MB; ++c) uv[c] = shfl4(mask, u, c);
+    // Re(u^H Q u) = Re(v^H u); beside it z' = W^-1 u and t = W^-1 w_mu (row la)
+    double n0 = 0.0, n1 = 0.0;
+    cd z0{0.0, 0.0}, z1{0.0, 0.0}, t0{0.0, 0.0}, t1{0.0, 0.0};
+#pragma unroll
+    for (int c = 0; c < MB; c += 2) {
+      n0 = fma(v[c].re, uv[c].re, fma(v[c].im, uv[c].im, n0));
+      z0 = cfma(z0, wi[c], uv[c]);
+      t0 = cfma(t0, wi[c], W[mu * MB + c]);
+      if (c + 1 < MB) {
+        n1 = fma(v[c + 1].re, uv[c + 1].re, fma(v[c + 1].im, uv[c + 1].im, n1));
+        z1 = cfma(z1, wi[c + 1], uv[c + 1]);
+        t1 = cfma(t1, wi[c + 1], W[mu * MB + c + 1]);
+      }
     }
-    cd qu{0.0, 0.0};
-    if (act)
+    const double nq = n0 + n1;
+    const cd zp = z0 + z1, tt = t0 + t1;
+    // off the chain: the reference's residual W^H (Q u) - e_mu with the current W
+    {
+      bool fin = true;
 #pragma unroll
-      for (int c = 0; c < MB; ++c) qu = qu + Q(la, c) * uv[c];
-    cd quv[MB];
+      for (int c = 0; c < MB; ++c) fin = fin && cfinite(uv[c]);
+      cd qu{0.0, 0.0};
+      if (act)
 #pragma unroll
-    for (int c = 0; c < MB; ++c) quv[c] = shfl4(mask, qu, c);
-    double r2 = 0.0, nq = 0.0;
-    if (act) {
+        for (int c = 0; c < MB; ++c) qu = cfma(qu, Q(la, c), uv[c]);
       cd r{0.0, 0.0};
 #pragma unroll
-      for (int k = 0; k < MB; ++k) r = r + cmulc(W[la * MB + k], quv[k]);
+      for (int k = 0; k < MB; ++k) r = cfmac(r, W[la * MB + k], shfl4(mask, qu, k));
       if (l == mu) r.re -= 1.0;
-      r2 = norm2(r);
-      nq = cmulc(u, qu).re;
+      double r2 = act ? norm2(r) : 0.0;
+      r2 += __shfl_xor_sync(mask, r2, 1, 4);
+      r2 += __shfl_xor_sync(mask, r2, 2, 4);
+      bad = bad || !fin || !(r2 <= kFastResid2);  // guard band (kFastResid)
     }
-    r2 += __shfl_xor_sync(mask, r2, 1, 4);
-    r2 += __shfl_xor_sync(mask, r2, 2, 4);
-    nq += __shfl_xor_sync(mask, nq, 1, 4);
-    nq += __shfl_xor_sync(mask, nq, 2, 4);
-    // ||W^H Q u - e_mu|| within the guard band under the reference's 1e-6
-    // (kFastResid): near the threshold the exact LU path decides
-    if (!fin || !(r2 <= kFastResid2)) return false;
     const double isc = rsqrt_pos(fmax(nq, floor_));
     const cd un{u.re * isc, u.im * isc};
-    const cd d = act ? un - W[mu * MB + la] : cd{0.0, 0.0};
-    cd dv[MB];
-#pragma unroll
-    for (int c = 0; c < MB; ++c) dv[c] = shfl4(mask, d, c);
-    cd z{0.0, 0.0};
-    if (act)
-#pragma unroll
-      for (int c = 0; c < MB; ++c) z = z + f.Winv[c * MB + la] * dv[c];
+    const cd z{fma(zp.re, isc, -tt.re), fma(zp.im, isc, -tt.im)};
     const cd zmu = shfl4(mask, z, mu);
     const cd den{1.0 + zmu.re, zmu.im};
     const double dn = norm2(den);
-    if (!(dn > 0.0)) return false;
+    bad = bad || !(dn > 0.0) || !isfinite(dn);
     const double idn = rcp_pos(dn);
     const cd iden{den.re * idn, -den.im * idn};
-    cd row[MB];
-#pragma unroll
-    for (int c = 0; c < MB; ++c) row[c] = f.Winv[c * MB + mu] * iden;
-    __syncwarp(mask);
+    const cd zi = z * iden;
+    __syncwarp(mask);  // every lane has read row mu of W^-1 and column mu of W
     if (act) {
 #pragma unroll
-      for (int c = 0; c < MB; ++c) f.Winv[c * MB + la] = f.Winv[c * MB + la] - z * row[c];
+      for (int c = 0; c < MB; ++c) f.Winv[c * MB + la] = wi[c] - zi * conjg(v[c]);
       W[mu * MB + la] = un;
     }
     __syncwarp(mask);
   }
-  return true;
+  return !bad;
 }
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
@@ -506,6 +444,16 @@ __device__ __forceinline__ void cp_async16_hint(void* smem_dst, const void* gmem
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
   asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem_src), "l"(pol)
                : "memory");
+}
+// the same with the destination given as a 32-bit shared-memory address
+__device__ __forceinline__ void cp_async16_hint_s(unsigned s, const void* gmem_src, unsigned long long pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem_src), "l"(pol)
+               : "memory");
+}
+// v through a warp shuffle from the lane itself: a per-thread register the
+// compiler cannot split into register + uniform-register parts (all 32 lanes)
+__device__ __forceinline__ unsigned opaque_u32(unsigned v) {
+  return __shfl_sync(0xffffffffu, v, (int)(threadIdx.x & 31));
 }
 __device__ __forceinline__ unsigned long long l2_evict_last() {
   unsigned long long p;

@@ -26,7 +26,7 @@ __global__ void k_ip(const cd* Wg, const cd* Qg, long long* cyc, cd* Wout, int r
       logdet2_inverse_thread<4>(W, w.Winv);
     }
     __syncthreads();
-    if (tid < 4) w.ok[tid] = chol_thread<4>(Q + tid * 10, w.L[tid], w.dinv[tid]) ? 1 : 0;
+    if (tid < 4) w.ok[tid] = herm_inverse_thread<4>(Q + tid * 10, w.Qi[tid]) ? 1 : 0;
     __syncthreads();
     if (r == 0 && tid == 0) printf("chol ok %d %d %d %d\n", w.ok[0], w.ok[1], w.ok[2], w.ok[3]);
     if (r == reps - 1 && tid == 0) t0 = clock64();
