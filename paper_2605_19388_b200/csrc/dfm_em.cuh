@@ -1331,19 +1331,20 @@ __device__ __forceinline__ void spec_rows(int F, int T, int N, int K, int n, int
   }
 }
 
-template <int KS>
+template <int KS, int TW = 1>  // TW tiles of 8 frames from t0 (T rows loaded once for all of them)
 __device__ __forceinline__ void spec_cols(int F, int T, int N, int K, int n, int t0, const double* __restrict__ Tf,
                                           const double* __restrict__ V, double* __restrict__ H, int warp, int nwarps,
                                           int lane, const double* __restrict__ tgt = nullptr, double eps = 0.0,
                                           double* __restrict__ Aw = nullptr, double* __restrict__ Bw = nullptr) {
-  const int g = lane >> 2, q = lane & 3, tl = t0 + g;
-  double b[KS];
+  const int g = lane >> 2, q = lane & 3;
+  double b[TW][KS];
 #pragma unroll
-  for (int s = 0; s < KS; ++s) {
-    const int k = 4 * s + q;
-    b[s] = (k < K && tl < T) ? V[((size_t)n * K + k) * T + tl] : 0.0;
-  }
-  const int t = t0 + 2 * q;
+  for (int w = 0; w < TW; ++w)
+#pragma unroll
+    for (int s = 0; s < KS; ++s) {
+      const int k = 4 * s + q, tl = t0 + 8 * w + g;
+      b[w][s] = (k < K && tl < T) ? V[((size_t)n * K + k) * T + tl] : 0.0;
+    }
   constexpr int kSpecBatch = spec_batch<KS>();
   const int ntile = (F + 7) / 8;
   for (int tb = warp; tb < ntile; tb += kSpecBatch * nwarps) {
@@ -1362,17 +1363,21 @@ __device__ __forceinline__ void spec_cols(int F, int T, int N, int K, int n, int
       const int tile = tb + u * nwarps;
       if (tile >= ntile) break;
       const int f = tile * 8 + g;
-      double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-      for (int s = 0; s < KS; ++s) dmma(c0, c1, a[u][s], b[s]);
-      if (tgt && f < F) is_weights2(F, T, N, n, f, t, c0, c1, tgt, eps, Aw, Bw);  // rec is stored too (divergence)
-      if (f < F) {
-        double* hp = H + ((size_t)f * N + n) * T;
-        if (!(T & 1) && t + 1 < T) {
-          *reinterpret_cast<double2*>(hp + t) = make_double2(c0, c1);
-        } else {
-          if (t < T) hp[t] = c0;
-          if (t + 1 < T) hp[t + 1] = c1;
+      for (int w = 0; w < TW; ++w) {
+        const int t = t0 + 8 * w + 2 * q;
+        double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+        for (int s = 0; s < KS; ++s) dmma(c0, c1, a[u][s], b[w][s]);
+        if (tgt && f < F) is_weights2(F, T, N, n, f, t, c0, c1, tgt, eps, Aw, Bw);  // rec is stored too (divergence)
+        if (f < F) {
+          double* hp = H + ((size_t)f * N + n) * T;
+          if (!(T & 1) && t + 1 < T) {
+            *reinterpret_cast<double2*>(hp + t) = make_double2(c0, c1);
+          } else {
+            if (t < T) hp[t] = c0;
+            if (t + 1 < T) hp[t + 1] = c1;
+          }
         }
       }
     }
@@ -1554,11 +1559,19 @@ __global__ void __launch_bounds__(32 * WARPS, WARPS > 8 ? 1 : (KT <= 2 ? 3 : 2))
 }
 
 // V update (engine.cpp:125-133): num[k][t] = sum_f T[f][n][k] A'[n][f][t].
-// CTA = (8 frames, source); its 4 warps split the bins, partials are added
+// CTA = (8 TW frames, source); its 8 warps split the bins, partials are added
 // in warp order; apply in place or write {num, den} for the allreduce.
+// TW = 2 (even T, even K, KT even): a lane loads a PAIR of frames of its bin
+// row (one 16-byte load each of A' and B': tile w of the CTA is frames
+// t0 + 2 c + w, c = 0..7) and KT consecutive bases of its T row (16-byte
+// loads: DMMA row g of base tile j is base KT g + j), so a k-step of 4 bins
+// touches 12 shared-memory-sized (128-byte) lines for 16 frames where the
+// 8-frame CTA touches 16 for 8, and every T row is read by half as many CTAs.
+// Each (base, frame) still sums the bins in the same order: the results are
+// the TW = 1 kernel's bitwise.
 constexpr int kVupdMWarps = 8;
-template <int KT>
-__global__ void __launch_bounds__(32 * kVupdMWarps, KT <= 2 ? 3 : 2) k_vupd_mma(int F, int T, int N, int K,
+template <int KT, int TW = 1>
+__global__ void __launch_bounds__(32 * kVupdMWarps, (KT * TW) <= 2 ? 3 : 2) k_vupd_mma(int F, int T, int N, int K,
                                                               const double* __restrict__ Tf,
                                                               const double* __restrict__ Aw,
                                                               const double* __restrict__ Bw,
@@ -1567,21 +1580,53 @@ __global__ void __launch_bounds__(32 * kVupdMWarps, KT <= 2 ? 3 : 2) k_vupd_mma(
                                                               double* __restrict__ Hout,
                                                               const double* __restrict__ tgt = nullptr,
                                                               int n_base = 0, StageClock* sc = nullptr) {
-  __shared__ double part[kVupdMWarps / 2][2][KT][64];
+  static_assert(TW == 1 || (TW == 2 && KT % 2 == 0), "frame pairs need an even number of base tiles");
+  constexpr int JT = KT * TW;  // accumulator tiles: (frame tile w, base tile j) -> w * KT + j
+  __shared__ double part[kVupdMWarps / 2][2][JT][64];
   const unsigned long long tr0 = ctatr_begin(2);
   sc_tick(sc, kScVupd);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
-  const int n = n_base + blockIdx.y, t0 = blockIdx.x * 8;  // n_base: source chunk (sharded overlap)
+  const int n = n_base + blockIdx.y, t0 = blockIdx.x * 8 * TW;  // n_base: source chunk (sharded overlap)
   if (skip && skip[n]) return;  // IS-NMF: this source has converged
   constexpr int kt = KT;
   const int steps = (F + 3) / 4;
   const int per = (steps + kVupdMWarps - 1) / kVupdMWarps;
   const int s0 = warp * per, s1 = min(steps, s0 + per);
-  constexpr int U = KT <= 1 ? 8 : 4;  // k-steps whose operands are loaded before their DMMAs
-  double num[KT][2], den[KT][2];
+  constexpr int U = JT <= 1 ? 8 : 4;  // k-steps whose operands are loaded before their DMMAs
+  double num[JT][2], den[JT][2];
 #pragma unroll
-  for (int j = 0; j < KT; ++j) num[j][0] = num[j][1] = den[j][0] = den[j][1] = 0.0;
+  for (int j = 0; j < JT; ++j) num[j][0] = num[j][1] = den[j][0] = den[j][1] = 0.0;
+  if constexpr (TW == 2) {
+    const int tp = t0 + 2 * g;  // the lane's frame pair (T even: whole or absent)
+    for (int sb = s0; sb < s1; sb += U) {
+      double2 av[U], bv[U], ta[U][KT / 2];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int f = 4 * (sb + u) + q;
+        const bool okf = sb + u < s1 && f < F;
+        const size_t ro = ((size_t)n * F + (okf ? f : 0)) * T + tp;
+        av[u] = (okf && tp < T) ? __ldg(reinterpret_cast<const double2*>(Aw + ro)) : make_double2(0.0, 0.0);
+        bv[u] = (okf && tp < T) ? __ldg(reinterpret_cast<const double2*>(Bw + ro)) : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < KT; j += 2) {
+          const int k = KT * g + j;  // K even: k + 1 < K too
+          ta[u][j / 2] = (okf && k < K) ? __ldg(reinterpret_cast<const double2*>(Tf + ((size_t)f * N + n) * K + k))
+                                        : make_double2(0.0, 0.0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < KT; ++j) {
+          const double tj = (j & 1) ? ta[u][j / 2].y : ta[u][j / 2].x;
+          dmma(num[j][0], num[j][1], tj, av[u].x);
+          dmma(den[j][0], den[j][1], tj, bv[u].x);
+          dmma(num[KT + j][0], num[KT + j][1], tj, av[u].y);
+          dmma(den[KT + j][0], den[KT + j][1], tj, bv[u].y);
+        }
+    }
+  } else {
   const int tb = t0 + g;
   for (int sb = s0; sb < s1; sb += U) {
     double av[U], bv[U], ta[U][KT];
@@ -1606,12 +1651,13 @@ __global__ void __launch_bounds__(32 * kVupdMWarps, KT <= 2 ? 3 : 2) k_vupd_mma(
           dmma(den[j][0], den[j][1], ta[u][j], bv[u]);
         }
   }
+  }
   // fixed-order tree over the warps: w += w + h for h = W/2, W/4, ..., 1
 #pragma unroll
   for (int h = kVupdMWarps / 2; h >= 1; h >>= 1) {
     if (warp >= h && warp < 2 * h)
 #pragma unroll
-      for (int j = 0; j < KT; ++j) {
+      for (int j = 0; j < JT; ++j) {
         part[warp - h][0][j][2 * lane] = num[j][0];
         part[warp - h][0][j][2 * lane + 1] = num[j][1];
         part[warp - h][1][j][2 * lane] = den[j][0];
@@ -1620,7 +1666,7 @@ __global__ void __launch_bounds__(32 * kVupdMWarps, KT <= 2 ? 3 : 2) k_vupd_mma(
     __syncthreads();
     if (warp < h)
 #pragma unroll
-      for (int j = 0; j < KT; ++j) {
+      for (int j = 0; j < JT; ++j) {
         num[j][0] += part[warp][0][j][2 * lane];
         num[j][1] += part[warp][0][j][2 * lane + 1];
         den[j][0] += part[warp][1][j][2 * lane];
@@ -1631,27 +1677,29 @@ __global__ void __launch_bounds__(32 * kVupdMWarps, KT <= 2 ? 3 : 2) k_vupd_mma(
   __syncthreads();
   if (warp == 0) {
 #pragma unroll
-    for (int j = 0; j < KT; ++j)
-      if (j < kt)
+    for (int jj = 0; jj < JT; ++jj)
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int k = 8 * j + g, t = t0 + 2 * q + i;
-          if (k >= K || t >= T) continue;
-          const double nu = num[j][i], de = den[j][i];
-          const size_t o = ((size_t)n * K + k) * T + t;
-          if (numden) {
-            numden[o] = nu;
-            numden[(size_t)N * K * T + o] = de;
-          } else {
-            V[o] = fmax(V[o] * sqrt(nu / fmax(de, floor_)), floor_);
-          }
+      for (int i = 0; i < 2; ++i) {
+        const int w = jj / KT, j = jj - w * KT;
+        // accumulator row g, column 2 q + i of tile (w, j)
+        const int k = TW == 2 ? KT * g + j : 8 * j + g;
+        const int t = TW == 2 ? t0 + 2 * (2 * q + i) + w : t0 + 2 * q + i;
+        if (k >= K || t >= T) continue;
+        const double nu = num[jj][i], de = den[jj][i];
+        const size_t o = ((size_t)n * K + k) * T + t;
+        if (numden) {
+          numden[o] = nu;
+          numden[(size_t)N * K * T + o] = de;
+        } else {
+          V[o] = fmax(V[o] * sqrt(nu / fmax(de, floor_)), floor_);
         }
+      }
   }
   if (!Hout || numden) return;  // sharded: V is final only after the allreduce
   __syncthreads();  // the CTA's new V columns are visible
   // H = T V_new (IS-NMF: and the next iteration's weights)
-  spec_cols<2 * KT>(F, T, N, K, n, t0, Tf, V, Hout, warp, kVupdMWarps, lane, tgt, floor_, const_cast<double*>(Aw),
-                    const_cast<double*>(Bw));
+  spec_cols<2 * KT, TW>(F, T, N, K, n, t0, Tf, V, Hout, warp, kVupdMWarps, lane, tgt, floor_, const_cast<double*>(Aw),
+                        const_cast<double*>(Bw));
   if (g_ctatr[2]) {
     __syncthreads();
     ctatr_end(2, tr0);

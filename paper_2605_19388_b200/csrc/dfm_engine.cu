@@ -478,13 +478,24 @@ void ensure_comm_resources(dfm_ctx* c) {
 }
 
 void launch_vupd(dfm_ctx* c) {
-  const dim3 grid((c->T + 7) / 8, c->N);
   const bool sharded = collective(c) || c->host_exchange;
   auto kern = k_vupd_mma<8>;
-  switch ((c->K + 7) / 8) {
+  // frame pairs per lane (k_vupd_mma<KT, 2>: 16 frames per CTA) for even T and K
+  static const bool no_pairs = getenv("DFM_VUPD_PAIRS") && atoi(getenv("DFM_VUPD_PAIRS")) == 0;
+  const int kt8 = (c->K + 7) / 8;
+  static int sms = 0;
+  if (!sms) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  // measured: config 3 (512 pair CTAs) 226 -> 198 us; config 1 (200 pair CTAs,
+  // one or two per SM) 22.2 -> 24.2 us -- the small grid is latency-bound and
+  // wants the CTAs, so pairs need two full rounds of CTAs per SM
+  const bool pairs = !no_pairs && !(c->T & 1) && !(c->K & 1) && kt8 >= 2 && kt8 <= 4 &&
+                     (long long)((c->T + 15) / 16) * c->N >= 2ll * sms;
+  const int tw = pairs ? 2 : 1;
+  const dim3 grid((c->T + 8 * tw - 1) / (8 * tw), c->N);
+  switch (kt8) {
     case 1: kern = k_vupd_mma<1>; break;
-    case 2: kern = k_vupd_mma<2>; break;
-    case 3: case 4: kern = k_vupd_mma<4>; break;
+    case 2: kern = pairs ? k_vupd_mma<2, 2> : k_vupd_mma<2>; break;
+    case 3: case 4: kern = pairs ? k_vupd_mma<4, 2> : k_vupd_mma<4>; break;
     default: kern = k_vupd_mma<8>; break;
   }
   if (!sharded || c->host_exchange) {
@@ -508,7 +519,7 @@ void launch_vupd(dfm_ctx* c) {
   ensure_comm_resources(c);
   for (int j = 0; j < nch; ++j) {
     const int n0 = c->N * j / nch, n1 = c->N * (j + 1) / nch;
-    const dim3 gj((c->T + 7) / 8, n1 - n0);
+    const dim3 gj(grid.x, n1 - n0);
     kern<<<gj, 32 * kVupdMWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->Aw.p, c->Bw.p, c->V.p,
                                                  c->numden.p, c->floor_, nullptr, nullptr, nullptr, n0,
                                                  c->stage.p);
