@@ -634,15 +634,33 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
       }
       __syncthreads();
     }
-    if constexpr (cs > 1) cl_sync();  // every CTA's frame partials are in its red[]
+    const int nslices = (FSJ && fsj) ? nwarps : SL;
+    if constexpr (cs > 1) {
+      // each CTA first adds its own slices into slice 0 (local shared memory),
+      // so only one value per CTA crosses the cluster (a remote load is ~1 us)
+      for (int q = tid; q < NM; q += FT) {
+        double nu = 0.0, de = 0.0;
+        for (int s = 0; s < nslices; ++s) {
+          nu += red[2 * (s * NM + q)];
+          de += red[2 * (s * NM + q) + 1];
+        }
+        red[2 * q] = nu;
+        red[2 * q + 1] = de;
+      }
+      cl_sync();  // every CTA's frame partials are in slice 0 of its red[]
+    }
     for (int q = tid; q < NM; q += FT) {
       double nu = 0.0, de = 0.0;
-      const int nslices = (FSJ && fsj) ? nwarps : SL;
-      for (int r = 0; r < cs; ++r) {
-        const double* rr = cs > 1 ? cl_peer(red, r) : red;
+      if constexpr (cs > 1) {
+        for (int r = 0; r < cs; ++r) {
+          const double* rr = cl_peer(red, r);
+          nu += rr[2 * q];
+          de += rr[2 * q + 1];
+        }
+      } else {
         for (int s = 0; s < nslices; ++s) {
-          nu += rr[2 * (s * NM + q)];
-          de += rr[2 * (s * NM + q) + 1];
+          nu += red[2 * (s * NM + q)];
+          de += red[2 * (s * NM + q) + 1];
         }
       }
       double& l = Lsm[q];
@@ -920,12 +938,28 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
   cost = warp_sum(cost);
   if ((tid & 31) == 0) wsum[tid >> 5] = cost;
   __syncthreads();
-  if constexpr (cs > 1) cl_sync();  // the peers' cost and Q partials are complete
+  if constexpr (cs > 1) {
+    // each CTA first adds its own Q slices into slice 0 (see the Lambda reduction)
+    if (a.start)
+      for (int idx = tid; idx < nitems * MAXMB; idx += FT) {
+        const int it = idx / MAXMB, mu = idx - it * MAXMB;
+        cd sum{0.0, 0.0};
+        for (int s = 0; s < SQ; ++s) sum = sum + qpart[mu * (SQ * nitems) + s * nitems + it];
+        qpart[mu * (SQ * nitems) + it] = sum;
+      }
+    if (tid == 0) {  // and its warps' cost terms into wsum[0]
+      double c = 0.0;
+      for (int w = 0; w < sp.nwarps; ++w) c += wsum[w];
+      wsum[0] = c;
+    }
+    cl_sync();  // the peers' cost and Q partials are complete
+  }
   if (tid == 0 && lead) {
     double c = 0.0;
-    for (int r = 0; r < cs; ++r) {
-      const double* ws = cs > 1 ? cl_peer(wsum, r) : wsum;
-      for (int w = 0; w < sp.nwarps; ++w) c += ws[w];
+    if constexpr (cs > 1) {
+      for (int r = 0; r < cs; ++r) c += cl_peer(wsum, r)[0];
+    } else {
+      for (int w = 0; w < sp.nwarps; ++w) c += wsum[w];
     }
     double d = 0.0;
     for (int b = 0; b < nb; ++b) d += ldet[b];
@@ -960,9 +994,10 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     const int mb = MBof(b);
     if (mu >= mb) continue;
     cd sum{0.0, 0.0};
-    for (int r = 0; r < cs; ++r) {
-      const cd* qp = cs > 1 ? cl_peer(qpart, r) : qpart;
-      for (int s = 0; s < SQ; ++s) sum = sum + qp[mu * (SQ * nitems) + s * nitems + it];
+    if constexpr (cs > 1) {
+      for (int r = 0; r < cs; ++r) sum = sum + cl_peer(qpart, r)[mu * (SQ * nitems) + it];
+    } else {
+      for (int s = 0; s < SQ; ++s) sum = sum + qpart[mu * (SQ * nitems) + s * nitems + it];
     }
     const int E = mb * (mb + 1) / 2;
     Qsum[a.qofs[b] + mu * E + rem] = cd{sum.re / (double)T, sum.im / (double)T};
