@@ -1320,13 +1320,15 @@ template <int KS>
 __device__ __forceinline__ void spec_rows(int F, int T, int N, int K, int n, int f0, const double* __restrict__ Tf,
                                           const double* __restrict__ V, double* __restrict__ H, int warp, int nwarps,
                                           int lane, const double* __restrict__ tgt = nullptr, double eps = 0.0,
-                                          double* __restrict__ Aw = nullptr, double* __restrict__ Bw = nullptr) {
+                                          double* __restrict__ Aw = nullptr, double* __restrict__ Bw = nullptr,
+                                          const double* tsm = nullptr) {
   const int g = lane >> 2, q = lane & 3, f = f0 + g;
   double a[KS];
 #pragma unroll
   for (int s = 0; s < KS; ++s) {
     const int k = 4 * s + q;
-    a[s] = (f < F && k < K) ? Tf[((size_t)f * N + n) * K + k] : 0.0;
+    // tsm: the CTA's 8 rows of T [8][4 KS] in shared memory (zero outside F, K)
+    a[s] = tsm ? tsm[g * (4 * KS) + k] : ((f < F && k < K) ? Tf[((size_t)f * N + n) * K + k] : 0.0);
   }
   constexpr int kSpecBatch = spec_batch<KS>();
   const int ntile = (T + 7) / 8;
@@ -1370,7 +1372,8 @@ template <int KS, int TW = 1>  // TW tiles of 8 frames from t0 (T rows loaded on
 __device__ __forceinline__ void spec_cols(int F, int T, int N, int K, int n, int t0, const double* __restrict__ Tf,
                                           const double* __restrict__ V, double* __restrict__ H, int warp, int nwarps,
                                           int lane, const double* __restrict__ tgt = nullptr, double eps = 0.0,
-                                          double* __restrict__ Aw = nullptr, double* __restrict__ Bw = nullptr) {
+                                          double* __restrict__ Aw = nullptr, double* __restrict__ Bw = nullptr,
+                                          const double* vsm = nullptr) {
   const int g = lane >> 2, q = lane & 3;
   double b[TW][KS];
 #pragma unroll
@@ -1378,7 +1381,8 @@ __device__ __forceinline__ void spec_cols(int F, int T, int N, int K, int n, int
 #pragma unroll
     for (int s = 0; s < KS; ++s) {
       const int k = 4 * s + q, tl = t0 + 8 * w + g;
-      b[w][s] = (k < K && tl < T) ? V[((size_t)n * K + k) * T + tl] : 0.0;
+      // vsm: the CTA's columns of V [4 KS][8 TW] in shared memory (zero outside K, T)
+      b[w][s] = vsm ? vsm[k * (8 * TW) + 8 * w + g] : ((k < K && tl < T) ? V[((size_t)n * K + k) * T + tl] : 0.0);
     }
   constexpr int kSpecBatch = spec_batch<KS>();
   const int ntile = (F + 7) / 8;
@@ -1569,24 +1573,31 @@ __global__ void __launch_bounds__(32 * WARPS, WARPS > 8 ? 1 : (KT <= 2 ? 3 : 2))
     __syncthreads();
   }
   __syncthreads();
-  if (warp == 0 && f < F) {
+  // the new rows also go to shared memory [8][8 KT] for the epilogue below
+  // (the reduction buffer is free: its last reads precede the barrier above),
+  // which would otherwise wait one more L2 round trip for them
+  double* tsm = &part[0][0][0][0];
+  if (warp == 0) {
 #pragma unroll
     for (int j = 0; j < KT; ++j)
-      if (j < kt)
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int k = 8 * j + 2 * q + i;
-          if (k >= K) continue;
+      for (int i = 0; i < 2; ++i) {
+        const int k = 8 * j + 2 * q + i;
+        double tv = 0.0;
+        if (f < F && k < K) {
           const double nu = num[j][i], de = den[j][i];
           double* tp = Tf + ((size_t)f * N + n) * K + k;
-          *tp = fmax(*tp * sqrt(nu / fmax(de, floor_)), floor_);
+          tv = fmax(*tp * sqrt(nu / fmax(de, floor_)), floor_);
+          *tp = tv;
         }
+        tsm[g * (8 * KT) + k] = tv;
+      }
   }
   if (!Hout) return;
-  __syncthreads();  // the CTA's new T rows are visible
+  __syncthreads();  // the CTA's new T rows are in tsm
   // h' = T_new V (IS-NMF: the weights of rec = T_new V instead)
   spec_rows<2 * KT>(F, T, N, K, n, f0, Tf, V, Hout, warp, WARPS, lane, tgt, floor_, const_cast<double*>(Aw),
-                    const_cast<double*>(Bw));
+                    const_cast<double*>(Bw), tsm);
   if (g_ctatr[0]) {
     __syncthreads();
     ctatr_end(0, tr0);
@@ -1710,6 +1721,10 @@ __global__ void __launch_bounds__(32 * kVupdMWarps, (KT * TW) <= 2 ? 3 : 2) k_vu
     __syncthreads();
   }
   __syncthreads();
+  // the new columns also go to shared memory [8 KT][8 TW] for the epilogue
+  // below (the reduction buffer is free: its last reads precede the barrier
+  // above), which would otherwise wait one more L2 round trip for them
+  double* vsm = &part[0][0][0][0];
   if (warp == 0) {
 #pragma unroll
     for (int jj = 0; jj < JT; ++jj)
@@ -1718,23 +1733,27 @@ __global__ void __launch_bounds__(32 * kVupdMWarps, (KT * TW) <= 2 ? 3 : 2) k_vu
         const int w = jj / KT, j = jj - w * KT;
         // accumulator row g, column 2 q + i of tile (w, j)
         const int k = TW == 2 ? KT * g + j : 8 * j + g;
-        const int t = TW == 2 ? t0 + 2 * (2 * q + i) + w : t0 + 2 * q + i;
-        if (k >= K || t >= T) continue;
-        const double nu = num[jj][i], de = den[jj][i];
-        const size_t o = ((size_t)n * K + k) * T + t;
-        if (numden) {
-          numden[o] = nu;
-          numden[(size_t)N * K * T + o] = de;
-        } else {
-          V[o] = fmax(V[o] * sqrt(nu / fmax(de, floor_)), floor_);
+        const int tl = TW == 2 ? 2 * (2 * q + i) + w : 2 * q + i, t = t0 + tl;
+        double vv = 0.0;
+        if (k < K && t < T) {
+          const double nu = num[jj][i], de = den[jj][i];
+          const size_t o = ((size_t)n * K + k) * T + t;
+          if (numden) {
+            numden[o] = nu;
+            numden[(size_t)N * K * T + o] = de;
+          } else {
+            vv = fmax(V[o] * sqrt(nu / fmax(de, floor_)), floor_);
+            V[o] = vv;
+          }
         }
+        vsm[k * (8 * TW) + tl] = vv;
       }
   }
   if (!Hout || numden) return;  // sharded: V is final only after the allreduce
-  __syncthreads();  // the CTA's new V columns are visible
+  __syncthreads();  // the CTA's new V columns are in vsm
   // H = T V_new (IS-NMF: and the next iteration's weights)
   spec_cols<2 * KT, TW>(F, T, N, K, n, t0, Tf, V, Hout, warp, kVupdMWarps, lane, tgt, floor_, const_cast<double*>(Aw),
-                        const_cast<double*>(Bw));
+                        const_cast<double*>(Bw), vsm);
   if (g_ctatr[2]) {
     __syncthreads();
     ctatr_end(2, tr0);
@@ -1759,6 +1778,24 @@ __global__ void __launch_bounds__(128, (MB_ * NB_ > 16) ? 4 : 6) k_pdw(const EmA
   sc_tick(a.sc, kScPdw);
   const double* Lg = a.lam + (size_t)f * N * M;
   const bool smemL = M * NP <= kMaxN * 64;
+  // frames above 16 mics: the frame's h' and P loads are issued before the
+  // Lambda staging and its barrier, one L2 round trip for both instead of two
+  // in turn (config 3: 249 -> 229 us; config 1 measured 20.3 -> 20.6 us with
+  // it, so small frames load after the barrier)
+  constexpr bool EARLY = SB && MB_ * NB_ > 16;
+  const bool live = t < T;
+  double h[kMaxN];
+  const double* Pt = a.P + (size_t)f * M * T + t;
+  double pv[SB ? MB_ * NB_ : 1];
+  auto load_frame = [&]() {
+#pragma unroll
+    for (int n = 0; n < kMaxN; ++n) h[n] = (n < N && live) ? __ldg(a.H + ((size_t)f * N + n) * T + t) : 0.0;
+    if constexpr (SB) {
+#pragma unroll
+      for (int m = 0; m < MB_ * NB_; ++m) pv[m] = live ? __ldg(Pt + (size_t)m * T) : 0.0;
+    }
+  };
+  if constexpr (EARLY) load_frame();
   if (smemL)
     for (int e = threadIdx.x; e < M * NP; e += blockDim.x) {
       const int m = e / NP, n = e - m * NP;
@@ -1770,7 +1807,8 @@ __global__ void __launch_bounds__(128, (MB_ * NB_ > 16) ? 4 : 6) k_pdw(const EmA
     for (int e = threadIdx.x; e < N * MS; e += blockDim.x) Lr[e] = Lg[e];
   __syncthreads();
   if (g_ctatr[1] && threadIdx.x == 0) ctatr_end(1, tr0);
-  if (t >= T) return;
+  if (!live) return;
+  if constexpr (!EARLY) load_frame();
   auto load_lam = [&](int m, double* lv) {
     if (smemL) {
 #pragma unroll
@@ -1786,15 +1824,6 @@ __global__ void __launch_bounds__(128, (MB_ * NB_ > 16) ? 4 : 6) k_pdw(const EmA
         if (n < N) lv[n] = Lg[n * M + m];
     }
   };
-  double h[kMaxN];
-#pragma unroll
-  for (int n = 0; n < kMaxN; ++n) h[n] = n < N ? __ldg(a.H + ((size_t)f * N + n) * T + t) : 0.0;
-  const double* Pt = a.P + (size_t)f * M * T + t;
-  double pv[SB ? MB_ * NB_ : 1];
-  if constexpr (SB) {
-#pragma unroll
-    for (int m = 0; m < MB_ * NB_; ++m) pv[m] = __ldg(Pt + (size_t)m * T);
-  }
   double A[kMaxN], B[kMaxN];
 #pragma unroll
   for (int n = 0; n < kMaxN; ++n) A[n] = B[n] = 0.0;
