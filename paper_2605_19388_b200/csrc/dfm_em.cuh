@@ -111,6 +111,11 @@ struct EmArgs {
   double* Bw;        // [N][F][T] T-update weights (B)
   double* P;         // [F][M][T] decorrelated power |W^H x|^2 of the current W
   double* cost_out;  // [F] per-bin cost of this launch's slot
+  // graph replays of a fit: the slot comes from a device counter instead
+  // (cost_out + min(*cost_slot + 1, cost_slot_max) * F; the V update of the
+  // same graph advances the counter), so a replay needs no copy of its costs
+  const int* cost_slot;
+  int cost_slot_max;
   int* fallbacks;
   int finish;  // 1 = cost only (first launch), 2 = Lambda update + cost
   int start;   // 1 = Q, IP, T-update weights
@@ -963,7 +968,9 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     }
     double d = 0.0;
     for (int b = 0; b < nb; ++b) d += ldet[b];
-    a.cost_out[f] = c - (double)T * d;
+    double* co = a.cost_out;
+    if (a.cost_slot) co += (size_t)min(*a.cost_slot + 1, a.cost_slot_max) * (size_t)a.F;
+    co[f] = c - (double)T * d;
   }
   if (!a.start) {
     if constexpr (cs > 1) cl_sync();  // the lead has read the peers' wsum
@@ -1625,8 +1632,12 @@ __global__ void __launch_bounds__(32 * kVupdMWarps, (KT * TW) <= 2 ? 3 : 2) k_vu
                                                               double floor_, const int* __restrict__ skip,
                                                               double* __restrict__ Hout,
                                                               const double* __restrict__ tgt = nullptr,
-                                                              int n_base = 0, StageClock* sc = nullptr) {
+                                                              int n_base = 0, StageClock* sc = nullptr,
+                                                              int* slot_inc = nullptr) {
   static_assert(TW == 1 || (TW == 2 && KT % 2 == 0), "frame pairs need an even number of base tiles");
+  // the fit's cost-slot counter (EmArgs::cost_slot): the bin kernel of this
+  // iteration has finished, the next one has not started
+  if (slot_inc && n_base == 0 && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *slot_inc += 1;
   constexpr int JT = KT * TW;  // accumulator tiles: (frame tile w, base tile j) -> w * KT + j
   __shared__ double part[kVupdMWarps / 2][2][JT][64];
   const unsigned long long tr0 = ctatr_begin(2);

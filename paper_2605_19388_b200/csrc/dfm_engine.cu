@@ -97,6 +97,8 @@ struct dfm_ctx {
   cudaStream_t stream = nullptr;
   DBuf<cd> x, W;
   DBuf<double> Tf, V, lam, H, Aw, Bw, P, numden, cost_part, cost_sum, cost_step;
+  DBuf<int> cost_slot;             // device counter of a fit's graph replays (EmArgs::cost_slot)
+  bool slot_mode = false;          // the launches being captured take their cost slot from cost_slot
   DBuf<cd> Ginv;  // (W^H)^-1 per (bin, block) for the Wiener filter
   DBuf<int> fallbacks;
   DBuf<StageClock> stage;  // device StageSeconds accumulator (dfm_em.cuh)
@@ -392,6 +394,13 @@ void launch_em(dfm_ctx* c, int finish, int start, int slot, double* cost_dst = n
   if (gfuse && c->Ginv.n < (size_t)c->F * c->L.wsz) c->Ginv.alloc((size_t)c->F * c->L.wsz);
   a.Gout = gfuse ? c->Ginv.p : nullptr;
   a.cost_out = cost_dst ? cost_dst : c->cost_part.p + (size_t)slot * c->F;
+  a.cost_slot = nullptr;
+  a.cost_slot_max = 0;
+  if (c->slot_mode) {  // graph replays of a fit (step_graph)
+    a.cost_out = c->cost_part.p;
+    a.cost_slot = c->cost_slot.p;
+    a.cost_slot_max = (int)(c->cost_part.n / (size_t)c->F) - 1;
+  }
   a.trace = c->tracing ? c->trace.p : nullptr;
   a.dbg = c->dbg;
   if (c->cs_em > 1) {  // a cluster of cs_em CTAs per bin
@@ -502,7 +511,8 @@ void launch_vupd(dfm_ctx* c) {
     kern<<<grid, 32 * kVupdMWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->Aw.p, c->Bw.p, c->V.p,
                                                    sharded ? c->numden.p : nullptr, c->floor_, nullptr,
                                                    (sharded || (c->dbg & 4)) ? nullptr : c->H.p, nullptr, 0,
-                                                   c->stage.p);  // H = T V_new fused
+                                                   c->stage.p,  // H = T V_new fused
+                                                   c->slot_mode ? c->cost_slot.p : nullptr);
     DFM_CK_LAUNCH();
     c->launches++;
     return;
@@ -522,7 +532,7 @@ void launch_vupd(dfm_ctx* c) {
     const dim3 gj(grid.x, n1 - n0);
     kern<<<gj, 32 * kVupdMWarps, 0, c->stream>>>(c->F, c->T, c->N, c->K, c->Tf.p, c->Aw.p, c->Bw.p, c->V.p,
                                                  c->numden.p, c->floor_, nullptr, nullptr, nullptr, n0,
-                                                 c->stage.p);
+                                                 c->stage.p, c->slot_mode ? c->cost_slot.p : nullptr);
     DFM_CK_LAUNCH();
     c->launches++;
     DFM_CK(cudaEventRecord(c->ev_chunk[j], c->stream));
@@ -570,7 +580,7 @@ void drop_graph(dfm_ctx* c) {
 }
 
 // Captures one steady-state iteration (k_em_bin finish+start writing the
-// scratch cost slot, then the follow-up kernels -- and, when sharded, the
+// cost slot its device counter names, then the follow-up kernels -- and, when sharded, the
 // NCCL allreduce, k_vapply and H = T V) into a CUDA graph; replays cut the
 // per-launch gaps.
 bool step_graph(dfm_ctx* c) {
@@ -584,10 +594,16 @@ bool step_graph(dfm_ctx* c) {
   cudaGraph_t g = nullptr;
   DFM_CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   const long long l0 = c->launches;
+  // the captured bin kernel writes its per-bin cost into the slot a device
+  // counter names, and the captured V update advances the counter: a fit
+  // replays the graph with no copy of the costs between the replays
+  c->slot_mode = true;
   try {
-    launch_em(c, 2, 1, 0, c->cost_step.p);
+    launch_em(c, 2, 1, 0);
     launch_rest(c, nullptr);
+    c->slot_mode = false;
   } catch (...) {
+    c->slot_mode = false;
     // leave the stream usable: end the capture and drop the partial graph
     cudaGraph_t partial = nullptr;
     cudaStreamEndCapture(c->stream, &partial);
@@ -612,11 +628,11 @@ bool step_graph(dfm_ctx* c) {
 // One steady-state iteration whose per-bin cost lands in cost_step: a graph
 // replay, or the same launches on the stream (with the per-kernel split
 // events when `split` is set).
-void run_step(dfm_ctx* c, bool split) {
+bool run_step(dfm_ctx* c, bool split) {
   if (!split && step_graph(c)) {
     DFM_CK(cudaGraphLaunch(c->step_exec, c->stream));
     c->launches += c->graph_launches;
-    return;
+    return true;  // the cost went to slot *cost_slot + 1 of cost_part
   }
   if (c->cost_step.n < (size_t)c->F) c->cost_step.alloc(c->F);
   if (split) DFM_CK(cudaEventRecord(c->ev[0], c->stream));
@@ -624,6 +640,7 @@ void run_step(dfm_ctx* c, bool split) {
   if (split) DFM_CK(cudaEventRecord(c->ev[1], c->stream));
   launch_rest(c, split ? c->ev : nullptr);
   if (split) DFM_CK(cudaEventRecord(c->ev[5], c->stream));
+  return false;  // the cost is in cost_step
 }
 
 // Wiener separation of the context's bins into the device buffer `img`
@@ -716,6 +733,8 @@ dfm_ctx* dfm_create(int F, int T, int nblocks, const int* block_sizes, int N, in
     if (!choose_tiling(c)) throw CudaError{DFM_ERR_UNSUPPORTED};
     set_kernel_attrs(c);
     ensure_cost(c, 2);
+    c->cost_slot.alloc(1);
+    DFM_CK(cudaMemset(c->cost_slot.p, 0, sizeof(int)));
   } catch (const CudaError&) {
     dfm_destroy(c);
     return nullptr;
@@ -910,6 +929,7 @@ void fit_begin(dfm_ctx* c, int iters) {
   DFM_CK(cudaSetDevice(c->device));
   ensure_cost(c, iters + 1);
   DFM_CK(cudaMemsetAsync(c->fallbacks.p, 0, sizeof(int), c->stream));
+  DFM_CK(cudaMemsetAsync(c->cost_slot.p, 0, sizeof(int), c->stream));  // replay j (1-based) writes slot j
   reset_stage_clock(c);
   while ((int)c->iter_ev.size() < iters + 2) {
     cudaEvent_t e;
@@ -925,9 +945,12 @@ void fit_launch(dfm_ctx* c, int i, int iters) {
     launch_em(c, i == 0 ? 1 : 2, i < iters ? 1 : 0, i);
     if (i < iters) launch_rest(c, nullptr);
   } else {
-    run_step(c, false);  // per-bin cost of iteration i-1 -> cost_step
-    DFM_CK(cudaMemcpyAsync(c->cost_part.p + (size_t)i * c->F, c->cost_step.p, sizeof(double) * c->F,
-                           cudaMemcpyDeviceToDevice, c->stream));
+    // per-bin cost of iteration i-1: a graph replay writes slot i itself
+    // (the fit's device counter holds i - 1), a stream-launched step leaves
+    // it in cost_step
+    if (!run_step(c, false))
+      DFM_CK(cudaMemcpyAsync(c->cost_part.p + (size_t)i * c->F, c->cost_step.p, sizeof(double) * c->F,
+                             cudaMemcpyDeviceToDevice, c->stream));
   }
   if (i == iters) {
     k_stage_close<<<1, 1, 0, c->stream>>>(c->stage.p);  // ends the last launch's StageClock interval

@@ -779,7 +779,7 @@ int is_nmf_dev(const double* h0_dev, int F, int T, int N, int K, int max_iters, 
       default: kern = k_vupd_mma<8>; break;
     }
     kern<<<dim3((T + 7) / 8, N), 32 * kVupdMWarps, 0, s>>>(F, T, N, K, Tf.p, Aw.p, Bw.p, V.p, nullptr, kEpsNmf,
-                                                         done.p, H.p, tgt.p, 0, nullptr);
+                                                         done.p, H.p, tgt.p, 0, nullptr, nullptr);
     DFM_CK_LAUNCH();
   };
   spec();

@@ -22,8 +22,8 @@ for rep in range(4):
     t = [time.perf_counter()]
     eng.set_obs(xs); t.append(time.perf_counter())
     eng.set_model(init.nmf, init.w0, init.lambda0); t.append(time.perf_counter())
-    eng.fit(20); t.append(time.perf_counter())
+    eng.fit(200); t.append(time.perf_counter())
     eng.get_model(); t.append(time.perf_counter())
     d = np.diff(t) * 1e3
-    print(f"set_obs {d[0]:.2f} ms ({xs.nbytes / d[0] / 1e6:.1f} GB/s)  set_model {d[1]:.2f}  fit(20) {d[2]:.2f}  "
+    print(f"set_obs {d[0]:.2f} ms ({xs.nbytes / d[0] / 1e6:.1f} GB/s)  set_model {d[1]:.2f}  fit(200) {d[2]:.2f}  "
           f"get_model {d[3]:.2f}  total {sum(d):.2f} ms")
