@@ -681,3 +681,24 @@ def test_two_cta_cluster_bins_match_oracle(dfm, oracle):
     img = dfm.wiener_block(x, fit.models, fit.spatial).images
     ref_img = oracle.wiener_block(x, sizes, ref)
     assert _rel(img, ref_img) < 1e-6
+
+
+@pytest.mark.parametrize("K", [24, 16])
+def test_v_update_frame_pair_kernel_matches_oracle(dfm, oracle, K):
+    """k_vupd_mma<KT, 2> (16 frames per CTA, a lane loads frame pairs and KT
+    consecutive bases) is selected for even T and K once its grid has two
+    rounds of CTAs per SM: T = 1210 frames (even, not a multiple of 16: the
+    last CTA is ragged) x 8 sources = 608 CTAs.  K = 24 leaves the fourth base
+    tile half empty.  Trajectory against the oracle at the north_star bar and
+    the fitted V within 1e-7."""
+    F, T, sizes, N, iters = 12, 1210, [2, 2], 8, 6
+    layout = dfm.BlockLayout(sizes)
+    x = dfm.generate_mixture(1, F, T, layout.total, N, K, 41)
+    init = dfm.random_init(F, T, layout, N, K, 42)
+    fit = dfm.fit_distributed(x, layout, init, iters, True)
+    ref = oracle.run_engine(x, sizes, _init_dict(init), iters)
+    cost = fit.report.cost_trace
+    assert np.max(np.abs(cost - ref["cost_trace"]) / np.abs(ref["cost_trace"])) < TRAJ_RTOL
+    assert np.all(cost[1:] <= cost[:-1] + 1e-9 * np.abs(cost[:-1]))
+    assert _rel(fit.models[0].V, ref["V"]) < 1e-7
+    assert _rel(fit.models[0].T, ref["T"]) < 1e-7
