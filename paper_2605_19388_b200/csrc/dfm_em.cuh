@@ -1050,7 +1050,14 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
         }
         __syncwarp(qmask);
       };
-      if (nb <= nw) {
+      if constexpr (4 * NB_ <= 32) {
+        // every block's quad in warp 0 (lanes 4 b .. 4 b + 3) under one
+        // compile-time mask: one warp instruction serves all the blocks (a
+        // 4-lane FP64 instruction occupies the pipe like a full one), and the
+        // sweep's code is fetched by one warp per CTA instead of one per block
+        constexpr unsigned qm = 4 * NB_ >= 32 ? 0xffffffffu : ((1u << (4 * NB_)) - 1u);
+        if (iw == 0 && il < 4 * NB_) sweep(il >> 2, qm);
+      } else if (nb <= nw) {
         if (iw < nb && il < 4) sweep(iw, 0xFu);
       } else {
         for (int b = (il >> 2) * nw + iw; b < nb; b += 8 * nw) sweep(b, 0xFu << (il & 28));

@@ -350,13 +350,15 @@ __device__ bool herm_inverse_thread(const cd* qp, cd* qi) {
 template <int MB>
 __device__ bool ip_sweep_quad(cd* W, IpWork<MB>& f, const cd* qb, double floor_, int l, unsigned mask) {
   constexpr int E = MB * (MB + 1) / 2;
-  bool okall = true;
+  // a Q_mu without a Cholesky factor fails the sweep; the quad still runs it
+  // (on whatever Qi holds: every index is data-independent and the results
+  // are discarded), so the quads sharing a warp stay convergent for the
+  // shuffles
+  bool bad = false;
 #pragma unroll
-  for (int mu = 0; mu < MB; ++mu) okall = okall && f.ok[mu];
-  if (!okall) return false;
+  for (int mu = 0; mu < MB; ++mu) bad = bad || !f.ok[mu];
   const bool act = l < MB;
   const int la = act ? l : 0;
-  bool bad = false;
 #pragma unroll 1
   for (int mu = 0; mu < MB; ++mu) {
     const cd* qp = qb + mu * E;
