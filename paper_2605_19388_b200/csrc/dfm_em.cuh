@@ -1022,6 +1022,13 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
       // sweeps run on different warps (schedulers), not all in warp 0
       const int iw = tid >> 5, il = tid & 31, nw = FT >> 5;
       const int l = il & 3;
+      if constexpr (4 * NB_ <= 32) {  // one warp for every (block, mu), as the sweep below
+        if (iw == 0 && il < 4 * NB_ && l < MB_) {
+          const int b = il >> 2;
+          IpWork<MB_>& w = *(IpWork<MB_>*)(smem + sp.ipscr + b * ipscr_bytes<MAXMB>());
+          w.ok[l] = herm_inverse_thread<MB_>(Qsum + a.qofs[b] + l * E, w.Qi[l]) ? 1 : 0;
+        }
+      } else
       for (int b = (il >> 2) * nw + iw; b < nb; b += 8 * nw)
         if (l < MB_) {
           IpWork<MB_>& w = *(IpWork<MB_>*)(smem + sp.ipscr + b * ipscr_bytes<MAXMB>());
