@@ -193,6 +193,10 @@ __device__ __forceinline__ void cl_sync() { cooperative_groups::this_cluster().s
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b);
 
+#ifndef DFM_IP_PACK_LANES
+#define DFM_IP_PACK_LANES 32
+#endif
+constexpr int kIpPackLanes = DFM_IP_PACK_LANES;  // blocks whose IP quads share warp 0 (4 lanes each)
 template <int MB_, int NB_, int NS_, int MAXMB, int CS_ = 1>
 __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 registers
   constexpr bool SB = MB_ > 0 && NB_ > 0;
@@ -1022,7 +1026,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
       // sweeps run on different warps (schedulers), not all in warp 0
       const int iw = tid >> 5, il = tid & 31, nw = FT >> 5;
       const int l = il & 3;
-      if constexpr (4 * NB_ <= 32) {  // one warp for every (block, mu), as the sweep below
+      if constexpr (4 * NB_ <= kIpPackLanes) {  // one warp for every (block, mu), as the sweep below
         if (iw == 0 && il < 4 * NB_ && l < MB_) {
           const int b = il >> 2;
           IpWork<MB_>& w = *(IpWork<MB_>*)(smem + sp.ipscr + b * ipscr_bytes<MAXMB>());
@@ -1036,6 +1040,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
         }
       __syncthreads();
       em_stamp(a, 6);
+      __syncwarp();  // thread 0 rejoins its warp after the stamp (the sweep below runs in warp 0)
       // one quad per (bin, block) system; with at least as many warps as
       // blocks each quad is lanes 0-3 of its own warp and the shuffle mask is
       // the compile-time 0xF (a runtime mask makes every __shfl_sync carry
@@ -1046,7 +1051,8 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
         const cd* qb = Qsum + a.qofs[b];
         const long long c0 = clock64();
         const bool ok = ip_sweep_quad<MB_>(wb, w, qb, floor_, l, qmask);
-        if (a.trace && lead && b == 0 && l == 0) a.trace[f * 16 + 8] = (unsigned long long)(clock64() - c0);
+        const unsigned long long dt = (unsigned long long)(clock64() - c0);  // every lane: no quad leaves the warp's path
+        if (a.trace && lead && b == 0 && l == 0) a.trace[f * 16 + 8] = dt;
         if (!ok && l == 0 && a.trace && lead) atomicAdd(a.trace + f * 16 + 7, 1ull);
         if (!ok && l == 0) {
           // exact path (engine.cpp:47-49: LU, residual test, pinv) from W_old
@@ -1057,7 +1063,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
         }
         __syncwarp(qmask);
       };
-      if constexpr (4 * NB_ <= 32) {
+      if constexpr (4 * NB_ <= kIpPackLanes) {
         // every block's quad in warp 0 (lanes 4 b .. 4 b + 3) under one
         // compile-time mask: one warp instruction serves all the blocks (a
         // 4-lane FP64 instruction occupies the pipe like a full one), and the
