@@ -458,6 +458,8 @@ def main():
     ap.add_argument("--tiling", default="", help="FT,TB override: frame tile of the per-bin kernel and of k_pd")
     ap.add_argument("--batch", type=int, default=0, help="config4: number of mixtures (default 64)")
     ap.add_argument("--no-init", action="store_true", help="skip the initialisation-pipeline measurement")
+    ap.add_argument("--spinup-ms", type=float, default=300.0,
+                    help="untimed steps for this long before the warm-up (GPU out of its idle clocks)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     c = CONFIGS[args.workload]
@@ -527,6 +529,19 @@ def main():
         return lib.dfm_bench_last_ms(ctx)
 
     dfm._capi.check(lib.dfm_prime(ctx))
+    # untimed spin-up before the W warm-up steps: the same steps for a fixed
+    # wall time, so a GPU that was idle (fresh process, fresh box) has left its
+    # idle clocks before anything is timed; every rank runs the same count
+    spin_until = time.perf_counter() + args.spinup_ms * 1e-3
+    spin = 0
+    while time.perf_counter() < spin_until and spin < 4000:
+        step()
+        spin += 1
+    if pg:
+        st = torch.tensor([spin], dtype=torch.int64, device="cuda")
+        pg.all_reduce(st, op=pg.ReduceOp.MAX)
+        for _ in range(int(st.item()) - spin):
+            step()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
