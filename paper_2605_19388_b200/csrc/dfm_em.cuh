@@ -726,7 +726,32 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
         ldet[b] = 2.0 * log_abs_det_serial(MBof(b), Wsm + WOFF(b), scr);
       }
     };
-    if (nfree > 0) {
+    bool quad_ld = false;
+    // (blocks of 3-4 mics; a 2 x 2 system is too small to gain: config 0 k_em_bin 17.1 -> 17.6 us with it)
+    if constexpr (SB && MB_ >= 3 && MB_ <= 4 && 4 * NB_ <= 32) quad_ld = !a.ld_in;
+    if (quad_ld) {
+      if constexpr (SB && MB_ <= 4 && 4 * NB_ <= 32) {
+        // the 4 lanes of a quad of the last warp factor the block's W each
+        // (the same values: no exchange) and solve one column of W^-1 each:
+        // the serial head of that warp's pass B is the LU plus one solve
+        // instead of the LU plus MB_ solves
+        const int il = tid - (FT - 32);
+        if (il >= 0 && il < 4 * NB_ && (il & 3) < MB_) {
+          const int b = il >> 2, l = il & 3;
+          IpWork<MB_>& w = *(IpWork<MB_>*)(smem + sp.ipscr + b * ipscr_bytes<MAXMB>());
+          const cd* wb = Wsm + b * MB_ * MB_;
+#pragma unroll
+          for (int r = 0; r < MB_; ++r) w.Wold[l * MB_ + r] = wb[l * MB_ + r];
+          const double ld = logdet2_inverse_thread<MB_>(wb, w.Winv, l);
+          if (l == 0) ldet[b] = ld;
+          if (a.Gout && lead) {  // G = (W^-1)^H (col-major): this lane's column of W^-1 is a row of G
+            cd* g = a.Gout + (size_t)f * wsz + b * MB_ * MB_;
+#pragma unroll
+            for (int r = 0; r < MB_; ++r) g[r * MB_ + l] = conjg(w.Winv[l * MB_ + r]);
+          }
+        }
+      }
+    } else if (nfree > 0) {
       if (tid >= first_free)
         for (int b = tid - first_free; b < nb; b += nfree) do_logdet(b);
     } else {

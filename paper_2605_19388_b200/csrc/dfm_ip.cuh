@@ -199,7 +199,7 @@ struct IpWork {
 // records a +inf cost, engine.hpp:41-43) and a non-finite inverse, which
 // sends the IP sweep to the exact fallback.
 template <int MB>
-__device__ double logdet2_inverse_thread(const cd* W, cd* Winv) {
+__device__ double logdet2_inverse_thread(const cd* W, cd* Winv, int one_col = -1) {
   cd L[MB][MB];
 #pragma unroll
   for (int r = 0; r < MB; ++r)
@@ -246,8 +246,10 @@ __device__ double logdet2_inverse_thread(const cd* W, cd* Winv) {
 #pragma unroll
       for (int c = k + 1; c < MB; ++c) L[r][c] = L[r][c] - L[r][k] * L[k][c];
   }
+  // one_col >= 0: only that column of the inverse (the lanes of a quad each
+  // factor W redundantly -- no exchange -- and solve one column each)
 #pragma unroll 1
-  for (int col = 0; col < MB; ++col) {
+  for (int col = one_col >= 0 ? one_col : 0; col < (one_col >= 0 ? one_col + 1 : MB); ++col) {
     // the row swaps applied to e_col leave a unit vector: follow its 1
     int pos = col;
 #pragma unroll
