@@ -98,7 +98,7 @@ def peaks():
 class ClockSampler:
     """Samples SM clocks and throttle reasons via NVML during the timed region."""
 
-    def __init__(self, device: int, period_s: float = 0.002):
+    def __init__(self, device: int, period_s: float = 0.0005):
         self.device, self.period, self.samples, self.reasons = device, period_s, [], set()
         self.max_mhz = None
         self._stop = threading.Event()
