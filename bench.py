@@ -100,6 +100,7 @@ class ClockSampler:
 
     def __init__(self, device: int, period_s: float = 0.0005):
         self.device, self.period, self.samples, self.reasons = device, period_s, [], set()
+        self.sample_now = lambda: None
         self.max_mhz = None
         self._stop = threading.Event()
         self._t = None
@@ -119,16 +120,21 @@ class ClockSampler:
                 getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80): "hw_power_brake",
             }
 
+            def once():
+                try:
+                    self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for bit, name in names.items():
+                        if r & bit:
+                            self.reasons.add(name)
+                except Exception:
+                    pass
+
+            self.sample_now = once  # also called by the timing loop itself (short regions)
+
             def run():
                 while not self._stop.is_set():
-                    try:
-                        self.samples.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
-                        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                        for bit, name in names.items():
-                            if r & bit:
-                                self.reasons.add(name)
-                    except Exception:
-                        pass
+                    once()
                     time.sleep(self.period)
 
             self._t = threading.Thread(target=run, daemon=True)
@@ -551,8 +557,10 @@ def main():
     launches0 = eng.launches()
     sampler = ClockSampler(local).start()
     t_ms = []
-    for _ in range(args.steps):
+    for i in range(args.steps):
         t_ms.append(step())
+        if i % 4 == 1:  # between steps (host side; the steps are timed on the device)
+            sampler.sample_now()
     dfm._capi.check(lib.dfm_sync(ctx))
     torch.cuda.synchronize()
     clocks = sampler.stop()
