@@ -268,6 +268,21 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
       LsT[e] = n < N ? Lsm[n * M + m] : 0.0;
     }
   };
+  // pass A's first frame (h and, for frames of <= 16 mics, P) is requested
+  // before Lambda and W are staged: its L2 / DRAM round trip overlaps the
+  // staging and its two barriers instead of following them
+  constexpr int MS0 = SB ? MB_ * NB_ : 1;
+  constexpr bool PF0 = SB && MS0 <= 16;
+  double hn0[kMaxN], pn0[PF0 ? MS0 : 1];
+  const bool early_a = PF0 && a.finish == 2 && tid < Tl;
+  if constexpr (PF0) {
+    if (early_a) {
+#pragma unroll
+      for (int n = 0; n < kMaxN; ++n) hn0[n] = n < N ? __ldg(Hf + n * T + tbeg + tid) : 0.0;
+#pragma unroll
+      for (int m = 0; m < MS0; ++m) pn0[m] = ld_hint(Pf + (size_t)m * T + tbeg + tid, pol_keep);
+    }
+  }
   for (int e = tid; e < N * M; e += FT) Lsm[e] = a.lam[(size_t)f * N * M + e];
   __syncthreads();
   build_lst();
@@ -479,7 +494,14 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     // software pipeline: the next tile's h and P are in flight while this
     // tile is computed and reduced
     double hn[kMaxN], pn[MP];
-    if (tid < Tl) {
+    if constexpr (PF0) {
+      if (early_a) {  // requested at the head of the kernel
+#pragma unroll
+        for (int n = 0; n < kMaxN; ++n) hn[n] = hn0[n];
+#pragma unroll
+        for (int m = 0; m < MP; ++m) pn[m] = pn0[m];
+      }
+    } else if (tid < Tl) {
       load_h(tbeg + tid, hn);
       if constexpr (PF) load_power(tbeg + tid, pn, pol_keep);
     }
