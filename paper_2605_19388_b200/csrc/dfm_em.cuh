@@ -2056,6 +2056,31 @@ __global__ void __launch_bounds__(kWienFT, 512 / kWienFT) k_wiener_ctx(const EmA
   cd* Gs = Ws + wsz;                                             // [wsz]
   double* Ls = (double*)(Gs + wsz);                              // [N][M]
   const int tn = min(kWienFT, T - t0);
+  // frames above 16 mics: the frame's h and samples are requested before W,
+  // G and Lambda are staged, one round trip for both instead of two in turn
+  // (config 3: 2920 -> 2682 us; config 1 measured 90.1 -> 93 us with it, so
+  // small frames load after the barrier -- as k_pdw)
+  constexpr bool EARLYW = SB && MB_ * NB_ > 16;
+  const int t = t0 + tid;
+  const bool act = tid < tn;
+  double h[kMaxN];
+  constexpr int MX = SB ? MB_ * NB_ : 1;
+  cd xv[MX];
+  auto load_frame = [&]() {
+    if (act) {
+#pragma unroll
+      for (int n = 0; n < kMaxN; ++n) h[n] = n < N ? __ldg(a.H + ((size_t)f * N + n) * T + t) : 0.0;
+      if constexpr (SB) {
+        const cd* xt = a.x + ((size_t)f * T + t) * M;
+#pragma unroll
+        for (int m = 0; m < MX; ++m) {
+          const double2 v = __ldg(reinterpret_cast<const double2*>(xt + m));
+          xv[m] = cd{v.x, v.y};
+        }
+      }
+    }
+  };
+  if constexpr (EARLYW) load_frame();
   for (int e = tid; e < wsz; e += kWienFT) Ws[e] = a.W[(size_t)f * wsz + e];
   // (W_b^H)^-1, precomputed once per (bin, block) by launch_wh_inverse
   // (every frame tile of a bin used to repeat the serial inverse while its
@@ -2063,23 +2088,11 @@ __global__ void __launch_bounds__(kWienFT, 512 / kWienFT) k_wiener_ctx(const EmA
   for (int e = tid; e < wsz; e += kWienFT) Gs[e] = G[(size_t)f * wsz + e];
   for (int e = tid; e < N * M; e += kWienFT) Ls[e] = a.lam[(size_t)f * N * M + e];
   __syncthreads();
-  const int t = t0 + tid;
-  const bool act = tid < tn;
-  double h[kMaxN];
-  constexpr int MX = SB ? MB_ * NB_ : 1;
+  if constexpr (!EARLYW) load_frame();
   cd y[MX];
   double eta[MX];
   if (act) {
-#pragma unroll
-    for (int n = 0; n < kMaxN; ++n) h[n] = n < N ? __ldg(a.H + ((size_t)f * N + n) * T + t) : 0.0;
     if constexpr (SB) {
-      const cd* xt = a.x + ((size_t)f * T + t) * M;
-      cd xv[MX];
-#pragma unroll
-      for (int m = 0; m < MX; ++m) {
-        const double2 v = __ldg(reinterpret_cast<const double2*>(xt + m));
-        xv[m] = cd{v.x, v.y};
-      }
 #pragma unroll
       for (int b = 0; b < NB_; ++b)
 #pragma unroll
