@@ -537,17 +537,18 @@ def main():
     dfm._capi.check(lib.dfm_prime(ctx))
     # untimed spin-up before the W warm-up steps: the same steps for a fixed
     # wall time, so a GPU that was idle (fresh process, fresh box) has left its
-    # idle clocks before anything is timed; every rank runs the same count
-    spin_until = time.perf_counter() + args.spinup_ms * 1e-3
-    spin = 0
-    while time.perf_counter() < spin_until and spin < 4000:
-        step()
-        spin += 1
+    # idle clocks before anything is timed
     if pg:
-        st = torch.tensor([spin], dtype=torch.int64, device="cuda")
-        pg.all_reduce(st, op=pg.ReduceOp.MAX)
-        for _ in range(int(st.item()) - spin):
+        # sharded steps hold an allreduce: every rank must run the same number
+        # of them, so the spin-up is a fixed count there, not a wall time
+        for _ in range(100 if args.spinup_ms > 0 else 0):
             step()
+    else:
+        spin_until = time.perf_counter() + args.spinup_ms * 1e-3
+        spin = 0
+        while time.perf_counter() < spin_until and spin < 4000:
+            step()
+            spin += 1
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
