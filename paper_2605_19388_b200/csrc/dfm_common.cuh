@@ -375,10 +375,13 @@ __device__ __forceinline__ cd dot4(int n, const F& term) {
 // s.S, which ends as W^-1); the entry value of W is kept in s.S0.  A zero
 // pivot column (singular W) poisons W^-1(0, 0) with NaN, which sends the
 // sweep to the exact path at its first column.
+// ld2 (optional): 2 ln|det W| from the pivots (the row swaps only change the
+// determinant's sign), -inf for a singular W.
 template <int MB>
-__device__ void ip_winv_warp(int mb, const cd* W, IpScratch<MB>& s) {
+__device__ void ip_winv_warp(int mb, const cd* W, IpScratch<MB>& s, double* ld2 = nullptr) {
   const int lane = threadIdx.x & 31;
   const int n2 = mb * mb;
+  double lacc = 0.0;
   for (int i = lane; i < n2; i += 32) {
     s.S0[i] = W[i];
     s.V[i] = W[i];
@@ -404,9 +407,11 @@ __device__ void ip_winv_warp(int mb, const cd* W, IpScratch<MB>& s) {
     if (!(best > 0.0) || !isfinite(best)) {
       __syncwarp();
       if (lane == 0) s.S[0] = cd{NAN, 0.0};
+      if (ld2 && lane == 0) *ld2 = best == 0.0 ? -INFINITY : NAN;
       __syncwarp();
       return;
     }
+    if (ld2) lacc += log(best);  // |pivot|^2: sum = 2 ln|det|
     const cd p = ck[piv];
     const double ib = rcp_pos(best);
     const cd ip{p.re * ib, -p.im * ib};
@@ -422,6 +427,7 @@ __device__ void ip_winv_warp(int mb, const cd* W, IpScratch<MB>& s) {
     }
     __syncwarp();
   }
+  if (ld2 && lane == 0) *ld2 = lacc;
 }
 
 // Packed Hermitian entry (r, c): the upper triangle is stored, (r, c) with

@@ -748,6 +748,19 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
         ldet[b] = 2.0 * log_abs_det_serial(MBof(b), Wsm + WOFF(b), scr);
       }
     };
+    // blocks above 4 mics (and the generic kernels): one warp forms W_b^-1 by
+    // the lane-parallel Gauss-Jordan the IP phase needs anyway, and 2 ln|det|
+    // from its pivots; the IP phase then finds W_b^-1 in place.  (A single
+    // thread's 12 x 12 LU through shared memory held its whole CTA at the
+    // first tile's barrier for ~30 us.)
+    constexpr bool WARP_LD = !(SB && MB_ <= 4);
+    if constexpr (WARP_LD) {
+      const int wl = tid >> 5, nwl = FT >> 5;
+      if (wl == nwl - 1)
+        for (int b = 0; b < nb; ++b)
+          ip_winv_warp<MAXMB>(MBof(b), Wsm + WOFF(b),
+                              *(IpScratch<MAXMB>*)(smem + sp.ipscr + b * ipscr_bytes<MAXMB>()), &ldet[b]);
+    } else {
     bool quad_ld = false;
     // (blocks of 3-4 mics; a 2 x 2 system is too small to gain: config 0 k_em_bin 17.1 -> 17.6 us with it)
     if constexpr (SB && MB_ >= 3 && MB_ <= 4 && 4 * NB_ <= 32) quad_ld = !a.ld_in;
@@ -779,6 +792,7 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
     } else {
       for (int b = tid; b < nb; b += FT) do_logdet(b);
     }
+    }  // !WARP_LD
   }
   {
     const int FTp = FT + 1;
@@ -1129,12 +1143,10 @@ __global__ void __launch_bounds__(512, 1) k_em_bin(const EmArgs a) {  // <= 128 
       cd* Qinv = (cd*)(smem + sp.red);
       {
         const int nw = sp.nwarps;
-        for (int b = warp; b < nb; b += nw)
-          ip_winv_warp<MAXMB>(MBof(b), Wsm + WOFF(b),
-                              *(IpScratch<MAXMB>*)(smem + sp.ipscr + b * ipscr_bytes<MAXMB>()));
+        // W^-1 of every block is in its IpScratch since the log-det step of pass B
         // each block's Q_mu^-1 in contiguous mu chunks, inverted together; on
         // the warps without a W^-1 task when there are enough of them
-        const int w0 = (nb < nw && nw - nb >= nb) ? nb : 0, nq_w = nw - w0;
+        const int w0 = 0, nq_w = nw - w0;  // every warp takes Q_mu^-1 work (no W^-1 tasks here any more)
         if (warp >= w0)
           for (int b = 0; b < nb; ++b) {
             const int mb = MBof(b), E = mb * (mb + 1) / 2;
